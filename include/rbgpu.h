@@ -1,0 +1,146 @@
+/*
+ * rbgpu.h -- C ABI of the B200 rule-evaluation engine (librbgpu.so).
+ *
+ * Replaces the hot path of the reference package `ruleblock`:
+ *   run_partition  pkg/src/ruleblock/engine.py:619-646
+ *   run_cross      pkg/src/ruleblock/engine.py:649-681 (+ _bipartite_patch 684-719)
+ * together with the per-slot evaluators they compile
+ *   (pkg/src/ruleblock/encode.py:191-324) and the numba kernels they call
+ *   (pkg/src/ruleblock/_kernels.py:29-83).
+ *
+ * Everything above this ABI (rule parsing, planning, text folding and
+ * tokenising, dictionary encoding, exact threshold tables) stays on the
+ * host in Python; everything below it runs on one sm_100a GPU.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Host buffers passed in are read during
+ *    the call and never retained.
+ *  - Every function returns RB_OK (0) or a negative status; the message of
+ *    the last failure on the calling thread is rb_last_error().
+ *  - Handles are owned by the library and freed with their *_destroy.
+ *  - One rb_ctx per (host thread, device); calls on one ctx are serialised
+ *    by the caller.  There is no CPU fallback: without a usable device every
+ *    entry point that needs one fails with RB_ERR_CUDA.
+ */
+#ifndef RBGPU_H
+#define RBGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (mapped by the Python shim: INVALID/LIMIT -> ConfigError,
+ * CUDA/OOM/INTERNAL -> RuleBlockError; engine.py:53-59, 240-245) */
+#define RB_OK 0
+#define RB_ERR_INVALID (-1)
+#define RB_ERR_CUDA (-2)
+#define RB_ERR_OOM (-3)
+#define RB_ERR_LIMIT (-4)
+#define RB_ERR_INTERNAL (-5)
+
+/* column kinds -- relation-wide encodings (encode.py:58-175) */
+#define RB_COL_CODES 0  /* int32 dictionary codes, <0 = never equal      */
+#define RB_COL_MASK 1   /* uint8 per tuple: t.attr = const holds          */
+#define RB_COL_TOKENS 2 /* CSR of sorted unique int32 token ids + missing */
+#define RB_COL_CHARS 3  /* CSR of folded codepoints (u8 or u32) + missing */
+
+/* slot kinds -- one per distinct predicate of the path (encode.py:291-324) */
+#define RB_SLOT_EQ_CODE 0  /* lhs[t] >= 0 && lhs[t] == rhs[s]           */
+#define RB_SLOT_EQ_CONST 1 /* mask[t]  (depends on t only)               */
+#define RB_SLOT_JACCARD 2  /* token-set Jaccard >= delta                 */
+#define RB_SLOT_EXACT 3    /* token sets equal and not both empty        */
+#define RB_SLOT_EDIT 4     /* 1 - lev/max(len) >= delta                  */
+
+#define RB_SLOT_PREFILTER 1u /* engine form with the float length prefilter */
+
+/* run flags (EngineConfig.symmetric_mode / enumerate_witnesses, engine.py:41-51) */
+#define RB_SYMMETRIC 1u
+#define RB_ENUMERATE 2u
+#define RB_STATS 4u /* count per-slot exact evaluations */
+
+#define RB_MAX_SLOTS 64
+#define RB_MAX_CHECKPOINTS 64
+
+/* One predicate slot.  tab0/tab1 index the program's int32 table buffer:
+ *   EDIT:    tab0 = maxgap[0..len0), tab1 = maxd[0..len1)
+ *   JACCARD: tab0 = minsmall[0..len0), tab1 = mink[0..len1)
+ * delta is the predicate threshold (used by the CPU oracle, not the GPU). */
+typedef struct rb_slot {
+    int32_t kind;
+    int32_t lhs; /* column read on the t side */
+    int32_t rhs; /* column read on the s side */
+    int32_t flags;
+    int64_t tab0;
+    int64_t tab1;
+    int32_t len0;
+    int32_t len1;
+    double delta;
+} rb_slot;
+
+typedef struct rb_stats {
+    int64_t comparisons; /* pairs evaluated: BlockStats.comparisons (engine.py:486) */
+    int64_t survivors;   /* pairs that needed the exact interpreter            */
+    int64_t emitted;     /* rows produced                                       */
+    double kernel_ms;    /* device time of the evaluation kernels (CUDA events) */
+    int32_t launches;    /* kernels launched by the run                         */
+    int32_t retries;     /* output-overflow re-runs                              */
+    int64_t slot_evals[RB_MAX_SLOTS]; /* exact evaluations per slot (RB_STATS) */
+} rb_stats;
+
+typedef struct rb_ctx rb_ctx;
+typedef struct rb_rel rb_rel;
+typedef struct rb_prog rb_prog;
+typedef struct rb_result rb_result;
+
+const char* rb_last_error(void);
+const char* rb_version(void);
+
+/* context: device + stream.  rb_ctx_set_stream makes the engine launch on a
+ * caller-owned cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream). */
+int rb_ctx_create(int device, rb_ctx** out);
+int rb_ctx_set_stream(rb_ctx* ctx, void* cuda_stream);
+int rb_ctx_destroy(rb_ctx* ctx);
+
+/* relation: uploaded once, shared by every program/partition over it
+ * (the role of EncodedRelation shared copy-on-write, pipeline.py:273-307) */
+int rb_relation_create(rb_ctx* ctx, int64_t n_tuples, rb_rel** out);
+int rb_relation_add_codes(rb_rel* rel, const int32_t* codes, int32_t* col);
+int rb_relation_add_mask(rb_rel* rel, const uint8_t* mask, int32_t* col);
+int rb_relation_add_tokens(rb_rel* rel, const int64_t* offsets, const int32_t* ids, const uint8_t* missing,
+                           int32_t* col);
+int rb_relation_add_chars(rb_rel* rel, const int64_t* offsets, const void* chars, int32_t width,
+                          const uint8_t* missing, int32_t* col);
+int rb_relation_destroy(rb_rel* rel);
+
+/* program: the compiled ExecutionPath (planner/plan.py:232-300).
+ * op[k] = 0 EvalPredicate(slot[k], fail[k]) | 1 Checkpoint(rule[k]),
+ * rule[k] indexing path.rule_ids (rule-set order). */
+int rb_program_create(rb_ctx* ctx, rb_rel* rel, const int32_t* op, const int32_t* slot, const int32_t* fail,
+                      const int32_t* rule, int32_t n_ins, const rb_slot* slots, int32_t n_slots,
+                      const int32_t* tables, int64_t n_tables, rb_prog** out);
+int rb_program_destroy(rb_prog* prog);
+
+/* run_partition: all pairs of refs[0..n) (i<j symmetric, i!=j otherwise);
+ * t = refs[i] (the lower position), s = refs[j].  refs == NULL means the
+ * identity partition 0..n-1.  Rows are (t, s, rule) with t<s by tid in
+ * symmetric mode.  rb_run_partition_rows restricts the outer position to
+ * [row_lo, row_hi) -- the unit of multi-GPU sharding. */
+int rb_run_partition(rb_ctx* ctx, rb_rel* rel, rb_prog* prog, const int32_t* refs, int64_t n, uint32_t flags,
+                     rb_result** out);
+int rb_run_partition_rows(rb_ctx* ctx, rb_rel* rel, rb_prog* prog, const int32_t* refs, int64_t n,
+                          int64_t row_lo, int64_t row_hi, uint32_t flags, rb_result** out);
+/* run_cross: every (t in left, s in right); t is always the left tuple. */
+int rb_run_cross(rb_ctx* ctx, rb_rel* rel, rb_prog* prog, const int32_t* left, int64_t nl, const int32_t* right,
+                 int64_t nr, uint32_t flags, rb_result** out);
+
+int rb_result_count(const rb_result* res, int64_t* rows);
+int rb_result_copy(const rb_result* res, int32_t* t, int32_t* s, int32_t* rule);
+int rb_result_stats(const rb_result* res, rb_stats* out);
+int rb_result_destroy(rb_result* res);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBGPU_H */
