@@ -1,0 +1,342 @@
+"""Benchmark of the rule-evaluation hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step evaluates every unordered tuple pair of one synthetic 1M-tuple
+citation-style relation (BASELINE config 2: 3 rules mixing equality, token
+Jaccard and edit distance) as ONE partition -- 499,999,500,000
+pairs -- and emits the surviving (t, s, rule) rows.
+
+* value   -- pairs / s over the timed steps, inputs resident in HBM, timed
+             with CUDA events on the stream the engine launches on, max over
+             ranks.  L2 is flushed (a 512 MiB write) between timed steps.
+* e2e     -- the same metric through the C ABI with HOST buffers: every step
+             uploads the encoded relation and the program (H2D), evaluates,
+             and copies the result rows back (D2H).
+* roofline-- SURVEY §8d streaming-bytes model for the pair kernel.
+* cpu_baseline -- the CPU oracle (a C restatement of the reference engine,
+             oracle/rb_oracle.c) on a bounded row sample on this host's cores;
+             the same rows are also checked for bit-exact parity against the GPU.
+
+Multi-GPU (torchrun): weak scaling -- every rank evaluates its own 1M-tuple
+partition (seed + rank), no data-path collective; NCCL only reduces the
+timings and the row counts at the end.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tuple pairs evaluated/sec and blocking wall-time at 1/2/4/8 B200 vs CPU ref"
+UNIT = "pairs/s"
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for k, nm in enumerate(names):
+                if len(f) > 3 + k and f[3 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes_per_pair(enc, path, evals_frac, rows_per_pair):
+    """A = sum_s E_s * b_s + C * 10 B, per pair.  E_s/pairs comes
+    from the oracle's exact first-touch counts on the sample rows."""
+    from paper_2410_04349_b200.encode import SLOT_EDIT, SLOT_EQ_CODE, SLOT_EXACT, SLOT_JACCARD
+
+    total = 0.0
+    terms = {}
+    for s, p in enumerate(path.predicate_table):
+        kind, _, rc, _ = enc.slot_for(p)
+        col = enc.columns[rc]
+        if kind == SLOT_EQ_CODE:
+            b = 4.0
+        elif kind in (SLOT_JACCARD, SLOT_EXACT):
+            b = 4.0 + 4.0 * float(np.diff(col.offsets).mean())
+        elif kind == SLOT_EDIT:
+            b = 4.0 + float(np.diff(col.offsets).mean()) * col.width
+        else:
+            b = 0.0
+        terms[p.describe()] = {"evals_per_pair": float(evals_frac[s]), "bytes": b}
+        total += float(evals_frac[s]) * b
+    return total + 10.0 * rows_per_pair, terms
+
+
+def cpu_sample(w, prog, rows, nthreads):
+    """Oracle on outer rows `rows` (list of (lo, hi)); returns rows, pairs, seconds, evals."""
+    from oracle import oracle
+
+    out, pairs, evals, secs = [], 0, np.zeros(prog.n_slots, dtype=np.int64), 0.0
+    for lo, hi in rows:
+        t0 = time.perf_counter()
+        r, cmp, ev = oracle.run(w.enc, prog, None, w.n, row_lo=lo, row_hi=hi, flags=1, nthreads=nthreads)
+        secs += time.perf_counter() - t0
+        out.append(r)
+        pairs += cmp
+        evals += ev
+    return np.concatenate(out) if out else np.zeros((0, 3), np.int64), pairs, secs, evals
+
+
+def sample_rows(n, budget_pairs, k=8):
+    """k row slices spread over the triangle whose pairs sum to ~budget."""
+    per = max(1, budget_pairs // k)
+    out = []
+    for q in range(k):
+        lo = int(q * n / k)
+        rows = max(1, per // max(1, n - lo - 1))
+        out.append((lo, min(n - 1, lo + rows)))
+    return out
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU engine restated in C (oracle), all
+    host threads, bounded sample per step; rank 0 only."""
+    if rank != 0:
+        return
+    from paper_2410_04349_b200 import synth
+    from paper_2410_04349_b200.encode import compile_program
+
+    w = synth.WORKLOADS[args.workload](args.n, seed=args.seed)
+    prog = compile_program(w.path, w.enc)
+    cores = os.cpu_count() or 1
+    rows = sample_rows(w.n, args.cpu_pairs)
+    for _ in range(args.warmup):
+        cpu_sample(w, prog, rows[:1], cores)
+    pairs = secs = 0
+    for _ in range(args.steps):
+        _, p, s, _ = cpu_sample(w, prog, rows, cores)
+        pairs += p
+        secs += s
+    v = pairs / secs
+    total_pairs = w.n * (w.n - 1) // 2
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"{w.name} n={w.n} (BASELINE config 2), one symmetric partition",
+                   "pairs_per_step_full": total_pairs, "sample_pairs_per_step": pairs // args.steps},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{len(rows)} outer-row slices, {pairs // args.steps} pairs per step; "
+                                   f"full step extrapolates to {total_pairs / v:.0f} s"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "blocking_wall_s_full_extrapolated": total_pairs / v,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="citation3")
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--cpu-pairs", type=int, default=120_000_000, help="oracle sample size (pairs)")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2410_04349_b200 import synth
+    from paper_2410_04349_b200._lib import RB_SYMMETRIC
+    from paper_2410_04349_b200.engine import DeviceRelation, PathProgram, context
+
+    w = synth.WORKLOADS[args.workload](args.n, seed=args.seed + rank)
+    ctx = context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    prog = PathProgram(w.path, w.enc, device=local)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        rows, st = prog.run_raw(None, w.n, RB_SYMMETRIC)
+    n_rows = len(rows[0])
+    pairs_step = int(st.comparisons)
+
+    times, kms = [], []
+    sampler = ClockSampler(local)
+    with sampler:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rows, st = prog.run_raw(None, w.n, RB_SYMMETRIC)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            kms.append(st.kernel_ms)
+            assert st.comparisons == pairs_step and len(rows[0]) == n_rows
+    barrier()
+    t_total = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+    counts = torch.tensor([pairs_step * args.steps, n_rows], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_total, op=dist.ReduceOp.MAX)
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+    ms_step = t_total.item() / args.steps
+    value = counts[0].item() / (t_total.item() / 1e3)
+
+    # ---- e2e: host buffers through the C ABI, copies inside the timed region
+    e2e_steps = args.e2e_steps or max(1, min(args.steps, 3))
+    h2d = sum(c.data.nbytes + (0 if c.offsets is None else c.offsets.nbytes)
+              + (0 if c.missing is None else c.missing.nbytes) for c in w.enc.columns)
+    h2d += prog.program.tables.nbytes + prog.program.slots.nbytes + 4 * 4 * len(prog.program.ins_op)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        drel = DeviceRelation(ctx, w.enc)  # H2D of every encoded column
+        p2 = PathProgram(w.path, w.enc, compiled=prog.program, drel=drel)  # H2D of the program
+        rows2, st2 = p2.run_raw(None, w.n, RB_SYMMETRIC)  # evaluate + D2H of the rows
+        assert len(rows2[0]) == n_rows
+        p2.close()
+        drel.close()
+    torch.cuda.synchronize()
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = counts[0].item() / args.steps / e2e_s.item()
+    d2h = 12 * n_rows + 8 * 68
+
+    # ---- CPU oracle sample (rank 0, N = 1): baseline + parity on the same rows
+    cpu = None
+    parity = None
+    roof = None
+    peak, peak_kind = measured_peak()
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        srows = sample_rows(w.n, args.cpu_pairs)
+        orc_rows, orc_pairs, orc_s, orc_evals = cpu_sample(w, prog.program, srows, cores)
+        cpu = {"value": orc_pairs / orc_s, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{len(srows)} outer-row slices of the same relation, {orc_pairs} pairs "
+                         f"(oracle/rb_oracle.c, OpenMP {cores} threads)"}
+        ok = True
+        for lo, hi in srows:
+            (gt, gs, gr), gst = prog.run_raw(None, w.n, RB_SYMMETRIC, row_lo=lo, row_hi=hi)
+            sel = (orc_rows[:, 0] >= lo) & (orc_rows[:, 0] < hi)
+            want = sorted(map(tuple, orc_rows[sel].tolist()))
+            got = sorted(zip(gt.tolist(), gs.tolist(), gr.tolist()))
+            ok &= want == got
+        parity = {"rows_checked": int(len(orc_rows)), "pairs_checked": int(orc_pairs), "bit_exact": bool(ok)}
+        bpp, terms = algorithmic_bytes_per_pair(w.enc, w.path, orc_evals / max(1, orc_pairs), n_rows / pairs_step)
+        k_ms = float(np.mean(kms))
+        achieved = bpp * pairs_step / (k_ms / 1e3) / 1e9
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tfile):
+            try:
+                traffic = json.load(open(tfile)).get("bytes_per_launch")
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_kind": peak_kind,
+                "model": "SURVEY 8d streaming bytes: sum_s E_s*b_s + 10 B per row; E_s from oracle first-touch counts",
+                "bytes_per_pair": bpp, "kernel_ms": k_ms, "terms": terms}
+
+    clocks = sampler.summary()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"{w.name} n={w.n} per GPU (BASELINE config 2: eq + jaccard + edit, 3 rules), "
+                                   "one symmetric partition per GPU",
+                       "pairs_per_step_per_gpu": pairs_step, "rows_per_step_per_gpu": n_rows,
+                       "l2": "flushed (512 MiB write) between timed steps", "parallelism": f"partition-per-gpu x{world}"},
+            "blocking_wall_s": ms_step / 1e3,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "blocking_wall_s": e2e_s.item()},
+            "roofline": roof, "cpu_baseline": cpu, "parity": parity,
+            "gpu_launches": int(st.launches) * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

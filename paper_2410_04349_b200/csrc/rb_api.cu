@@ -1,0 +1,688 @@
+// rb_api.cu -- the C ABI (include/rbgpu.h): contexts, device-resident
+// relations and programs, run orchestration and results.
+//
+// Host-side work here is bookkeeping only: it copies plain arrays to HBM,
+// derives the phase-1 filter plan from the instruction list (which slots
+// each rule's checkpoint needs: the EVALs whose subtree encloses it,
+// planner/plan.py:269-300), builds the work-item list and launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "rb_internal.cuh"
+
+using namespace rb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                                    \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail(e_ == cudaErrorMemoryAllocation ? RB_ERR_OOM : RB_ERR_CUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t grow(size_t need) {
+        if (need <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t want = std::max(need, (size_t)256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) bytes = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+}  // namespace
+
+struct rb_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 0;
+    int blocks_per_sm = 1;
+    DevBuf items, refs, counters, scratch;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+struct rb_rel {
+    rb_ctx* ctx = nullptr;
+    int64_t n = 0;
+    std::vector<DevColumn> cols;
+    std::vector<int64_t> max_len;
+    std::vector<void*> allocs;
+    void* d_cols = nullptr;
+    bool cols_dirty = true;
+};
+
+struct rb_prog {
+    rb_ctx* ctx = nullptr;
+    rb_rel* rel = nullptr;
+    FilterPlan F{};
+    VerifyProg V{};
+    int32_t n_slots = 0;
+    int64_t lmax_edit = -1;  // longest string any edit slot reads (-1: no edit slot)
+    std::vector<void*> allocs;
+};
+
+struct rb_result {
+    int64_t count = 0;
+    int32_t* d_t = nullptr;
+    int32_t* d_s = nullptr;
+    int32_t* d_r = nullptr;
+    cudaStream_t stream = nullptr;
+    rb_stats stats{};
+};
+
+extern "C" {
+
+const char* rb_last_error(void) { return g_err.c_str(); }
+const char* rb_version(void) { return "rbgpu 0.1 sm_100a"; }
+
+int rb_ctx_create(int device, rb_ctx** out) {
+    if (!out) return fail(RB_ERR_INVALID, "rb_ctx_create: out is NULL");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(RB_ERR_INVALID, "device %d out of range (%d devices)", device, ndev);
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) return fail(RB_ERR_CUDA, "device %d is sm_%d%d; librbgpu is built for sm_100a", device,
+                                     prop.major, prop.minor);
+    rb_ctx* c = new (std::nothrow) rb_ctx();
+    if (!c) return fail(RB_ERR_OOM, "host allocation failed");
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(RB_ERR_CUDA, "context setup: %s", cudaGetErrorString(e));
+    }
+    c->own_stream = true;
+    c->blocks_per_sm = pair_kernel_blocks_per_sm();
+    *out = c;
+    return RB_OK;
+}
+
+int rb_ctx_set_stream(rb_ctx* c, void* stream) {
+    if (!c) return fail(RB_ERR_INVALID, "null ctx");
+    CK(cudaSetDevice(c->device));
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    c->stream = (cudaStream_t)stream;
+    c->own_stream = false;
+    return RB_OK;
+}
+
+int rb_ctx_destroy(rb_ctx* c) {
+    if (!c) return RB_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    c->items.release();
+    c->refs.release();
+    c->counters.release();
+    c->scratch.release();
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return RB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// relation
+
+int rb_relation_create(rb_ctx* c, int64_t n, rb_rel** out) {
+    if (!c || !out) return fail(RB_ERR_INVALID, "rb_relation_create: null argument");
+    if (n < 0 || n > INT32_MAX) return fail(RB_ERR_INVALID, "relation size %lld out of range", (long long)n);
+    rb_rel* r = new (std::nothrow) rb_rel();
+    if (!r) return fail(RB_ERR_OOM, "host allocation failed");
+    r->ctx = c;
+    r->n = n;
+    *out = r;
+    return RB_OK;
+}
+
+static cudaError_t upload(rb_rel* r, const void* src, size_t bytes, void** dst) {
+    *dst = nullptr;
+    if (bytes == 0) bytes = 16;  // never hand out null for an empty array
+    cudaError_t e = cudaMalloc(dst, bytes);
+    if (e != cudaSuccess) return e;
+    r->allocs.push_back(*dst);
+    if (src) return cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, r->ctx->stream);
+    return cudaMemsetAsync(*dst, 0, bytes, r->ctx->stream);
+}
+
+static int add_column(rb_rel* r, const DevColumn& dc, int64_t max_len, int32_t* col) {
+    if ((int)r->cols.size() >= MAX_COLS) return fail(RB_ERR_LIMIT, "relation has more than %d columns", MAX_COLS);
+    r->cols.push_back(dc);
+    r->max_len.push_back(max_len);
+    r->cols_dirty = true;
+    if (col) *col = (int32_t)r->cols.size() - 1;
+    return RB_OK;
+}
+
+int rb_relation_add_codes(rb_rel* r, const int32_t* codes, int32_t* col) {
+    if (!r || (!codes && r->n)) return fail(RB_ERR_INVALID, "rb_relation_add_codes: null argument");
+    CK(cudaSetDevice(r->ctx->device));
+    DevColumn dc{};
+    dc.kind = RB_COL_CODES;
+    void* p;
+    CK(upload(r, codes, sizeof(int32_t) * r->n, &p));
+    dc.codes = (const int32_t*)p;
+    return add_column(r, dc, 0, col);
+}
+
+int rb_relation_add_mask(rb_rel* r, const uint8_t* mask, int32_t* col) {
+    if (!r || (!mask && r->n)) return fail(RB_ERR_INVALID, "rb_relation_add_mask: null argument");
+    CK(cudaSetDevice(r->ctx->device));
+    DevColumn dc{};
+    dc.kind = RB_COL_MASK;
+    void* p;
+    CK(upload(r, mask, r->n, &p));
+    dc.mask = (const uint8_t*)p;
+    return add_column(r, dc, 0, col);
+}
+
+static int check_offsets(const int64_t* offsets, int64_t n, int64_t* max_len) {
+    if (offsets[0] != 0) return fail(RB_ERR_INVALID, "offsets[0] must be 0");
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; i++) {
+        int64_t l = offsets[i + 1] - offsets[i];
+        if (l < 0) return fail(RB_ERR_INVALID, "offsets not monotone at row %lld", (long long)i);
+        m = std::max(m, l);
+    }
+    if (m > INT32_MAX / 2) return fail(RB_ERR_LIMIT, "row of %lld elements is too long", (long long)m);
+    *max_len = m;
+    return RB_OK;
+}
+
+int rb_relation_add_tokens(rb_rel* r, const int64_t* offsets, const int32_t* ids, const uint8_t* missing,
+                           int32_t* col) {
+    if (!r || !offsets) return fail(RB_ERR_INVALID, "rb_relation_add_tokens: null argument");
+    int64_t max_len;
+    if (int rc = check_offsets(offsets, r->n, &max_len)) return rc;
+    const int64_t nnz = offsets[r->n];
+    if (nnz && !ids) return fail(RB_ERR_INVALID, "rb_relation_add_tokens: ids is NULL");
+    CK(cudaSetDevice(r->ctx->device));
+    DevColumn dc{};
+    dc.kind = RB_COL_TOKENS;
+    void *d_off, *d_ids, *d_miss = nullptr, *d_len, *d_sig, *d_hash;
+    CK(upload(r, offsets, sizeof(int64_t) * (r->n + 1), &d_off));
+    CK(upload(r, ids, sizeof(int32_t) * nnz, &d_ids));
+    if (missing) CK(upload(r, missing, r->n, &d_miss));
+    CK(upload(r, nullptr, sizeof(int32_t) * r->n, &d_len));
+    CK(upload(r, nullptr, sizeof(uint4) * r->n, &d_sig));
+    CK(upload(r, nullptr, sizeof(uint2) * r->n, &d_hash));
+    CK(launch_token_features((const int64_t*)d_off, (const int32_t*)d_ids, (const uint8_t*)d_miss, r->n,
+                             (int32_t*)d_len, (uint4*)d_sig, (uint2*)d_hash, r->ctx->stream));
+    dc.offsets = (const int64_t*)d_off;
+    dc.data = d_ids;
+    dc.len = (const int32_t*)d_len;
+    dc.sig = (const uint4*)d_sig;
+    dc.hash = (const uint2*)d_hash;
+    return add_column(r, dc, max_len, col);
+}
+
+int rb_relation_add_chars(rb_rel* r, const int64_t* offsets, const void* chars, int32_t width,
+                          const uint8_t* missing, int32_t* col) {
+    if (!r || !offsets) return fail(RB_ERR_INVALID, "rb_relation_add_chars: null argument");
+    if (width != 1 && width != 4) return fail(RB_ERR_INVALID, "char width must be 1 or 4, got %d", width);
+    int64_t max_len;
+    if (int rc = check_offsets(offsets, r->n, &max_len)) return rc;
+    const int64_t nnz = offsets[r->n];
+    if (nnz && !chars) return fail(RB_ERR_INVALID, "rb_relation_add_chars: chars is NULL");
+    CK(cudaSetDevice(r->ctx->device));
+    DevColumn dc{};
+    dc.kind = RB_COL_CHARS;
+    dc.width = width;
+    void *d_off, *d_chars, *d_miss = nullptr, *d_len, *d_bag;
+    CK(upload(r, offsets, sizeof(int64_t) * (r->n + 1), &d_off));
+    CK(upload(r, chars, (size_t)width * nnz, &d_chars));
+    if (missing) CK(upload(r, missing, r->n, &d_miss));
+    CK(upload(r, nullptr, sizeof(int32_t) * r->n, &d_len));
+    CK(upload(r, nullptr, sizeof(uint4) * r->n, &d_bag));
+    CK(launch_char_features((const int64_t*)d_off, d_chars, width, (const uint8_t*)d_miss, r->n, (int32_t*)d_len,
+                            (uint4*)d_bag, r->ctx->stream));
+    dc.offsets = (const int64_t*)d_off;
+    dc.data = d_chars;
+    dc.len = (const int32_t*)d_len;
+    dc.bag = (const uint4*)d_bag;
+    return add_column(r, dc, max_len, col);
+}
+
+int rb_relation_destroy(rb_rel* r) {
+    if (!r) return RB_OK;
+    cudaSetDevice(r->ctx->device);
+    cudaStreamSynchronize(r->ctx->stream);
+    for (void* p : r->allocs) cudaFree(p);
+    if (r->d_cols) cudaFree(r->d_cols);
+    delete r;
+    return RB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// program
+
+int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* slot, const int32_t* failj,
+                      const int32_t* rule, int32_t n_ins, const rb_slot* slots, int32_t n_slots,
+                      const int32_t* tables, int64_t n_tables, rb_prog** out) {
+    if (!c || !rel || !out || (n_ins && (!op || !slot || !failj || !rule)) || (n_slots && !slots))
+        return fail(RB_ERR_INVALID, "rb_program_create: null argument");
+    if (rel->ctx != c) return fail(RB_ERR_INVALID, "relation belongs to another context");
+    if (n_slots > RB_MAX_SLOTS) return fail(RB_ERR_LIMIT, "%d slots exceed the limit of %d", n_slots, RB_MAX_SLOTS);
+    if (n_tables < 0 || (n_tables && !tables)) return fail(RB_ERR_INVALID, "bad table buffer");
+    const int ncols = (int)rel->cols.size();
+
+    // ---- validate slots
+    for (int s = 0; s < n_slots; s++) {
+        const rb_slot& sl = slots[s];
+        if (sl.lhs < 0 || sl.lhs >= ncols || sl.rhs < 0 || sl.rhs >= ncols)
+            return fail(RB_ERR_INVALID, "slot %d: column out of range", s);
+        const int kl = rel->cols[sl.lhs].kind, kr = rel->cols[sl.rhs].kind;
+        bool ok = false;
+        switch (sl.kind) {
+            case RB_SLOT_EQ_CODE: ok = kl == RB_COL_CODES && kr == RB_COL_CODES; break;
+            case RB_SLOT_EQ_CONST: ok = kl == RB_COL_MASK; break;
+            case RB_SLOT_JACCARD:
+            case RB_SLOT_EXACT: ok = kl == RB_COL_TOKENS && kr == RB_COL_TOKENS; break;
+            case RB_SLOT_EDIT: ok = kl == RB_COL_CHARS && kr == RB_COL_CHARS; break;
+            default: return fail(RB_ERR_INVALID, "slot %d: unknown kind %d", s, sl.kind);
+        }
+        if (!ok) return fail(RB_ERR_INVALID, "slot %d: column kinds do not fit slot kind %d", s, sl.kind);
+        if (sl.kind == RB_SLOT_JACCARD || sl.kind == RB_SLOT_EDIT) {
+            if (sl.tab0 < 0 || sl.tab1 < 0 || sl.len0 < 1 || sl.len1 < 1 || sl.tab0 + sl.len0 > n_tables ||
+                sl.tab1 + sl.len1 > n_tables)
+                return fail(RB_ERR_INVALID, "slot %d: table range outside the table buffer", s);
+            const int64_t lm = std::max(rel->max_len[sl.lhs], rel->max_len[sl.rhs]);
+            const int64_t need0 = lm + 1, need1 = sl.kind == RB_SLOT_EDIT ? lm + 1 : 2 * lm + 1;
+            if (sl.len0 < need0 || sl.len1 < need1)
+                return fail(RB_ERR_INVALID, "slot %d: tables cover lengths < %lld", s, (long long)lm);
+        }
+    }
+
+    // ---- instructions: checkpoint ordinals and each rule's needed slots
+    std::vector<int4> ins(std::max(n_ins, 1));
+    std::vector<int32_t> cp_rule(MAX_RULES, 0);
+    std::vector<uint64_t> need;
+    for (int k = 0; k < n_ins; k++) {
+        if (op[k] == 1) {
+            if ((int)need.size() >= MAX_RULES)
+                return fail(RB_ERR_LIMIT, "more than %d checkpoints in the path", MAX_RULES);
+            if (rule[k] < 0) return fail(RB_ERR_INVALID, "instruction %d: bad rule index", k);
+            uint64_t m = 0;
+            for (int p = 0; p < k; p++)
+                if (op[p] == 0 && failj[p] > k) m |= 1ull << slot[p];
+            cp_rule[need.size()] = rule[k];
+            ins[k] = make_int4(1, (int)need.size(), -1, rule[k]);
+            need.push_back(m);
+        } else if (op[k] == 0) {
+            if (slot[k] < 0 || slot[k] >= n_slots) return fail(RB_ERR_INVALID, "instruction %d: bad slot", k);
+            if (failj[k] <= k || failj[k] > n_ins) return fail(RB_ERR_INVALID, "instruction %d: bad fail_jump", k);
+            ins[k] = make_int4(0, slot[k], failj[k], -1);
+        } else {
+            return fail(RB_ERR_INVALID, "instruction %d: bad op %d", k, op[k]);
+        }
+    }
+
+    CK(cudaSetDevice(c->device));
+    rb_prog* P = new (std::nothrow) rb_prog();
+    if (!P) return fail(RB_ERR_OOM, "host allocation failed");
+    P->ctx = c;
+    P->rel = rel;
+    P->n_slots = n_slots;
+    auto up = [&](const void* src, size_t bytes, void** dst) -> cudaError_t {
+        *dst = nullptr;
+        cudaError_t e = cudaMalloc(dst, std::max(bytes, (size_t)16));
+        if (e != cudaSuccess) return e;
+        P->allocs.push_back(*dst);
+        return cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
+    };
+    auto bail = [&](cudaError_t e) {
+        for (void* p : P->allocs) cudaFree(p);
+        delete P;
+        return fail(e == cudaErrorMemoryAllocation ? RB_ERR_OOM : RB_ERR_CUDA, "program upload: %s",
+                    cudaGetErrorString(e));
+    };
+    void *d_ins, *d_slots, *d_tables, *d_cp, *d_cols;
+    cudaError_t e;
+    if ((e = up(ins.data(), sizeof(int4) * ins.size(), &d_ins))) return bail(e);
+    if ((e = up(cp_rule.data(), sizeof(int32_t) * cp_rule.size(), &d_cp))) return bail(e);
+    std::vector<int32_t> tab(tables ? tables : (const int32_t*)nullptr,
+                             tables ? tables + n_tables : (const int32_t*)nullptr);
+    if (tab.empty()) tab.push_back(0);
+    if ((e = up(tab.data(), sizeof(int32_t) * tab.size(), &d_tables))) return bail(e);
+    const int32_t* T = (const int32_t*)d_tables;
+    std::vector<DevSlot> ds(std::max(n_slots, 1));
+    for (int s = 0; s < n_slots; s++) {
+        const rb_slot& sl = slots[s];
+        ds[s] = DevSlot{sl.kind, sl.lhs, sl.rhs, sl.flags, T + sl.tab0, T + sl.tab1, sl.len0, sl.len1};
+        if (sl.kind == RB_SLOT_EDIT)
+            P->lmax_edit = std::max<int64_t>(P->lmax_edit, std::max(rel->max_len[sl.lhs], rel->max_len[sl.rhs]));
+    }
+    if ((e = up(ds.data(), sizeof(DevSlot) * ds.size(), &d_slots))) return bail(e);
+    if ((e = up(rel->cols.data(), sizeof(DevColumn) * rel->cols.size(), &d_cols))) return bail(e);
+
+    // ---- phase-1 filter plan
+    FilterPlan& F = P->F;
+    memset(&F, 0, sizeof F);
+    F.n_rules = (int)need.size();
+    for (size_t r = 0; r < need.size(); r++) F.need[r] = need[r];
+    auto rules_with = [&](uint64_t slot_bits) {
+        uint64_t m = 0;
+        for (size_t r = 0; r < need.size(); r++)
+            if (need[r] & slot_bits) m |= 1ull << r;
+        return m;
+    };
+    std::map<std::pair<int, int>, int> eqf, tokf, strf;
+    std::map<int, int> constf;
+    for (int s = 0; s < n_slots; s++) {
+        const rb_slot& sl = slots[s];
+        const uint64_t bit = 1ull << s;
+        const DevColumn& L = rel->cols[sl.lhs];
+        const DevColumn& R = rel->cols[sl.rhs];
+        const auto key = std::make_pair(sl.lhs, sl.rhs);
+        if (sl.kind == RB_SLOT_EQ_CODE) {
+            auto it = eqf.find(key);
+            int f;
+            if (it != eqf.end()) {
+                f = it->second;
+            } else {
+                if (F.n_eq >= MAX_EQ) continue;  // left unfiltered: stays "maybe"
+                f = eqf[key] = F.n_eq++;
+                F.eq_outer[f] = L.codes;
+                F.eq_inner[f] = R.codes;
+            }
+            F.eq_slots[f] |= bit;
+        } else if (sl.kind == RB_SLOT_EQ_CONST) {
+            auto it = constf.find(sl.lhs);
+            int f;
+            if (it != constf.end()) {
+                f = it->second;
+            } else {
+                if (F.n_const >= MAX_CONST) continue;
+                f = constf[sl.lhs] = F.n_const++;
+                F.const_mask[f] = L.mask;
+            }
+            F.const_slots[f] |= bit;
+        } else if (sl.kind == RB_SLOT_JACCARD || sl.kind == RB_SLOT_EXACT) {
+            auto it = tokf.find(key);
+            int f;
+            if (it != tokf.end()) {
+                f = it->second;
+            } else {
+                if (F.n_tok >= MAX_TOK) continue;
+                f = tokf[key] = F.n_tok++;
+                F.tok_ooff[f] = L.offsets;
+                F.tok_oids[f] = (const int32_t*)L.data;
+                F.tok_olen[f] = L.len;
+                F.tok_ohash[f] = L.hash;
+                F.tok_ilen[f] = R.len;
+                F.tok_isig[f] = R.sig;
+                F.tok_ihash[f] = R.hash;
+            }
+            if (F.tok_nslots[f] >= MAX_FSLOTS) continue;
+            TokSlotF& ts = F.tok_slot[f][F.tok_nslots[f]++];
+            ts.kind = sl.kind;
+            ts.bit = s;
+            ts.tab0 = T + sl.tab0;
+            ts.tab1 = T + sl.tab1;
+            ts.len0 = sl.kind == RB_SLOT_JACCARD ? sl.len0 : 0;
+            ts.len1 = sl.kind == RB_SLOT_JACCARD ? sl.len1 : 0;
+            F.tok_rules[f] |= rules_with(bit);
+        } else if (sl.kind == RB_SLOT_EDIT) {
+            auto it = strf.find(key);
+            int f;
+            if (it != strf.end()) {
+                f = it->second;
+            } else {
+                if (F.n_str >= MAX_STR) continue;
+                f = strf[key] = F.n_str++;
+                F.str_olen[f] = L.len;
+                F.str_obag[f] = L.bag;
+                F.str_ilen[f] = R.len;
+                F.str_ibag[f] = R.bag;
+            }
+            if (F.str_nslots[f] >= MAX_FSLOTS) continue;
+            StrSlotF& ss = F.str_slot[f][F.str_nslots[f]++];
+            ss.bit = s;
+            ss.maxgap = T + sl.tab0;
+            ss.maxd = T + sl.tab1;
+            ss.len0 = sl.len0;
+            ss.len1 = sl.len1;
+            F.str_rules[f] |= rules_with(bit);
+        }
+    }
+    P->V.ins = (const int4*)d_ins;
+    P->V.slots = (const DevSlot*)d_slots;
+    P->V.cols = (const DevColumn*)d_cols;
+    P->V.cp_rule = (const int32_t*)d_cp;
+    P->V.n_ins = n_ins;
+    P->V.n_slots = n_slots;
+    if ((e = cudaStreamSynchronize(c->stream))) return bail(e);
+    *out = P;
+    return RB_OK;
+}
+
+int rb_program_destroy(rb_prog* P) {
+    if (!P) return RB_OK;
+    cudaSetDevice(P->ctx->device);
+    cudaStreamSynchronize(P->ctx->stream);
+    for (void* p : P->allocs) cudaFree(p);
+    delete P;
+    return RB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// runs
+
+static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t n, int64_t split, int64_t row_lo,
+               int64_t row_hi, uint32_t flags, rb_result** out) {
+    if (!c || !rel || !P || !out) return fail(RB_ERR_INVALID, "run: null argument");
+    if (P->rel != rel || rel->ctx != c) return fail(RB_ERR_INVALID, "run: program/relation/context mismatch");
+    if (n < 0 || n > INT32_MAX) return fail(RB_ERR_INVALID, "run: partition size out of range");
+    if (refs) {
+        for (int64_t k = 0; k < n; k++)
+            if (refs[k] < 0 || refs[k] >= rel->n)
+                return fail(RB_ERR_INVALID, "tuple ref %d at position %lld outside the relation",
+                            refs[k], (long long)k);
+    } else if (n > rel->n) {
+        return fail(RB_ERR_INVALID, "identity partition of %lld tuples exceeds the relation", (long long)n);
+    }
+    *out = nullptr;
+    CK(cudaSetDevice(c->device));
+    rb_result* res = new (std::nothrow) rb_result();
+    if (!res) return fail(RB_ERR_OOM, "host allocation failed");
+    res->stream = c->stream;
+    auto cleanup = [&](int rc) {
+        if (res->d_t) cudaFree(res->d_t);
+        if (res->d_s) cudaFree(res->d_s);
+        if (res->d_r) cudaFree(res->d_r);
+        delete res;
+        return rc;
+    };
+
+    const int32_t mode = split >= 0 ? MODE_CROSS : ((flags & RB_SYMMETRIC) ? MODE_SYM : MODE_ASYM);
+    row_lo = std::max<int64_t>(0, row_lo);
+    row_hi = std::min<int64_t>(row_hi, split >= 0 ? split : n);
+
+    // ---- work items: BLOCK outer rows x CHUNK inner columns
+    std::vector<int4> items;
+    for (int64_t r0 = row_lo; r0 < row_hi; r0 += BLOCK) {
+        const int64_t rhi = std::min<int64_t>(r0 + BLOCK, row_hi);
+        int64_t c0 = mode == MODE_CROSS ? split : (mode == MODE_SYM ? r0 + 1 : 0);
+        for (; c0 < n; c0 += CHUNK)
+            items.push_back(make_int4((int)r0, (int)c0, (int)std::min<int64_t>(c0 + CHUNK, n), (int)rhi));
+    }
+    const int n_items = (int)items.size();
+    if (n_items == 0) {
+        *out = res;
+        return RB_OK;
+    }
+
+    if (cudaError_t e = c->items.grow(sizeof(int4) * items.size())) return cleanup(fail(RB_ERR_CUDA, "items: %s", cudaGetErrorString(e)));
+    if (refs)
+        if (cudaError_t e = c->refs.grow(sizeof(int32_t) * n)) return cleanup(fail(RB_ERR_CUDA, "refs: %s", cudaGetErrorString(e)));
+    // counters: [0] item counter (u32, padded), [1] out_count, [2] pairs, [3] survivors, [4..68) slot evals
+    const size_t n_counters = 4 + RB_MAX_SLOTS;
+    if (cudaError_t e = c->counters.grow(sizeof(unsigned long long) * n_counters))
+        return cleanup(fail(RB_ERR_CUDA, "counters: %s", cudaGetErrorString(e)));
+
+    const int grid = std::max(1, std::min(n_items, c->sm_count * c->blocks_per_sm));
+    int64_t stride = 0;
+    if (P->lmax_edit >= 0) {
+        stride = (P->lmax_edit + 2 + 31) & ~(int64_t)31;
+        if (cudaError_t e = c->scratch.grow(sizeof(int32_t) * stride * (size_t)grid * BLOCK))
+            return cleanup(fail(RB_ERR_OOM, "edit scratch (%lld B): %s",
+                                (long long)(sizeof(int32_t) * stride * (size_t)grid * BLOCK), cudaGetErrorString(e)));
+    }
+
+    CK(cudaMemcpyAsync(c->items.p, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice, c->stream));
+    if (refs) CK(cudaMemcpyAsync(c->refs.p, refs, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+
+    long long cap = 1 << 16;
+    unsigned long long* ctr = (unsigned long long*)c->counters.p;
+    for (int attempt = 0;; attempt++) {
+        res->d_t = nullptr;
+        res->d_s = nullptr;
+        res->d_r = nullptr;
+        cudaError_t e = cudaMalloc(&res->d_t, sizeof(int32_t) * cap);
+        if (!e) e = cudaMalloc(&res->d_s, sizeof(int32_t) * cap);
+        if (!e) e = cudaMalloc(&res->d_r, sizeof(int32_t) * cap);
+        if (e) return cleanup(fail(RB_ERR_OOM, "output buffer of %lld rows: %s", cap, cudaGetErrorString(e)));
+        CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * n_counters, c->stream));
+
+        RunParams R{};
+        R.refs = refs ? (const int32_t*)c->refs.p : nullptr;
+        R.n = n;
+        R.mode = mode;
+        R.flags = flags;
+        R.items = (const int4*)c->items.p;
+        R.n_items = n_items;
+        R.item_counter = (unsigned int*)&ctr[0];
+        R.out_t = res->d_t;
+        R.out_s = res->d_s;
+        R.out_r = res->d_r;
+        R.out_count = &ctr[1];
+        R.cap = cap;
+        R.stat_pairs = &ctr[2];
+        R.stat_surv = &ctr[3];
+        R.slot_evals = &ctr[4];
+        R.scratch = (int32_t*)c->scratch.p;
+        R.scratch_stride = stride;
+
+        CK(cudaEventRecord(c->ev0, c->stream));
+        e = launch_pair_kernel(P->F, P->V, R, grid, c->stream);
+        if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel launch: %s", cudaGetErrorString(e)));
+        CK(cudaEventRecord(c->ev1, c->stream));
+        unsigned long long host_ctr[n_counters];
+        CK(cudaMemcpyAsync(host_ctr, ctr, sizeof host_ctr, cudaMemcpyDeviceToHost, c->stream));
+        e = cudaStreamSynchronize(c->stream);
+        if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel: %s", cudaGetErrorString(e)));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+        res->stats.kernel_ms += ms;
+        res->stats.launches += 1;
+        const long long rows = (long long)host_ctr[1];
+        if (rows <= cap) {
+            res->count = rows;
+            res->stats.comparisons = (int64_t)host_ctr[2];
+            res->stats.survivors = (int64_t)host_ctr[3];
+            res->stats.emitted = rows;
+            res->stats.retries = attempt;
+            for (int s = 0; s < RB_MAX_SLOTS; s++) res->stats.slot_evals[s] = (int64_t)host_ctr[4 + s];
+            break;
+        }
+        cudaFree(res->d_t);
+        cudaFree(res->d_s);
+        cudaFree(res->d_r);
+        cap = rows;
+    }
+    *out = res;
+    return RB_OK;
+}
+
+int rb_run_partition(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t n, uint32_t flags,
+                     rb_result** out) {
+    return run(c, rel, P, refs, n, -1, 0, n, flags, out);
+}
+
+int rb_run_partition_rows(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t n, int64_t row_lo,
+                          int64_t row_hi, uint32_t flags, rb_result** out) {
+    return run(c, rel, P, refs, n, -1, row_lo, row_hi, flags, out);
+}
+
+int rb_run_cross(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* left, int64_t nl, const int32_t* right,
+                 int64_t nr, uint32_t flags, rb_result** out) {
+    if ((nl && !left) || (nr && !right) || nl < 0 || nr < 0) return fail(RB_ERR_INVALID, "rb_run_cross: bad refs");
+    std::vector<int32_t> both((size_t)(nl + nr));
+    if (nl) memcpy(both.data(), left, sizeof(int32_t) * nl);
+    if (nr) memcpy(both.data() + nl, right, sizeof(int32_t) * nr);
+    return run(c, rel, P, both.data(), nl + nr, nl, 0, nl, flags, out);
+}
+
+int rb_result_count(const rb_result* r, int64_t* rows) {
+    if (!r || !rows) return fail(RB_ERR_INVALID, "rb_result_count: null argument");
+    *rows = r->count;
+    return RB_OK;
+}
+
+int rb_result_copy(const rb_result* r, int32_t* t, int32_t* s, int32_t* rule) {
+    if (!r) return fail(RB_ERR_INVALID, "rb_result_copy: null result");
+    if (r->count == 0) return RB_OK;
+    if (!t || !s || !rule) return fail(RB_ERR_INVALID, "rb_result_copy: null output array");
+    const size_t bytes = sizeof(int32_t) * r->count;
+    CK(cudaMemcpyAsync(t, r->d_t, bytes, cudaMemcpyDeviceToHost, r->stream));
+    CK(cudaMemcpyAsync(s, r->d_s, bytes, cudaMemcpyDeviceToHost, r->stream));
+    CK(cudaMemcpyAsync(rule, r->d_r, bytes, cudaMemcpyDeviceToHost, r->stream));
+    CK(cudaStreamSynchronize(r->stream));
+    return RB_OK;
+}
+
+int rb_result_stats(const rb_result* r, rb_stats* out) {
+    if (!r || !out) return fail(RB_ERR_INVALID, "rb_result_stats: null argument");
+    *out = r->stats;
+    return RB_OK;
+}
+
+int rb_result_destroy(rb_result* r) {
+    if (!r) return RB_OK;
+    if (r->d_t) cudaFree(r->d_t);
+    if (r->d_s) cudaFree(r->d_s);
+    if (r->d_r) cudaFree(r->d_r);
+    delete r;
+    return RB_OK;
+}
+
+}  // extern "C"

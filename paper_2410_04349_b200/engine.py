@@ -1,0 +1,415 @@
+"""Drop-in replacement of the reference engine's public entry points.
+
+Same names, arguments, return types and error classes as
+``ruleblock.engine`` (pkg/src/ruleblock/engine.py:41-62, 287-335, 342-368,
+619-681); the evaluation itself runs in librbgpu.so on one sm_100a GPU.
+
+What maps to what:
+
+* ``EngineConfig`` -- same fields and validation (engine.py:41-62).
+  ``symmetric_mode`` and ``enumerate_witnesses`` change results; the
+  scheduling knobs (n_t, n_w, lanes_per_block, num_blocks, stealing,
+  buffer_half_capacity, chunk_size) never changed results in the reference
+  (engine.py:323-333 test) and are accepted for compatibility: on the GPU the
+  schedule is persistent CTAs pulling (row block x column chunk) items from
+  an atomic counter.
+* ``PathProgram`` -- the path compiled against one encoding, here also
+  resident on the device (instructions, slot descriptors, exact tables).
+* ``run_partition`` / ``run_cross`` -- one kernel launch each; results are
+  deduplicated like ``_dedup_witnesses`` (engine.py:600-616).
+"""
+
+from __future__ import annotations
+
+import os
+import threading
+import time
+import weakref
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import RB_ENUMERATE, RB_STATS, RB_SYMMETRIC, check, i32, lib, ptr
+from .encode import COL_CHARS, COL_CODES, COL_MASK, COL_TOKENS, Encoded, RelationEncoding, compile_program
+from .errors import ConfigError, SchemaError
+
+STEALING_MODES = ("off", "inter", "inter+intra")
+
+
+@dataclass
+class EngineConfig:
+    n_t: int = 256
+    n_w: int = 1024
+    lanes_per_block: int = 32
+    num_blocks: Optional[int] = None
+    symmetric_mode: bool = True
+    stealing: str = "inter+intra"
+    buffer_half_capacity: int = 4096
+    chunk_size: int = 4096
+    enumerate_witnesses: bool = False
+    device_stats: bool = True  # per-slot exact-evaluation counters (RB_STATS)
+
+    def __post_init__(self) -> None:
+        if self.n_t < 1 or self.n_w < 1 or self.lanes_per_block < 1:
+            raise ConfigError("n_t, n_w and lanes_per_block must all be >= 1")
+        if self.stealing not in STEALING_MODES:
+            raise ConfigError(f"stealing must be one of {STEALING_MODES}, got {self.stealing!r}")
+        if self.buffer_half_capacity < 1 or self.chunk_size < 1:
+            raise ConfigError("buffer_half_capacity and chunk_size must be >= 1")
+
+    def resolved_blocks(self) -> int:
+        return self.num_blocks if self.num_blocks else (os.cpu_count() or 1)
+
+    def flags(self) -> int:
+        f = RB_SYMMETRIC if self.symmetric_mode else 0
+        if self.enumerate_witnesses:
+            f |= RB_ENUMERATE
+        if self.device_stats:
+            f |= RB_STATS
+        return f
+
+
+@dataclass
+class BlockStats:
+    block_id: int
+    intervals_processed: int = 0
+    intervals_stolen: int = 0
+    range_steals: int = 0
+    comparisons: int = 0
+    index_jumps: int = 0
+    busy_s: float = 0.0
+    slot_evals: Optional[np.ndarray] = None
+    emitted: int = 0
+    survivors: int = 0  # pairs the phase-1 filter could not rule out
+
+
+@dataclass
+class RunStats:
+    blocks: list = field(default_factory=list)
+    wall_s: float = 0.0
+    n_intervals: int = 0
+    kernel_ms: float = 0.0
+    launches: int = 0
+
+    def total_comparisons(self) -> int:
+        return sum(b.comparisons for b in self.blocks)
+
+    def describe(self) -> str:
+        lines = [f"wall_s={self.wall_s:.4f} intervals={self.n_intervals} kernel_ms={self.kernel_ms:.3f}"]
+        for b in self.blocks:
+            lines.append(
+                f"block {b.block_id}: comparisons={b.comparisons} survivors={b.survivors} emitted={b.emitted}"
+            )
+        return "\n".join(lines)
+
+
+class CandidateSet:
+    """Surviving pairs ``(t_tid, s_tid, rule_id)`` plus statistics.  The
+    rows are held as arrays; ``pairs`` materialises the reference's list of
+    tuples on first use."""
+
+    def __init__(self, pairs=None, stats: Optional[RunStats] = None, *, arrays=None, rule_ids=None):
+        self.stats = stats if stats is not None else RunStats()
+        self._pairs = list(pairs) if pairs is not None else None
+        self._arrays = arrays  # (t int64[k], s int64[k], rule_index int64[k])
+        self._rule_ids = list(rule_ids) if rule_ids is not None else []
+
+    @property
+    def pairs(self) -> list:
+        if self._pairs is None:
+            t, s, r = self._arrays
+            ids = self._rule_ids
+            self._pairs = [(a, b, ids[k]) for a, b, k in zip(t.tolist(), s.tolist(), r.tolist())]
+        return self._pairs
+
+    @property
+    def arrays(self):
+        """(t, s, rule_index) int64 arrays."""
+        if self._arrays is None:
+            idx = {rid: k for k, rid in enumerate(self._rule_ids)}
+            p = self._pairs or []
+            self._arrays = (
+                np.array([x[0] for x in p], dtype=np.int64),
+                np.array([x[1] for x in p], dtype=np.int64),
+                np.array([idx.get(x[2], -1) for x in p], dtype=np.int64),
+            )
+        return self._arrays
+
+    def pair_set(self) -> set:
+        t, s, _ = self.arrays
+        return set(zip(t.tolist(), s.tolist()))
+
+    def sorted_pairs(self) -> list:
+        return sorted(self.pairs)
+
+    def __len__(self) -> int:
+        return len(self._pairs) if self._pairs is not None else len(self._arrays[0])
+
+
+# ---------------------------------------------------------------------------
+# device objects
+
+
+def default_device() -> int:
+    return int(os.environ.get("RB_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
+class Context:
+    """One rb_ctx (device + stream).  One per (host thread, device)."""
+
+    def __init__(self, device: int):
+        h = _lib.c_vp()
+        check(lib().rb_ctx_create(int(device), _lib.ctypes.byref(h)))
+        self.handle = h
+        self.device = int(device)
+        self._fin = weakref.finalize(self, lib().rb_ctx_destroy, h)
+
+    def set_stream(self, cuda_stream: int) -> None:
+        check(lib().rb_ctx_set_stream(self.handle, _lib.c_vp(cuda_stream)))
+
+
+_tls = threading.local()
+
+
+def context(device: Optional[int] = None) -> Context:
+    device = default_device() if device is None else int(device)
+    cache = getattr(_tls, "ctx", None)
+    if cache is None:
+        cache = _tls.ctx = {}
+    if device not in cache:
+        cache[device] = Context(device)
+    return cache[device]
+
+
+class DeviceRelation:
+    """An ``Encoded`` uploaded to one device (rb_rel).  Columns added to
+    the encoding later are appended on the next ``sync``."""
+
+    def __init__(self, ctx: Context, enc: Encoded):
+        h = _lib.c_vp()
+        check(lib().rb_relation_create(ctx.handle, enc.n, _lib.ctypes.byref(h)))
+        self.handle = h
+        self.ctx = ctx
+        self.enc = enc
+        self.n_uploaded = 0
+        self._fin = weakref.finalize(self, lib().rb_relation_destroy, h)
+        self.sync()
+
+    def close(self) -> None:
+        self._fin()
+
+    def sync(self) -> None:
+        L = lib()
+        while self.n_uploaded < len(self.enc.columns):
+            c = self.enc.columns[self.n_uploaded]
+            col = _lib.ctypes.c_int32(-1)
+            if c.kind == COL_CODES:
+                data = i32(c.data)
+                check(L.rb_relation_add_codes(self.handle, ptr(data), _lib.ctypes.byref(col)))
+            elif c.kind == COL_MASK:
+                data = np.ascontiguousarray(c.data, dtype=np.uint8)
+                check(L.rb_relation_add_mask(self.handle, ptr(data), _lib.ctypes.byref(col)))
+            elif c.kind == COL_TOKENS:
+                offs = np.ascontiguousarray(c.offsets, dtype=np.int64)
+                ids = i32(c.data)
+                miss = None if c.missing is None else np.ascontiguousarray(c.missing, dtype=np.uint8)
+                check(L.rb_relation_add_tokens(self.handle, ptr(offs), ptr(ids), ptr(miss), _lib.ctypes.byref(col)))
+            elif c.kind == COL_CHARS:
+                offs = np.ascontiguousarray(c.offsets, dtype=np.int64)
+                data = np.ascontiguousarray(c.data)
+                miss = None if c.missing is None else np.ascontiguousarray(c.missing, dtype=np.uint8)
+                check(
+                    L.rb_relation_add_chars(
+                        self.handle, ptr(offs), ptr(data), c.width, ptr(miss), _lib.ctypes.byref(col)
+                    )
+                )
+            else:
+                raise ConfigError(f"unknown column kind {c.kind}")
+            if col.value != self.n_uploaded:
+                raise ConfigError("device column order diverged from the encoding")
+            self.n_uploaded += 1
+
+
+_dev_rel_cache: dict = {}
+
+
+def device_relation(ctx: Context, enc: Encoded) -> DeviceRelation:
+    key = (id(ctx), id(enc))
+    dr = _dev_rel_cache.get(key)
+    if dr is None or dr.enc is not enc or dr.ctx is not ctx:
+        dr = DeviceRelation(ctx, enc)
+        _dev_rel_cache[key] = dr
+        weakref.finalize(enc, _dev_rel_cache.pop, key, None)
+    dr.sync()
+    return dr
+
+
+class PathProgram:
+    """A path compiled against one encoding and resident on one device
+    (the reference's PathProgram, engine.py:342-368)."""
+
+    def __init__(self, path, enc: Encoded, reg=None, device: Optional[int] = None, *, compiled=None,
+                 drel: Optional[DeviceRelation] = None):
+        self.path = path
+        self.enc = enc
+        self.n_slots = len(path.predicate_table)
+        self.program = compiled if compiled is not None else compile_program(path, enc, reg)
+        self.rule_ids = list(path.rule_ids)
+        self.ctx = context(device) if drel is None else drel.ctx
+        self.drel = drel if drel is not None else device_relation(self.ctx, enc)
+        h = _lib.c_vp()
+        p = self.program
+        check(
+            lib().rb_program_create(
+                self.ctx.handle, self.drel.handle,
+                ptr(p.ins_op), ptr(p.ins_slot), ptr(p.ins_fail), ptr(p.ins_rule), len(p.ins_op),
+                ptr(p.slots), p.n_slots, ptr(p.tables), len(p.tables), _lib.ctypes.byref(h),
+            )
+        )
+        self.handle = h
+        self._fin = weakref.finalize(self, lib().rb_program_destroy, h)
+
+    def close(self) -> None:
+        self._fin()
+
+    # -- raw runs ---------------------------------------------------------
+
+    def run_raw(self, refs, n: int, flags: int, *, split: int = -1, row_lo: int = 0, row_hi: Optional[int] = None):
+        """Evaluate on the device.  Returns ((t, s, rule) int32 arrays, rb_stats)."""
+        L = lib()
+        res = _lib.c_vp()
+        refs_a = None if refs is None else i32(refs)
+        if split >= 0:
+            left, right = refs_a[:split], refs_a[split:]
+            check(L.rb_run_cross(self.ctx.handle, self.drel.handle, self.handle, ptr(np.ascontiguousarray(left)),
+                                 len(left), ptr(np.ascontiguousarray(right)), len(right), flags,
+                                 _lib.ctypes.byref(res)))
+        elif row_lo == 0 and (row_hi is None or row_hi >= n):
+            check(L.rb_run_partition(self.ctx.handle, self.drel.handle, self.handle, ptr(refs_a), n, flags,
+                                     _lib.ctypes.byref(res)))
+        else:
+            check(L.rb_run_partition_rows(self.ctx.handle, self.drel.handle, self.handle, ptr(refs_a), n,
+                                          row_lo, n if row_hi is None else row_hi, flags, _lib.ctypes.byref(res)))
+        try:
+            cnt = _lib.ctypes.c_int64(0)
+            check(L.rb_result_count(res, _lib.ctypes.byref(cnt)))
+            k = cnt.value
+            t = np.empty(k, dtype=np.int32)
+            s = np.empty(k, dtype=np.int32)
+            r = np.empty(k, dtype=np.int32)
+            if k:
+                check(L.rb_result_copy(res, ptr(t), ptr(s), ptr(r)))
+            st = _lib.RbStats()
+            check(L.rb_result_stats(res, _lib.ctypes.byref(st)))
+        finally:
+            L.rb_result_destroy(res)
+        return (t, s, r), st
+
+
+# ---------------------------------------------------------------------------
+# reference-facing API
+
+
+def _dedup(t, s, r, symmetric: bool, enumerate_all: bool):
+    """engine.py:600-616 on arrays: enumerate -> unique rows; symmetric ->
+    the smallest rule index per (t, s); asymmetric -> rows as they are."""
+    t = t.astype(np.int64)
+    s = s.astype(np.int64)
+    r = r.astype(np.int64)
+    if len(t) == 0 or (not enumerate_all and not symmetric):
+        return t, s, r
+    order = np.lexsort((r, s, t))
+    t, s, r = t[order], s[order], r[order]
+    if enumerate_all:
+        keep = np.ones(len(t), dtype=bool)
+        keep[1:] = (t[1:] != t[:-1]) | (s[1:] != s[:-1]) | (r[1:] != r[:-1])
+    else:
+        keep = np.ones(len(t), dtype=bool)
+        keep[1:] = (t[1:] != t[:-1]) | (s[1:] != s[:-1])
+    return t[keep], s[keep], r[keep]
+
+
+_enc_cache: dict = {}
+
+
+def _encoding_for(relation, encoded):
+    if isinstance(encoded, Encoded):
+        return encoded
+    key = id(relation)
+    hit = _enc_cache.get(key)
+    if hit is not None and hit.relation is relation:
+        return hit
+    enc = RelationEncoding(relation)
+    _enc_cache[key] = enc
+    try:
+        weakref.finalize(relation, _enc_cache.pop, key, None)
+    except TypeError:
+        pass
+    return enc
+
+
+def _program_for(path, relation, reg, encoded, program) -> PathProgram:
+    if isinstance(program, PathProgram):
+        return program
+    enc = _encoding_for(relation, encoded)
+    if isinstance(enc, RelationEncoding):
+        enc.prepare(list(path.predicate_table))
+    return PathProgram(path, enc, reg)
+
+
+def _refs_array(partition) -> np.ndarray:
+    refs = np.asarray(partition.tuple_refs, dtype=np.int64)
+    if len(np.unique(refs)) != len(refs):
+        raise SchemaError(f"partition {getattr(partition, 'pid', '?')} has duplicate tuple refs")
+    return refs.astype(np.int32)
+
+
+def _candidates(prog: PathProgram, rows, st, cfg: EngineConfig, n_outer: int, wall: float) -> CandidateSet:
+    t, s, r = _dedup(*rows, cfg.symmetric_mode, cfg.enumerate_witnesses)
+    block = BlockStats(
+        block_id=0,
+        intervals_processed=max(1, -(-n_outer // cfg.n_t)),
+        comparisons=int(st.comparisons),
+        busy_s=st.kernel_ms / 1e3,
+        slot_evals=np.array(st.slot_evals[: prog.n_slots], dtype=np.int64),
+        emitted=int(st.emitted),
+        survivors=int(st.survivors),
+    )
+    stats = RunStats(
+        blocks=[block],
+        wall_s=wall,
+        n_intervals=max(1, -(-n_outer // cfg.n_t)),
+        kernel_ms=float(st.kernel_ms),
+        launches=int(st.launches),
+    )
+    return CandidateSet(stats=stats, arrays=(t, s, r), rule_ids=prog.rule_ids)
+
+
+def run_partition(partition, relation, path, cfg=None, reg=None, encoded=None, program=None) -> CandidateSet:
+    """All pairs of one partition (engine.py:619-646): symmetric i<j with
+    t = the lower position, or every ordered i != j."""
+    cfg = cfg or EngineConfig()
+    if partition is None or len(partition.tuple_refs) == 0:
+        return CandidateSet(pairs=[])
+    started = time.perf_counter()
+    prog = _program_for(path, relation, reg, encoded, program)
+    refs = _refs_array(partition)
+    rows, st = prog.run_raw(refs, len(refs), cfg.flags())
+    return _candidates(prog, rows, st, cfg, len(refs), time.perf_counter() - started)
+
+
+def run_cross(left, right, relation, path, cfg=None, reg=None, encoded=None, program=None) -> CandidateSet:
+    """Every (t in left, s in right) pair, t always the left tuple
+    (engine.py:649-681 with _bipartite_patch 684-719)."""
+    cfg = cfg or EngineConfig()
+    started = time.perf_counter()
+    prog = _program_for(path, relation, reg, encoded, program)
+    lrefs = _refs_array(left)
+    rrefs = _refs_array(right)
+    refs = np.concatenate([lrefs, rrefs])
+    if len(np.unique(refs)) != len(refs):
+        raise SchemaError("partition -1 has duplicate tuple refs")  # the combined partition (engine.py:671-675)
+    rows, st = prog.run_raw(refs, len(refs), cfg.flags(), split=len(lrefs))
+    return _candidates(prog, rows, st, cfg, len(lrefs), time.perf_counter() - started)

@@ -1,0 +1,189 @@
+"""Seeded synthetic relations of the benchmark shapes, generated column-wise.
+
+The reference generates citation-style workloads row by row in Python
+(``citation_benchmark``, pkg/src/ruleblock/datasets.py:332-398) and encodes
+them with ``EncodedRelation`` at ~14 us/tuple.  At 1M-10M tuples that is
+minutes of host time, so the benchmark relations here are produced directly
+in the encoded columnar form the C ABI takes (codes / token CSR / char CSR),
+with the same value domains and the same duplicate-injection scheme, and
+a data-aware plan is derived from sampled selectivities (SURVEY §8d,
+config 2).  Text is generated already folded (lower-case ASCII, single
+spaces inside names), so the column values equal their folded forms.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .encode import COL_CHARS, COL_CODES, COL_TOKENS, Column, Encoded
+from .plan import plan_from_stats
+from .rules import parse_ruleset, predicate_universe
+
+TITLE_VOCAB = 800  # datasets.py:320-323: 20 stems x 40 suffixes
+FIRST = ["alice", "bob", "carol", "david", "erin", "frank", "grace", "henry", "irene", "jack",
+         "karen", "liam", "maria", "nolan", "olivia", "peter", "quinn", "rachel", "simon", "tara"]
+LAST = ["anders", "brown", "chen", "davis", "evans", "fischer", "garcia", "hansen", "ito", "jones",
+        "kumar", "larsen", "meyer", "novak", "olsen", "patel", "quirk", "rossi", "schmidt", "tanaka"]
+
+CITATION3_RULES = [
+    {"id": "R1", "when": [
+        {"t_attr": "year", "op": "eq", "s_attr": "year"},
+        {"t_attr": "title", "op": "sim", "s_attr": "title", "measure": "jaccard", "threshold": 0.75}]},
+    {"id": "R2", "when": [
+        {"t_attr": "authors", "op": "sim", "s_attr": "authors", "measure": "edit", "threshold": 0.8},
+        {"t_attr": "title", "op": "sim", "s_attr": "title", "measure": "jaccard", "threshold": 0.5}]},
+    {"id": "R3", "when": [
+        {"t_attr": "venue", "op": "eq", "s_attr": "venue"},
+        {"t_attr": "cat", "op": "eq", "s_attr": "cat"},
+        {"t_attr": "title", "op": "sim", "s_attr": "title", "measure": "exact_token", "threshold": 1.0}]},
+]
+
+KIND_COST = {"eq": 0.1, "exact_token": 0.3, "jaccard": 0.6, "edit": 1.0}
+
+
+@dataclass
+class Workload:
+    name: str
+    enc: Encoded
+    rules: object
+    path: object
+    n: int
+
+
+def _distinct_rows(rng, n: int, width: int, domain: int) -> np.ndarray:
+    """n rows of `width` distinct ints in [0, domain), rejection-sampled."""
+    out = rng.integers(0, domain, size=(n, width), dtype=np.int32)
+    while True:
+        s = np.sort(out, axis=1)
+        bad = np.nonzero((s[:, 1:] == s[:, :-1]).any(axis=1))[0]
+        if len(bad) == 0:
+            return out
+        out[bad] = rng.integers(0, domain, size=(len(bad), width), dtype=np.int32)
+
+
+def _csr_from_padded(vals: np.ndarray, lens: np.ndarray, sort_rows: bool) -> tuple[np.ndarray, np.ndarray]:
+    n, w = vals.shape
+    if sort_rows:
+        big = np.where(np.arange(w)[None, :] < lens[:, None], vals, np.iinfo(vals.dtype).max)
+        vals = np.sort(big, axis=1)
+    mask = np.arange(w)[None, :] < lens[:, None]
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=offsets[1:])
+    return offsets, vals[mask]
+
+
+def citation3(n: int = 1_000_000, seed: int = 2024, plan_sample: int = 200_000) -> Workload:
+    """BASELINE config 2: citation-style relation, 3 rules mixing eq,
+    jaccard and edit predicates."""
+    rng = np.random.default_rng(seed)
+    n_pairs = n // 4  # half of the tuples belong to an injected duplicate pair
+    # ---- base records (one per entity): duplicates copy and perturb
+    title_k = rng.integers(6, 11, size=n, dtype=np.int64)
+    title = _distinct_rows(rng, n, 10, TITLE_VOCAB)
+    n_auth = rng.integers(1, 4, size=n)
+    auth_first = rng.integers(0, len(FIRST), size=(n, 3))
+    auth_last = rng.integers(0, len(LAST), size=(n, 3))
+    year = rng.integers(0, 16, size=n, dtype=np.int32)
+    venue = rng.integers(0, 10, size=n, dtype=np.int32)
+    zipf_p = 1.0 / np.arange(1, 1001) ** 1.1
+    cat = rng.choice(1000, size=n, p=zipf_p / zipf_p.sum()).astype(np.int32)
+    # ---- duplicates: tuple 2k+1 describes the same paper as 2k (k < n_pairs)
+    a = np.arange(0, 2 * n_pairs, 2)
+    b = a + 1
+    title[b] = title[a]
+    roll = rng.random(n_pairs)
+    drop1 = (roll >= 0.55) & (roll < 0.90) & (title_k[a] > 6)
+    drop2 = (roll >= 0.90) & (title_k[a] > 7)
+    title_k[b] = title_k[a] - drop1 - 2 * drop2
+    n_auth[b], auth_first[b], auth_last[b] = n_auth[a], auth_first[a], auth_last[a]
+    year[b] = np.where(rng.random(n_pairs) < 0.96, year[a], (year[a] + 1) % 16)
+    venue[b] = np.where(rng.random(n_pairs) < 0.8, venue[a], rng.integers(0, 10, size=n_pairs))
+    cat[b] = np.where(rng.random(n_pairs) < 0.9, cat[a], cat[b])
+    auth_edit = np.zeros(n, dtype=np.int8)  # 1: double the first space, 2: drop the last char
+    r = rng.random(n_pairs)
+    auth_edit[b] = np.where(r < 0.35, np.where(rng.random(n_pairs) < 0.5, 1, 2), 0)
+
+    # ---- encode: token CSR (ids = vocabulary index), author chars
+    t_off, t_ids = _csr_from_padded(title, title_k, sort_rows=True)
+    names = [f"{f} {l}".encode() for f in FIRST for l in LAST]
+    name_idx = auth_first * len(LAST) + auth_last
+    strs = []
+    for k in range(n):
+        s = b", ".join(names[name_idx[k, j]] for j in range(n_auth[k]))
+        e = auth_edit[k]
+        if e == 1:
+            s = s.replace(b" ", b"  ", 1)
+        elif e == 2 and len(s) > 1:
+            s = s[:-1]
+        strs.append(s)
+    a_len = np.fromiter((len(s) for s in strs), dtype=np.int64, count=n)
+    a_off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(a_len, out=a_off[1:])
+    a_chars = np.frombuffer(b"".join(strs), dtype=np.uint8).copy()
+
+    enc = Encoded(n)
+    enc.add(("codes", "year"), Column(COL_CODES, year))
+    enc.add(("codes", "venue"), Column(COL_CODES, venue))
+    enc.add(("codes", "cat"), Column(COL_CODES, cat))
+    enc.add(("tokens", "title"), Column(COL_TOKENS, t_ids.astype(np.int32), t_off, np.zeros(n, np.uint8)))
+    enc.add(("chars", "authors"), Column(COL_CHARS, a_chars, a_off, np.zeros(n, np.uint8)))
+    import json
+
+    rules = parse_ruleset(json.dumps(CITATION3_RULES))
+    path = data_aware_plan(enc, rules, sample=plan_sample, seed=seed)
+    return Workload("citation3", enc, rules, path, n)
+
+
+def sampled_selectivity(enc: Encoded, predicates, sample: int, seed: int) -> dict:
+    """Pass rate of each predicate over `sample` random pairs, measured with
+    the reference's exact slot semantics (host numpy, no device)."""
+    from .encode import compile_program  # noqa: F401  (semantics live in the tables)
+
+    rng = np.random.default_rng(seed + 17)
+    i = rng.integers(0, enc.n, size=sample)
+    j = rng.integers(0, enc.n, size=sample)
+    keep = i != j
+    i, j = i[keep], j[keep]
+    out = {}
+    for p in predicates:
+        kind, lc, rc, _ = enc.slot_for(p)
+        L, R = enc.columns[lc], enc.columns[rc]
+        if p.comparator == "eq" and p.rhs_attr is not None:
+            hit = (L.data[i] >= 0) & (L.data[i] == R.data[j])
+        elif p.comparator == "eq":
+            hit = L.data[i] != 0
+        elif p.measure in ("jaccard", "exact_token"):
+            hit = np.zeros(len(i), dtype=bool)
+            m = min(len(i), 20000)
+            for k in range(m):
+                x = L.data[L.offsets[i[k]]:L.offsets[i[k] + 1]]
+                y = R.data[R.offsets[j[k]]:R.offsets[j[k] + 1]]
+                if p.measure == "exact_token":
+                    hit[k] = len(x) > 0 and np.array_equal(x, y)
+                else:
+                    inter = len(np.intersect1d(x, y, assume_unique=True))
+                    u = len(x) + len(y) - inter
+                    hit[k] = u > 0 and inter / u >= p.threshold
+            hit = hit[:m]
+        else:
+            la = np.diff(L.offsets)[i]
+            lb = np.diff(R.offsets)[j]
+            longest = np.maximum(la, lb)
+            hit = (longest - np.minimum(la, lb)) <= (1.0 - p.threshold) * longest  # length part only
+        out[p] = float(np.clip(hit.mean(), 1e-6, 1 - 1e-6))
+    return out
+
+
+def data_aware_plan(enc: Encoded, rules, sample: int = 200_000, seed: int = 0):
+    """Cost-effectiveness order (1 - sp) / cost from sampled selectivities
+    and per-kind cost constants, then the reference's tree + compile
+    (planner/plan.py:28-76, 147-300)."""
+    uni = predicate_universe(rules)
+    sps = sampled_selectivity(enc, uni, sample, seed)
+    costs = {p: KIND_COST["eq" if p.comparator == "eq" else p.measure] for p in uni}
+    return plan_from_stats(rules, costs, sps)
+
+
+WORKLOADS = {"citation3": citation3}
