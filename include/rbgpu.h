@@ -87,6 +87,9 @@ typedef struct rb_stats {
     int32_t launches;    /* kernels launched by the run                         */
     int32_t retries;     /* output-overflow re-runs                              */
     int64_t slot_evals[RB_MAX_SLOTS]; /* exact evaluations per slot (RB_STATS) */
+    int32_t specialized;   /* 1: the NVRTC-specialised kernel ran, 0: the generic one */
+    int32_t reserved;
+    double jit_compile_ms; /* one-off specialisation cost of this program's kernel */
 } rb_stats;
 
 typedef struct rb_ctx rb_ctx;
@@ -121,6 +124,10 @@ int rb_program_create(rb_ctx* ctx, rb_rel* rel, const int32_t* op, const int32_t
                       const int32_t* rule, int32_t n_ins, const rb_slot* slots, int32_t n_slots,
                       const int32_t* tables, int64_t n_tables, rb_prog** out);
 int rb_program_destroy(rb_prog* prog);
+/* how the pair kernel of this program was built: 1 specialised by NVRTC, 0
+ * generic; *log receives the compiler log or why specialisation was skipped
+ * (valid until the program is destroyed). */
+int rb_program_kernel_info(const rb_prog* prog, int32_t* specialized, double* compile_ms, const char** log);
 
 /* run_partition: all pairs of refs[0..n) (i<j symmetric, i!=j otherwise);
  * t = refs[i] (the lower position), s = refs[j].  refs == NULL means the

@@ -46,6 +46,7 @@ def lib():
         if not os.path.exists(LIB_PATH):
             build()
         L = ctypes.CDLL(LIB_PATH)
+        L.orc_slot_size.restype = ctypes.c_int32
         L.orc_run.restype = ctypes.c_int64
         L.orc_run.argtypes = [
             ctypes.c_void_p, ctypes.c_int32,

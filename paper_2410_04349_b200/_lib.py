@@ -39,6 +39,9 @@ class RbStats(ctypes.Structure):
         ("launches", ctypes.c_int32),
         ("retries", ctypes.c_int32),
         ("slot_evals", ctypes.c_int64 * MAX_SLOTS),
+        ("specialized", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("jit_compile_ms", ctypes.c_double),
     ]
 
 
@@ -59,6 +62,8 @@ _SIGNATURES = {
         [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int32, c_vp, ctypes.c_int32, c_vp, ctypes.c_int64, c_vpp],
     ),
     "rb_program_destroy": (ctypes.c_int, [c_vp]),
+    "rb_program_kernel_info": (
+        ctypes.c_int, [c_vp, c_i32p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_char_p)]),
     "rb_run_partition": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, ctypes.c_int64, ctypes.c_uint32, c_vpp]),
     "rb_run_partition_rows": (
         ctypes.c_int,

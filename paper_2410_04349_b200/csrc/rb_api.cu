@@ -93,6 +93,8 @@ struct rb_prog {
     int32_t n_slots = 0;
     int64_t lmax_edit = -1;  // longest string any edit slot reads (-1: no edit slot)
     std::vector<void*> allocs;
+    JitKernel jit;
+    long long last_rows = 0;  // output size of the previous run: sizes the next buffer
 };
 
 struct rb_result {
@@ -398,18 +400,26 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
     FilterPlan& F = P->F;
     memset(&F, 0, sizeof F);
     F.n_rules = (int)need.size();
-    for (size_t r = 0; r < need.size(); r++) F.need[r] = need[r];
-    auto rules_with = [&](uint64_t slot_bits) {
+    F.all_rules = need.size() >= 64 ? ~0ull : ((1ull << need.size()) - 1);
+    auto kill_of = [&](int s) {  // rules whose precondition contains slot s
         uint64_t m = 0;
         for (size_t r = 0; r < need.size(); r++)
-            if (need[r] & slot_bits) m |= 1ull << r;
+            if (need[r] & (1ull << s)) m |= 1ull << r;
         return m;
     };
+    // shared-memory threshold tables: every filtered jaccard / edit slot gets
+    // a prefix of its two tables; lengths beyond the prefix are not filtered
+    struct TabReq {
+        bool tok;
+        int feat, z;
+        int64_t src0, len0, src1, len1;
+    };
+    std::vector<TabReq> treq;
     std::map<std::pair<int, int>, int> eqf, tokf, strf;
     std::map<int, int> constf;
     for (int s = 0; s < n_slots; s++) {
         const rb_slot& sl = slots[s];
-        const uint64_t bit = 1ull << s;
+        const uint64_t kill = kill_of(s);
         const DevColumn& L = rel->cols[sl.lhs];
         const DevColumn& R = rel->cols[sl.rhs];
         const auto key = std::make_pair(sl.lhs, sl.rhs);
@@ -419,12 +429,12 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             if (it != eqf.end()) {
                 f = it->second;
             } else {
-                if (F.n_eq >= MAX_EQ) continue;  // left unfiltered: stays "maybe"
+                if (F.n_eq >= MAX_EQ) continue;  // left unfiltered: decided by the exact pass
                 f = eqf[key] = F.n_eq++;
                 F.eq_outer[f] = L.codes;
                 F.eq_inner[f] = R.codes;
             }
-            F.eq_slots[f] |= bit;
+            F.eq_kill[f] |= kill;
         } else if (sl.kind == RB_SLOT_EQ_CONST) {
             auto it = constf.find(sl.lhs);
             int f;
@@ -435,7 +445,7 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                 f = constf[sl.lhs] = F.n_const++;
                 F.const_mask[f] = L.mask;
             }
-            F.const_slots[f] |= bit;
+            F.const_kill[f] |= kill;
         } else if (sl.kind == RB_SLOT_JACCARD || sl.kind == RB_SLOT_EXACT) {
             auto it = tokf.find(key);
             int f;
@@ -453,14 +463,20 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                 F.tok_ihash[f] = R.hash;
             }
             if (F.tok_nslots[f] >= MAX_FSLOTS) continue;
-            TokSlotF& ts = F.tok_slot[f][F.tok_nslots[f]++];
-            ts.kind = sl.kind;
-            ts.bit = s;
-            ts.tab0 = T + sl.tab0;
-            ts.tab1 = T + sl.tab1;
-            ts.len0 = sl.kind == RB_SLOT_JACCARD ? sl.len0 : 0;
-            ts.len1 = sl.kind == RB_SLOT_JACCARD ? sl.len1 : 0;
-            F.tok_rules[f] |= rules_with(bit);
+            // keep jaccard slots ahead of exact_token slots on each feature
+            int at = F.tok_nslots[f]++;
+            if (sl.kind == RB_SLOT_JACCARD) {
+                for (int z = at; z > F.tok_njac[f]; z--) F.tok_slot[f][z] = F.tok_slot[f][z - 1];
+                for (auto& t : treq)
+                    if (t.feat == f && t.tok) t.z += (t.z >= F.tok_njac[f]) ? 1 : 0;
+                at = F.tok_njac[f]++;
+            }
+            FSlot& fs = F.tok_slot[f][at];
+            fs = FSlot{};
+            fs.kill = kill;
+            fs.kind = sl.kind;
+            if (sl.kind == RB_SLOT_JACCARD) treq.push_back({true, f, at, sl.tab0, sl.len0, sl.tab1, sl.len1});
+            F.tok_rules[f] |= kill;
         } else if (sl.kind == RB_SLOT_EDIT) {
             auto it = strf.find(key);
             int f;
@@ -475,15 +491,37 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                 F.str_ibag[f] = R.bag;
             }
             if (F.str_nslots[f] >= MAX_FSLOTS) continue;
-            StrSlotF& ss = F.str_slot[f][F.str_nslots[f]++];
-            ss.bit = s;
-            ss.maxgap = T + sl.tab0;
-            ss.maxd = T + sl.tab1;
-            ss.len0 = sl.len0;
-            ss.len1 = sl.len1;
-            F.str_rules[f] |= rules_with(bit);
+            const int at = F.str_nslots[f]++;
+            FSlot& fs = F.str_slot[f][at];
+            fs.kill = kill;
+            fs.kind = sl.kind;
+            treq.push_back({false, f, at, sl.tab0, sl.len0, sl.tab1, sl.len1});
+            F.str_rules[f] |= kill;
         }
     }
+    std::vector<int32_t> stab(TAB_BASE, 0);  // guard entries: lookups of missing (-1) lengths land here
+    {
+        int64_t total = TAB_BASE;
+        for (auto& t : treq) total += t.len0 + t.len1;
+        const bool full = total <= SMEM_TAB;
+        const int64_t per = treq.empty() ? 0 : std::max<int64_t>(1, (SMEM_TAB - TAB_BASE) / (2 * (int64_t)treq.size()));
+        for (auto& t : treq) {
+            FSlot& fs = t.tok ? F.tok_slot[t.feat][t.z] : F.str_slot[t.feat][t.z];
+            const int64_t c0 = full ? t.len0 : std::min(t.len0, per);
+            const int64_t c1 = full ? t.len1 : std::min(t.len1, per);
+            fs.off0 = (int32_t)stab.size();
+            fs.cap0 = (int32_t)c0;
+            stab.insert(stab.end(), tables + t.src0, tables + t.src0 + c0);
+            fs.off1 = (int32_t)stab.size();
+            fs.cap1 = (int32_t)c1;
+            stab.insert(stab.end(), tables + t.src1, tables + t.src1 + c1);
+        }
+        F.full_tab = full ? 1 : 0;
+    }
+    void* d_stab;
+    if ((e = up(stab.data(), sizeof(int32_t) * stab.size(), &d_stab))) return bail(e);
+    F.tab_src = (const int32_t*)d_stab;
+    F.n_tab = (int32_t)stab.size();
     P->V.ins = (const int4*)d_ins;
     P->V.slots = (const DevSlot*)d_slots;
     P->V.cols = (const DevColumn*)d_cols;
@@ -491,7 +529,16 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
     P->V.n_ins = n_ins;
     P->V.n_slots = n_slots;
     if ((e = cudaStreamSynchronize(c->stream))) return bail(e);
+    P->jit = jit_pair_kernel(P->F, c->device);
     *out = P;
+    return RB_OK;
+}
+
+int rb_program_kernel_info(const rb_prog* P, int32_t* specialized, double* compile_ms, const char** log) {
+    if (!P) return fail(RB_ERR_INVALID, "rb_program_kernel_info: null program");
+    if (specialized) *specialized = P->jit.ok ? 1 : 0;
+    if (compile_ms) *compile_ms = P->jit.compile_ms;
+    if (log) *log = P->jit.log.c_str();
     return RB_OK;
 }
 
@@ -559,7 +606,8 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     if (cudaError_t e = c->counters.grow(sizeof(unsigned long long) * n_counters))
         return cleanup(fail(RB_ERR_CUDA, "counters: %s", cudaGetErrorString(e)));
 
-    const int grid = std::max(1, std::min(n_items, c->sm_count * c->blocks_per_sm));
+    const int bps = P->jit.ok ? P->jit.blocks_per_sm : c->blocks_per_sm;
+    const int grid = std::max(1, std::min(n_items, c->sm_count * bps));
     int64_t stride = 0;
     if (P->lmax_edit >= 0) {
         stride = (P->lmax_edit + 2 + 31) & ~(int64_t)31;
@@ -571,7 +619,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     CK(cudaMemcpyAsync(c->items.p, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice, c->stream));
     if (refs) CK(cudaMemcpyAsync(c->refs.p, refs, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
 
-    long long cap = 1 << 16;
+    long long cap = std::max<long long>(1 << 20, P->last_rows + P->last_rows / 4);
     unsigned long long* ctr = (unsigned long long*)c->counters.p;
     for (int attempt = 0;; attempt++) {
         res->d_t = nullptr;
@@ -603,7 +651,8 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         R.scratch_stride = stride;
 
         CK(cudaEventRecord(c->ev0, c->stream));
-        e = launch_pair_kernel(P->F, P->V, R, grid, c->stream);
+        e = P->jit.ok ? launch_jit_kernel(P->jit, P->F, P->V, R, grid, c->stream)
+                      : launch_pair_kernel(P->F, P->V, R, grid, c->stream);
         if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel launch: %s", cudaGetErrorString(e)));
         CK(cudaEventRecord(c->ev1, c->stream));
         unsigned long long host_ctr[n_counters];
@@ -621,6 +670,9 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             res->stats.survivors = (int64_t)host_ctr[3];
             res->stats.emitted = rows;
             res->stats.retries = attempt;
+            res->stats.specialized = P->jit.ok ? 1 : 0;
+            res->stats.jit_compile_ms = P->jit.compile_ms;
+            P->last_rows = rows;
             for (int s = 0; s < RB_MAX_SLOTS; s++) res->stats.slot_evals[s] = (int64_t)host_ctr[4 + s];
             break;
         }

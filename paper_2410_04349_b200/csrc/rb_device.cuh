@@ -1,0 +1,645 @@
+// rb_device.cuh -- all device code of the pair evaluation, self-contained so
+// that it compiles both with nvcc (the generic kernel, built into
+// librbgpu.so) and with NVRTC at program-creation time (a kernel specialised
+// to one program's shape: number of equality / token / string features and
+// slots per feature become compile-time constants, so the per-pair loop has
+// no dispatch left -- query compilation, the way a database compiles a plan).
+//
+// Layout in HBM (one rb_rel per relation, uploaded once):
+//   CODES  col: int32 codes[n]
+//   MASK   col: uint8 mask[n]
+//   TOKENS col: int64 offsets[n+1], int32 ids[nnz]            (from the host)
+//               int32 len[n] (-1 = missing), uint4 sig[n] (128-bit token
+//               signature), uint2 hash[n] (64-bit id-list hash)  (derived on device)
+//   CHARS  col: int64 offsets[n+1], u8|u32 chars[nnz]         (from the host)
+//               int32 len[n] (-1 = missing), uint4 bag[n] (16 x u8 saturating
+//               character-bucket counts)                        (derived on device)
+// The derived per-tuple features are what the pair kernel streams: fixed-size,
+// 16-byte aligned, read with 128-bit loads.  The ragged arrays are touched
+// only by the exact interpreter for surviving pairs.
+//
+// Exactness of the phase-1 filters (each is a bound on the reference's own
+// quantity, so a pair is dropped only when a predicate is certainly false):
+//  * token signature: bit(id) = top-7 bits of id*phi.  u = popc(sig_t & sig_s)
+//    + (|t| - popc(sig_t)) counts every outer token whose bit is present in
+//    the inner signature plus every outer token that shares its bit with an
+//    earlier one, so u >= |A n B|; u < mink[n+m] proves jaccard < delta.
+//  * id-list hash: different hashes prove different lists (exact_token).
+//  * character histogram: 16 buckets of saturating u8 counts; saturation is
+//    1-Lipschitz so D' = sum |ha-hb| <= D, and lev >= ceil((D'+|la-lb|)/2)
+//    (bag distance), so a bound above maxd[L] proves the edit test fails.
+#pragma once
+
+#ifdef __CUDACC_RTC__
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#define INT_MIN (-2147483647 - 1)
+#define INT_MAX 2147483647
+#define INT64_MAX 9223372036854775807LL
+#define RB_SLOT_EQ_CODE 0
+#define RB_SLOT_EQ_CONST 1
+#define RB_SLOT_JACCARD 2
+#define RB_SLOT_EXACT 3
+#define RB_SLOT_EDIT 4
+#define RB_SYMMETRIC 1u
+#define RB_ENUMERATE 2u
+#define RB_STATS 4u
+#define RB_MAX_CHECKPOINTS 64
+#endif
+
+namespace rb {
+
+constexpr int MAX_COLS = 64;
+constexpr int MAX_EQ = 6;      // equality features filtered in the pair loop
+constexpr int MAX_TOK = 2;     // token-set features (jaccard / exact_token)
+constexpr int MAX_STR = 2;     // string features (edit)
+constexpr int MAX_CONST = 8;   // t.attr = const masks
+constexpr int MAX_FSLOTS = 4;  // slots sharing one token / string feature
+constexpr int MAX_RULES = RB_MAX_CHECKPOINTS;
+constexpr int SMEM_TAB = 2048; // int32 threshold-table entries staged in shared memory
+
+constexpr int BLOCK = 256;     // threads per CTA = outer rows per item
+constexpr int TJ = 128;        // inner tuples per shared-memory tile
+constexpr int QCAP = 256;      // survivor queue entries per warp
+constexpr int NWARPS = BLOCK / 32;
+constexpr int64_t CHUNK = 16384;  // inner columns per work item
+
+enum RunMode : int32_t { MODE_SYM = 0, MODE_ASYM = 1, MODE_CROSS = 2 };
+
+struct DevColumn {
+    int32_t kind;
+    int32_t width;
+    const int32_t* codes;
+    const uint8_t* mask;
+    const int64_t* offsets;
+    const void* data;
+    const int32_t* len;
+    const uint4* sig;
+    const uint2* hash;
+    const uint4* bag;
+};
+
+struct DevSlot {
+    int32_t kind;
+    int32_t lhs;
+    int32_t rhs;
+    int32_t flags;
+    const int32_t* tab0;
+    const int32_t* tab1;
+    int32_t len0;
+    int32_t len1;
+};
+
+// One filtered slot on a token / string feature.  Its exact tables are
+// staged in shared memory at [off0, off0+cap0) and [off1, off1+cap1); a
+// length beyond a cap is simply not filtered (left to the exact pass).
+struct FSlot {
+    uint64_t kill;  // rules whose precondition contains this slot
+    int32_t kind;
+    int32_t off0, cap0;
+    int32_t off1, cap1;
+    int32_t pad;
+};
+
+// Phase-1 filter program.  Per pair the kernel keeps the set of rules that
+// may still hold ("alive"); a predicate proven false kills every rule that
+// needs it.  Equality / const tests are exact; token and string slots use
+// exact-safe bounds.  Survivors are re-evaluated exactly.
+struct FilterPlan {
+    int32_t n_eq, n_tok, n_str, n_const, n_rules, n_tab;
+    int32_t full_tab, pad_;  // full_tab: every shared table covers its column's longest row
+    uint64_t all_rules;
+    const int32_t* tab_src;  // n_tab int32 entries copied to shared memory
+    const int32_t* eq_outer[MAX_EQ];
+    const int32_t* eq_inner[MAX_EQ];
+    uint64_t eq_kill[MAX_EQ];
+    const uint8_t* const_mask[MAX_CONST];
+    uint64_t const_kill[MAX_CONST];
+    const int64_t* tok_ooff[MAX_TOK];
+    const int32_t* tok_oids[MAX_TOK];
+    const int32_t* tok_olen[MAX_TOK];
+    const uint2* tok_ohash[MAX_TOK];
+    const int32_t* tok_ilen[MAX_TOK];
+    const uint4* tok_isig[MAX_TOK];
+    const uint2* tok_ihash[MAX_TOK];
+    int32_t tok_nslots[MAX_TOK];  // slots on the feature: the first tok_njac are jaccard, the rest exact_token
+    int32_t tok_njac[MAX_TOK];
+    uint64_t tok_rules[MAX_TOK];
+    FSlot tok_slot[MAX_TOK][MAX_FSLOTS];
+    const int32_t* str_olen[MAX_STR];
+    const uint4* str_obag[MAX_STR];
+    const int32_t* str_ilen[MAX_STR];
+    const uint4* str_ibag[MAX_STR];
+    int32_t str_nslots[MAX_STR];
+    uint64_t str_rules[MAX_STR];
+    FSlot str_slot[MAX_STR][MAX_FSLOTS];
+};
+
+// Exact interpreter program (evaluate_pair, engine.py:93-132).
+struct VerifyProg {
+    const int4* ins;  // {op, slot | checkpoint ordinal, fail_jump, rule}
+    const DevSlot* slots;
+    const DevColumn* cols;
+    const int32_t* cp_rule;  // checkpoint ordinal -> index into path.rule_ids
+    int32_t n_ins;
+    int32_t n_slots;
+};
+
+struct RunParams {
+    const int32_t* refs;  // position -> tid; nullptr = identity
+    int64_t n;
+    int32_t mode;
+    uint32_t flags;
+    const int4* items;  // {row0, col0, col1, row_hi}
+    int32_t n_items;
+    unsigned int* item_counter;
+    int32_t* out_t;
+    int32_t* out_s;
+    int32_t* out_r;
+    unsigned long long* out_count;
+    long long cap;
+    unsigned long long* stat_pairs;
+    unsigned long long* stat_surv;
+    unsigned long long* slot_evals;
+    int32_t* scratch;
+    int64_t scratch_stride;
+};
+
+// device-side helpers shared by kernels
+__host__ __device__ inline uint32_t sig_bit(int32_t id) { return ((uint32_t)id * 0x9E3779B1u) >> 25; }
+__host__ __device__ inline uint32_t bag_bucket(uint32_t c) { return (c * 0x9E3779B1u) >> 28; }
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// ---------------------------------------------------------------------------
+// exact interpreter (survivors only)
+
+static __device__ __forceinline__ uint32_t char_at(const DevColumn& c, int64_t k) {
+    return c.width == 1 ? __ldg((const uint8_t*)c.data + k) : __ldg((const uint32_t*)c.data + k);
+}
+
+// Banded Levenshtein with cutoff k (Ukkonen): exact when the distance is
+// <= k, otherwise returns k+1.  Rows run over the shorter string, the
+// single DP row (longer string) lives in this thread's scratch slice.
+static __device__ int lev_bounded(const DevColumn& ca, int64_t a0, int la, const DevColumn& cb, int64_t b0, int lb, int k,
+                           int32_t* row) {
+    const DevColumn* cs = &ca;
+    const DevColumn* cl = &cb;
+    int64_t s0 = a0, l0 = b0;
+    int n = la, m = lb;
+    if (n > m) {
+        cs = &cb;
+        cl = &ca;
+        s0 = b0;
+        l0 = a0;
+        n = lb;
+        m = la;
+    }
+    const int INF = k + 1;
+    if (m - n > k) return INF;
+    if (n == 0) return m;
+    for (int j = 0; j <= m; j++) row[j] = min(j, INF);
+    for (int i = 1; i <= n; i++) {
+        const uint32_t ai = char_at(*cs, s0 + i - 1);
+        const int jlo = max(1, i - k), jhi = min(m, i + k);
+        int diag = row[jlo - 1];
+        int left = (jlo == 1) ? min(i, INF) : INF;
+        if (jlo == 1) row[0] = min(i, INF);
+        int rmin = (jlo == 1) ? left : INF;
+        for (int j = jlo; j <= jhi; j++) {
+            const int up = row[j];
+            int v = diag + (ai == char_at(*cl, l0 + j - 1) ? 0 : 1);
+            v = min(v, up + 1);
+            v = min(v, left + 1);
+            v = min(v, INF);
+            diag = up;
+            row[j] = v;
+            left = v;
+            rmin = min(rmin, v);
+        }
+        if (rmin > k) return INF;
+    }
+    return row[m];
+}
+
+static __device__ int intersect_ids(const int32_t* __restrict__ a, int n, const int32_t* __restrict__ b, int m) {
+    int i = 0, j = 0, inter = 0;
+    while (i < n && j < m) {
+        const int32_t x = __ldg(a + i), y = __ldg(b + j);
+        inter += (x == y);
+        i += (x <= y);
+        j += (y <= x);
+    }
+    return inter;
+}
+
+static __device__ bool exact_slot(const VerifyProg& V, int s, int32_t ti, int32_t si, int32_t* scratch) {
+    const DevSlot sl = V.slots[s];
+    const DevColumn& ca = V.cols[sl.lhs];
+    const DevColumn& cb = V.cols[sl.rhs];
+    switch (sl.kind) {
+        case RB_SLOT_EQ_CODE: {
+            const int32_t x = __ldg(ca.codes + ti);
+            return x >= 0 && x == __ldg(cb.codes + si);
+        }
+        case RB_SLOT_EQ_CONST:
+            return __ldg(ca.mask + ti) != 0;
+        case RB_SLOT_JACCARD: {
+            const int n = __ldg(ca.len + ti), m = __ldg(cb.len + si);
+            if (n < 0 || m < 0 || (n | m) == 0) return false;
+            const int small = min(n, m), big = max(n, m);
+            if (big < sl.len0 && small < __ldg(sl.tab0 + big)) return false;
+            const int inter = intersect_ids((const int32_t*)ca.data + ca.offsets[ti], n,
+                                            (const int32_t*)cb.data + cb.offsets[si], m);
+            return n + m < sl.len1 && inter >= __ldg(sl.tab1 + n + m);
+        }
+        case RB_SLOT_EXACT: {
+            const int n = __ldg(ca.len + ti), m = __ldg(cb.len + si);
+            if (n < 0 || m < 0 || (n | m) == 0 || n != m) return false;
+            const int32_t* a = (const int32_t*)ca.data + ca.offsets[ti];
+            const int32_t* b = (const int32_t*)cb.data + cb.offsets[si];
+            for (int k = 0; k < n; k++)
+                if (__ldg(a + k) != __ldg(b + k)) return false;
+            return true;
+        }
+        case RB_SLOT_EDIT: {
+            const int la = __ldg(ca.len + ti), lb = __ldg(cb.len + si);
+            if (la < 0 || lb < 0) return false;
+            const int L = max(la, lb);
+            if (L == 0) return true;
+            if (L >= sl.len0 || L >= sl.len1) return false;  // cannot happen: tables cover the columns
+            if (abs(la - lb) > __ldg(sl.tab0 + L)) return false;
+            const int k = __ldg(sl.tab1 + L);
+            if (k < 0) return false;
+            const int d = lev_bounded(ca, ca.offsets[ti], la, cb, cb.offsets[si], lb, k, scratch);
+            return d <= k;
+        }
+    }
+    return false;
+}
+
+// Returns the mask of checkpoint ordinals reached (first one only unless
+// enumerating).  engine.py:531-559.
+static __device__ uint64_t interpret(const VerifyProg& V, int32_t ti, int32_t si, bool enumerate, int32_t* scratch,
+                              unsigned long long* slot_evals) {
+    uint64_t reuse = 0, value = 0, hit = 0;
+    int ip = 0;
+    while (ip < V.n_ins) {
+        const int4 ins = __ldg(V.ins + ip);
+        if (ins.x == 1) {
+            hit |= 1ull << ins.y;
+            if (!enumerate) break;
+            ip++;
+            continue;
+        }
+        const uint64_t bit = 1ull << ins.y;
+        bool truth;
+        if (reuse & bit) {
+            truth = (value & bit) != 0;
+        } else {
+            truth = exact_slot(V, ins.y, ti, si, scratch);
+            reuse |= bit;
+            if (truth) value |= bit;
+            if (slot_evals) atomicAdd(slot_evals + ins.y, 1ull);
+        }
+        ip = truth ? ip + 1 : ins.z;
+    }
+    return hit;
+}
+
+static __device__ __noinline__ void drain_queue(const VerifyProg& V, const RunParams& R, const int2* q, int qn, const int* cp_rule,
+                            int32_t* scratch) {
+    const int lane = threadIdx.x & 31;
+    const bool enumerate = (R.flags & RB_ENUMERATE) != 0;
+    const bool sym = (R.flags & RB_SYMMETRIC) != 0;
+    for (int base = 0; base < qn; base += 32) {
+        const int k = base + lane;
+        uint64_t hit = 0;
+        int32_t ti = 0, si = 0;
+        if (k < qn) {
+            const int2 e = q[k];
+            ti = e.x;
+            si = e.y;
+            hit = interpret(V, ti, si, enumerate, scratch, (R.flags & RB_STATS) ? R.slot_evals : nullptr);
+        }
+        const int cnt = __popcll(hit);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total == 0) continue;
+        unsigned long long at = 0;
+        if (lane == 31) at = atomicAdd(R.out_count, (unsigned long long)total);
+        at = __shfl_sync(0xffffffffu, at, 31) + (unsigned long long)(incl - cnt);
+        int32_t a = ti, b = si;
+        if (sym && a > b) {
+            a = si;
+            b = ti;
+        }
+        while (hit) {
+            const int ord = __ffsll((long long)hit) - 1;
+            hit &= hit - 1;
+            if (at < (unsigned long long)R.cap) {
+                R.out_t[at] = a;
+                R.out_s[at] = b;
+                R.out_r[at] = cp_rule[ord];
+            }
+            at++;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the pair kernel
+
+struct __align__(16) Tile {
+    uint4 toksig[MAX_TOK][TJ];
+    uint4 strbag[MAX_STR][TJ];
+    uint2 tokhash[MAX_TOK][TJ];
+    int32_t eq[MAX_EQ][TJ];
+    int32_t toklen[MAX_TOK][TJ];
+    int32_t strlen_[MAX_STR][TJ];
+    int32_t tid[TJ];
+};
+
+// Shape of the filter program: compile-time constants in a specialised
+// (NVRTC) build, kernel-parameter reads in the generic build.
+#ifdef RB_SPEC
+#define RB_NEQ SPEC_NEQ
+#define RB_NCONST SPEC_NCONST
+#define RB_NTOK SPEC_NTOK
+#define RB_NSTR SPEC_NSTR
+#define RB_TOK_NS(f) ((f) == 0 ? SPEC_TOK0_NS : SPEC_TOK1_NS)
+#define RB_TOK_NJ(f) ((f) == 0 ? SPEC_TOK0_NJ : SPEC_TOK1_NJ)
+#define RB_STR_NS(f) ((f) == 0 ? SPEC_STR0_NS : SPEC_STR1_NS)
+#define RB_FULLTAB SPEC_FULLTAB
+#else
+#define RB_NEQ F.n_eq
+#define RB_NCONST F.n_const
+#define RB_NTOK F.n_tok
+#define RB_NSTR F.n_str
+#define RB_TOK_NS(f) F.tok_nslots[f]
+#define RB_TOK_NJ(f) F.tok_njac[f]
+#define RB_STR_NS(f) F.str_nslots[f]
+#define RB_FULLTAB F.full_tab
+#endif
+
+// Shared tables start at TAB_BASE so that the (discarded) lookups of pairs
+// with a missing side, whose lengths are -1, stay inside the array.
+constexpr int TAB_BASE = 2;
+
+// Mask = uint32_t when the path has <= 32 checkpoints, else uint64_t.
+template <typename Mask>
+__device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg& V, const RunParams& R) {
+    __shared__ Tile T;
+    __shared__ int2 queue[NWARPS][QCAP];
+    __shared__ int32_t tab[SMEM_TAB];
+    __shared__ int cp_rule[MAX_RULES];
+    __shared__ int s_item;
+
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const unsigned FULL = 0xffffffffu;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    int2* q = queue[warp];
+    int qn = 0;
+    unsigned long long my_pairs = 0, my_surv = 0;
+    int32_t* scratch = R.scratch + (int64_t)(blockIdx.x * BLOCK + threadIdx.x) * R.scratch_stride;
+
+    for (int k = threadIdx.x; k < MAX_RULES; k += BLOCK) cp_rule[k] = V.cp_rule[k];
+    for (int k = threadIdx.x; k < F.n_tab; k += BLOCK) tab[k] = F.tab_src[k];
+
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_item = (int)atomicAdd(R.item_counter, 1u);
+        __syncthreads();
+        const int it = s_item;
+        if (it >= R.n_items) break;
+        const int4 item = R.items[it];
+        const int64_t i = (int64_t)item.x + threadIdx.x;
+        const int64_t col0 = item.y, col1 = item.z;
+        const bool row_ok = i < (int64_t)item.w;
+
+        // ---- outer tuple -> registers
+        int32_t ti = 0;
+        Mask alive0 = 0;
+        int32_t ocode[MAX_EQ];
+        int32_t olen[MAX_TOK], orem[MAX_TOK];
+        uint32_t lev[MAX_TOK][4];
+        uint2 ohash[MAX_TOK];
+        int32_t oslen[MAX_STR];
+        uint4 obag[MAX_STR];
+        if (row_ok) {
+            ti = R.refs ? R.refs[i] : (int32_t)i;
+            alive0 = (Mask)F.all_rules;
+            if (R.mode == MODE_SYM) {
+                const int64_t lo = col0 > i + 1 ? col0 : i + 1;
+                my_pairs += (unsigned long long)(col1 > lo ? col1 - lo : 0);
+            } else if (R.mode == MODE_ASYM) {
+                my_pairs += (unsigned long long)((col1 - col0) - ((i >= col0 && i < col1) ? 1 : 0));
+            } else {
+                my_pairs += (unsigned long long)(col1 - col0);
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < MAX_EQ; f++) {
+            ocode[f] = INT_MIN;  // never equals an inner code (those are >= -2)
+            if (f < RB_NEQ && row_ok) {
+                const int32_t c = __ldg(F.eq_outer[f] + ti);
+                if (c >= 0)
+                    ocode[f] = c;
+                else
+                    alive0 &= ~(Mask)F.eq_kill[f];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < MAX_CONST; k++)
+            if (k < RB_NCONST && row_ok && !__ldg(F.const_mask[k] + ti)) alive0 &= ~(Mask)F.const_kill[k];
+#pragma unroll
+        for (int f = 0; f < MAX_TOK; f++) {
+            olen[f] = -1;
+            orem[f] = 0;
+            ohash[f] = make_uint2(0, 0);
+#pragma unroll
+            for (int w = 0; w < 4; w++) lev[f][w] = 0;
+            if (f < RB_NTOK && row_ok) {
+                olen[f] = __ldg(F.tok_olen[f] + ti);
+                ohash[f] = __ldg(F.tok_ohash[f] + ti);
+                const int64_t a = __ldg(F.tok_ooff[f] + ti), b = __ldg(F.tok_ooff[f] + ti + 1);
+                for (int64_t k = a; k < b; k++) {
+                    const uint32_t bit = sig_bit(__ldg(F.tok_oids[f] + k));
+                    const uint32_t m = 1u << (bit & 31);
+                    const uint32_t wsel = bit >> 5;
+#pragma unroll
+                    for (int w = 0; w < 4; w++) {
+                        if (w == (int)wsel) {
+                            if (lev[f][w] & m) orem[f]++;  // shares its bit with an earlier token
+                            lev[f][w] |= m;
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < MAX_STR; f++) {
+            oslen[f] = -1;
+            obag[f] = make_uint4(0, 0, 0, 0);
+            if (f < RB_NSTR && row_ok) {
+                oslen[f] = __ldg(F.str_olen[f] + ti);
+                obag[f] = __ldg(F.str_obag[f] + ti);
+            }
+        }
+
+        // ---- stream inner tiles
+        for (int64_t jt = col0; jt < col1; jt += TJ) {
+            const int tn = (int)(col1 - jt < TJ ? col1 - jt : TJ);
+            __syncthreads();
+            for (int k = threadIdx.x; k < tn; k += BLOCK) {
+                const int64_t j = jt + k;
+                const int32_t sj = R.refs ? __ldg(R.refs + j) : (int32_t)j;
+                T.tid[k] = sj;
+#pragma unroll
+                for (int f = 0; f < MAX_EQ; f++)
+                    if (f < RB_NEQ) T.eq[f][k] = __ldg(F.eq_inner[f] + sj);
+#pragma unroll
+                for (int f = 0; f < MAX_TOK; f++)
+                    if (f < RB_NTOK) {
+                        T.toklen[f][k] = __ldg(F.tok_ilen[f] + sj);
+                        T.toksig[f][k] = __ldg(F.tok_isig[f] + sj);
+                        T.tokhash[f][k] = __ldg(F.tok_ihash[f] + sj);
+                    }
+#pragma unroll
+                for (int f = 0; f < MAX_STR; f++)
+                    if (f < RB_NSTR) {
+                        T.strlen_[f][k] = __ldg(F.str_ilen[f] + sj);
+                        T.strbag[f][k] = __ldg(F.str_ibag[f] + sj);
+                    }
+            }
+            __syncthreads();
+
+            // valid(jj) <=> jj >= jj_lo && jj != jj_skip
+            int jj_lo = 0, jj_skip = -1;
+            if (!row_ok) {
+                jj_lo = TJ + 1;
+            } else if (R.mode == MODE_SYM) {
+                const int64_t d = i - jt + 1;
+                jj_lo = d < 0 ? 0 : (d > TJ + 1 ? TJ + 1 : (int)d);
+            } else if (R.mode == MODE_ASYM) {
+                const int64_t d = i - jt;
+                jj_skip = (d >= 0 && d < TJ) ? (int)d : -1;
+            }
+
+            for (int jj = 0; jj < tn; jj++) {
+                Mask alive = (jj >= jj_lo && jj != jj_skip) ? alive0 : (Mask)0;
+#pragma unroll
+                for (int f = 0; f < MAX_EQ; f++)
+                    if (f < RB_NEQ && ocode[f] != T.eq[f][jj]) alive &= ~(Mask)F.eq_kill[f];
+
+#pragma unroll
+                for (int f = 0; f < MAX_TOK; f++) {
+                    if (f < RB_NTOK && __any_sync(FULL, (alive & (Mask)F.tok_rules[f]) != 0)) {
+                        const int m = T.toklen[f][jj];
+                        const uint4 is = T.toksig[f][jj];
+                        const int n = olen[f];
+                        const bool live = (n >= 0) & (m >= 0) & ((n | m) != 0);
+                        const int small = min(n, m), big = max(n, m);
+                        int u = __popc(lev[f][0] & is.x) + __popc(lev[f][1] & is.y) + __popc(lev[f][2] & is.z) +
+                                __popc(lev[f][3] & is.w) + orem[f];
+                        u = min(u, small);
+#pragma unroll
+                        for (int z = 0; z < MAX_FSLOTS; z++) {
+                            if (z < RB_TOK_NS(f)) {
+                                const FSlot& fs = F.tok_slot[f][z];
+                                bool ok;
+                                if (z < RB_TOK_NJ(f)) {  // jaccard: exact integer tables
+                                    const int ms = (RB_FULLTAB || (unsigned)big < (unsigned)fs.cap0) ? tab[fs.off0 + big] : 0;
+                                    const int mk = (RB_FULLTAB || (unsigned)(n + m) < (unsigned)fs.cap1) ? tab[fs.off1 + n + m] : 0;
+                                    ok = live & (small >= ms) & (u >= mk);
+                                } else {  // exact_token
+                                    const uint2 h = T.tokhash[f][jj];
+                                    ok = live & (n == m) & (h.x == ohash[f].x) & (h.y == ohash[f].y);
+                                }
+                                if (!ok) alive &= ~(Mask)fs.kill;
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int f = 0; f < MAX_STR; f++) {
+                    if (f < RB_NSTR && __any_sync(FULL, (alive & (Mask)F.str_rules[f]) != 0)) {
+                        const int la = oslen[f], lb = T.strlen_[f][jj];
+                        const uint4 ib = T.strbag[f][jj];
+                        const int L = max(la, lb);
+                        const int gap = abs(la - lb);
+                        const int D = (int)(__vsadu4(obag[f].x, ib.x) + __vsadu4(obag[f].y, ib.y) +
+                                            __vsadu4(obag[f].z, ib.z) + __vsadu4(obag[f].w, ib.w));
+                        const int lower = max(gap, (D + gap + 1) >> 1);
+                        const bool present = (la >= 0) & (lb >= 0);
+#pragma unroll
+                        for (int z = 0; z < MAX_FSLOTS; z++) {
+                            if (z < RB_STR_NS(f)) {
+                                const FSlot& fs = F.str_slot[f][z];
+                                const int mg = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap0) ? tab[fs.off0 + L] : INT_MAX;
+                                const int md = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap1) ? tab[fs.off1 + L] : INT_MAX;
+                                const bool ok = present & ((L == 0) | ((gap <= mg) & (lower <= md)));
+                                if (!ok) alive &= ~(Mask)fs.kill;
+                            }
+                        }
+                    }
+                }
+
+                const bool surv = alive != 0;
+                const unsigned bal = __ballot_sync(FULL, surv);
+                if (bal) {
+                    if (surv) q[qn + __popc(bal & lt_mask)] = make_int2(ti, T.tid[jj]);
+                    qn += __popc(bal);
+                    my_surv += surv ? 1 : 0;
+                    if (qn > QCAP - 32) {
+                        __syncwarp();
+                        drain_queue(V, R, q, qn, cp_rule, scratch);
+                        __syncwarp();
+                        qn = 0;
+                    }
+                }
+            }
+        }
+        if (qn) {
+            __syncwarp();
+            drain_queue(V, R, q, qn, cp_rule, scratch);
+            __syncwarp();
+            qn = 0;
+        }
+    }
+
+    // ---- statistics
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        my_pairs += __shfl_down_sync(FULL, my_pairs, o);
+        my_surv += __shfl_down_sync(FULL, my_surv, o);
+    }
+    if (lane == 0) {
+        atomicAdd(R.stat_pairs, my_pairs);
+        atomicAdd(R.stat_surv, my_surv);
+    }
+}
+
+}  // namespace rb
+
+#ifdef RB_SPEC
+extern "C" __global__ void __launch_bounds__(rb::BLOCK, SPEC_MINBLOCKS)
+    rb_pair_kernel_spec(const __grid_constant__ rb::FilterPlan F, const __grid_constant__ rb::VerifyProg V,
+                        const __grid_constant__ rb::RunParams R) {
+    rb::pair_body<SPEC_MASK>(F, V, R);
+}
+#endif

@@ -92,6 +92,8 @@ class RunStats:
     n_intervals: int = 0
     kernel_ms: float = 0.0
     launches: int = 0
+    specialized: bool = False  # the NVRTC-specialised pair kernel ran
+    jit_log: str = ""
 
     def total_comparisons(self) -> int:
         return sum(b.comparisons for b in self.blocks)
@@ -270,6 +272,13 @@ class PathProgram:
         )
         self.handle = h
         self._fin = weakref.finalize(self, lib().rb_program_destroy, h)
+        spec = _lib.ctypes.c_int32(0)
+        cms = _lib.ctypes.c_double(0)
+        log = _lib.ctypes.c_char_p()
+        check(lib().rb_program_kernel_info(h, _lib.ctypes.byref(spec), _lib.ctypes.byref(cms), _lib.ctypes.byref(log)))
+        self.specialized = bool(spec.value)
+        self.jit_compile_ms = float(cms.value)
+        self.jit_log = (log.value or b"").decode(errors="replace")
 
     def close(self) -> None:
         self._fin()
@@ -383,6 +392,8 @@ def _candidates(prog: PathProgram, rows, st, cfg: EngineConfig, n_outer: int, wa
         n_intervals=max(1, -(-n_outer // cfg.n_t)),
         kernel_ms=float(st.kernel_ms),
         launches=int(st.launches),
+        specialized=bool(st.specialized),
+        jit_log=prog.jit_log,
     )
     return CandidateSet(stats=stats, arrays=(t, s, r), rule_ids=prog.rule_ids)
 

@@ -27,8 +27,19 @@ def gpu_rows(rel, path, case, prog=None):
     return sorted(cs.pairs), cs
 
 
+@pytest.fixture(params=["specialized", "generic"])
+def kernel_flavour(request, monkeypatch):
+    """Run every case through the NVRTC-specialised kernel and through the
+    generic (statically built) kernel."""
+    if request.param == "generic":
+        monkeypatch.setenv("RB_JIT", "0")
+    else:
+        monkeypatch.delenv("RB_JIT", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("name", NAMES)
-def test_gpu_matches_reference_golden(name):
+def test_gpu_matches_reference_golden(name, kernel_flavour):
     rel, path, cases = goldens.load(name)
     for case in cases:
         got, cs = gpu_rows(rel, path, case)
@@ -36,6 +47,7 @@ def test_gpu_matches_reference_golden(name):
         assert cs.stats.total_comparisons() == case["comparisons"], f"{name}/{case['name']}"
         evals = cs.stats.blocks[0].slot_evals
         assert (evals <= cs.stats.total_comparisons()).all()
+        assert cs.stats.specialized == (kernel_flavour == "specialized"), cs.stats.jit_log
 
 
 def test_empty_and_singleton_partitions():
