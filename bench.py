@@ -243,12 +243,16 @@ def main():
             barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
+            h0 = time.perf_counter()
             e0.record(stream)
             rows, st = prog.run_raw(None, w.n, RB_SYMMETRIC)
             e1.record(stream)
             torch.cuda.synchronize()
+            h1 = time.perf_counter()
             times.append(e0.elapsed_time(e1))
             kms.append(st.kernel_ms)
+            print(f"step: events {times[-1]:.1f} ms, kernel {st.kernel_ms:.1f} ms, host {1e3 * (h1 - h0):.1f} ms, "
+                  f"survivors {st.survivors}, rows {len(rows[0])}", file=sys.stderr)
             assert st.comparisons == pairs_step and len(rows[0]) == n_rows
     barrier()
     t_total = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")

@@ -73,6 +73,10 @@ struct rb_ctx {
     int blocks_per_sm = 1;
     DevBuf items, refs, counters, scratch;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // output buffers of the last destroyed result, reused by the next run
+    int32_t* pool[3] = {nullptr, nullptr, nullptr};
+    long long pool_cap = 0;
+    unsigned long long* host_ctr = nullptr;  // pinned: counters read back after each run
 };
 
 struct rb_rel {
@@ -98,6 +102,8 @@ struct rb_prog {
 };
 
 struct rb_result {
+    rb_ctx* ctx = nullptr;
+    long long cap = 0;
     int64_t count = 0;
     int32_t* d_t = nullptr;
     int32_t* d_s = nullptr;
@@ -134,6 +140,10 @@ int rb_ctx_create(int device, rb_ctx** out) {
     }
     c->own_stream = true;
     c->blocks_per_sm = pair_kernel_blocks_per_sm();
+    if (cudaMallocHost(&c->host_ctr, sizeof(unsigned long long) * (4 + RB_MAX_SLOTS)) != cudaSuccess) {
+        cudaGetLastError();
+        c->host_ctr = nullptr;
+    }
     *out = c;
     return RB_OK;
 }
@@ -157,6 +167,9 @@ int rb_ctx_destroy(rb_ctx* c) {
     c->scratch.release();
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    for (int k = 0; k < 3; k++)
+        if (c->pool[k]) cudaFree(c->pool[k]);
+    if (c->host_ctr) cudaFreeHost(c->host_ctr);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return RB_OK;
@@ -413,10 +426,12 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
         bool tok;
         int feat, z;
         int64_t src0, len0, src1, len1;
+        int64_t nmax, mmax;  // jaccard: longest token row on the t / s side
     };
     std::vector<TabReq> treq;
     std::map<std::pair<int, int>, int> eqf, tokf, strf;
     std::map<int, int> constf;
+    std::vector<int> cls(n_slots, -1);  // 0: eq/const filter, 1+f: token feature f, -1: not filtered
     for (int s = 0; s < n_slots; s++) {
         const rb_slot& sl = slots[s];
         const uint64_t kill = kill_of(s);
@@ -435,6 +450,7 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                 F.eq_inner[f] = R.codes;
             }
             F.eq_kill[f] |= kill;
+            cls[s] = 0;
         } else if (sl.kind == RB_SLOT_EQ_CONST) {
             auto it = constf.find(sl.lhs);
             int f;
@@ -446,6 +462,7 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                 F.const_mask[f] = L.mask;
             }
             F.const_kill[f] |= kill;
+            cls[s] = 0;
         } else if (sl.kind == RB_SLOT_JACCARD || sl.kind == RB_SLOT_EXACT) {
             auto it = tokf.find(key);
             int f;
@@ -475,8 +492,12 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             fs = FSlot{};
             fs.kill = kill;
             fs.kind = sl.kind;
-            if (sl.kind == RB_SLOT_JACCARD) treq.push_back({true, f, at, sl.tab0, sl.len0, sl.tab1, sl.len1});
+            if (sl.kind == RB_SLOT_JACCARD)
+                treq.push_back({true, f, at, sl.tab0, sl.len0, sl.tab1, sl.len1, rel->max_len[sl.lhs],
+                                rel->max_len[sl.rhs]});
             F.tok_rules[f] |= kill;
+            F.tok_kill[f] |= kill;
+            cls[s] = 1 + f;
         } else if (sl.kind == RB_SLOT_EDIT) {
             auto it = strf.find(key);
             int f;
@@ -495,18 +516,60 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             FSlot& fs = F.str_slot[f][at];
             fs.kill = kill;
             fs.kind = sl.kind;
-            treq.push_back({false, f, at, sl.tab0, sl.len0, sl.tab1, sl.len1});
+            treq.push_back({false, f, at, sl.tab0, sl.len0, sl.tab1, sl.len1, 0, 0});
             F.str_rules[f] |= kill;
+            F.str_kill[f] |= kill;
+        }
+    }
+    // a token feature is "always" needed when some rule using it has no slot
+    // filtered before it: then every warp with a valid pair evaluates it
+    for (int f = 0; f < F.n_tok; f++) {
+        for (size_t r = 0; r < need.size(); r++) {
+            bool uses = false, earlier = false;
+            for (int s = 0; s < n_slots; s++) {
+                if (!(need[r] & (1ull << s))) continue;
+                if (cls[s] == 1 + f) uses = true;
+                if (cls[s] >= 0 && cls[s] < 1 + f) earlier = true;
+            }
+            if (uses && !earlier) F.tok_always[f] = 1;
         }
     }
     std::vector<int32_t> stab(TAB_BASE, 0);  // guard entries: lookups of missing (-1) lengths land here
     {
-        int64_t total = TAB_BASE;
-        for (auto& t : treq) total += t.len0 + t.len1;
-        const bool full = total <= SMEM_TAB;
+        // jaccard slots prefer one 2-D table need[n][m] (n in [0,nmax], m in
+        // [-1,mmax]) folding both length tests: a single lookup per pair
+        int64_t total1d = TAB_BASE, total2d = TAB_BASE;
+        for (auto& t : treq) {
+            total1d += t.len0 + t.len1;
+            total2d += t.tok ? (t.nmax + 1) * (t.mmax + 2) : t.len0 + t.len1;
+        }
+        F.tok2d = total2d <= SMEM_TAB ? 1 : 0;
+        const bool full = F.tok2d || total1d <= SMEM_TAB;
         const int64_t per = treq.empty() ? 0 : std::max<int64_t>(1, (SMEM_TAB - TAB_BASE) / (2 * (int64_t)treq.size()));
+        const int32_t INF = 1 << 30;
         for (auto& t : treq) {
             FSlot& fs = t.tok ? F.tok_slot[t.feat][t.z] : F.str_slot[t.feat][t.z];
+            if (t.tok && F.tok2d) {
+                const int32_t* minsmall = tables + t.src0;
+                const int32_t* mink = tables + t.src1;
+                fs.w2 = (int32_t)(t.mmax + 2);
+                fs.off0 = (int32_t)stab.size();
+                fs.cap0 = (int32_t)((t.nmax + 1) * fs.w2);
+                for (int64_t nn = 0; nn <= t.nmax; nn++)
+                    for (int64_t mm = -1; mm <= t.mmax; mm++) {
+                        int32_t v = INF;
+                        if (mm >= 0 && (nn | mm) != 0) {
+                            const int64_t small = std::min(nn, mm), big = std::max(nn, mm);
+                            const int32_t ms = big < t.len0 ? minsmall[big] : 0;
+                            const int32_t mk = nn + mm < t.len1 ? mink[nn + mm] : INF;
+                            if (small >= ms && mk <= small) v = mk;
+                        }
+                        stab.push_back(v);
+                    }
+                fs.off1 = fs.off0;
+                fs.cap1 = fs.cap0;
+                continue;
+            }
             const int64_t c0 = full ? t.len0 : std::min(t.len0, per);
             const int64_t c1 = full ? t.len1 : std::min(t.len1, per);
             fs.off0 = (int32_t)stab.size();
@@ -584,10 +647,11 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     row_lo = std::max<int64_t>(0, row_lo);
     row_hi = std::min<int64_t>(row_hi, split >= 0 ? split : n);
 
-    // ---- work items: BLOCK outer rows x CHUNK inner columns
+    // ---- work items: BLOCK * rows outer rows x CHUNK inner columns
+    const int64_t rows_per_item = (int64_t)BLOCK * (P->jit.ok ? P->jit.rows : 1);
     std::vector<int4> items;
-    for (int64_t r0 = row_lo; r0 < row_hi; r0 += BLOCK) {
-        const int64_t rhi = std::min<int64_t>(r0 + BLOCK, row_hi);
+    for (int64_t r0 = row_lo; r0 < row_hi; r0 += rows_per_item) {
+        const int64_t rhi = std::min<int64_t>(r0 + rows_per_item, row_hi);
         int64_t c0 = mode == MODE_CROSS ? split : (mode == MODE_SYM ? r0 + 1 : 0);
         for (; c0 < n; c0 += CHUNK)
             items.push_back(make_int4((int)r0, (int)c0, (int)std::min<int64_t>(c0 + CHUNK, n), (int)rhi));
@@ -621,14 +685,24 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
 
     long long cap = std::max<long long>(1 << 20, P->last_rows + P->last_rows / 4);
     unsigned long long* ctr = (unsigned long long*)c->counters.p;
+    res->ctx = c;
     for (int attempt = 0;; attempt++) {
-        res->d_t = nullptr;
-        res->d_s = nullptr;
-        res->d_r = nullptr;
-        cudaError_t e = cudaMalloc(&res->d_t, sizeof(int32_t) * cap);
-        if (!e) e = cudaMalloc(&res->d_s, sizeof(int32_t) * cap);
-        if (!e) e = cudaMalloc(&res->d_r, sizeof(int32_t) * cap);
-        if (e) return cleanup(fail(RB_ERR_OOM, "output buffer of %lld rows: %s", cap, cudaGetErrorString(e)));
+        if (c->pool[0] && c->pool_cap >= cap) {  // reuse the pooled buffers
+            res->d_t = c->pool[0];
+            res->d_s = c->pool[1];
+            res->d_r = c->pool[2];
+            cap = c->pool_cap;
+            c->pool[0] = c->pool[1] = c->pool[2] = nullptr;
+            c->pool_cap = 0;
+        } else {
+            res->d_t = res->d_s = res->d_r = nullptr;
+            cudaError_t e = cudaMalloc(&res->d_t, sizeof(int32_t) * cap);
+            if (!e) e = cudaMalloc(&res->d_s, sizeof(int32_t) * cap);
+            if (!e) e = cudaMalloc(&res->d_r, sizeof(int32_t) * cap);
+            if (e) return cleanup(fail(RB_ERR_OOM, "output buffer of %lld rows: %s", cap, cudaGetErrorString(e)));
+        }
+        res->cap = cap;
+        cudaError_t e;
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * n_counters, c->stream));
 
         RunParams R{};
@@ -655,8 +729,9 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
                       : launch_pair_kernel(P->F, P->V, R, grid, c->stream);
         if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel launch: %s", cudaGetErrorString(e)));
         CK(cudaEventRecord(c->ev1, c->stream));
-        unsigned long long host_ctr[n_counters];
-        CK(cudaMemcpyAsync(host_ctr, ctr, sizeof host_ctr, cudaMemcpyDeviceToHost, c->stream));
+        unsigned long long stack_ctr[n_counters];
+        unsigned long long* host_ctr = c->host_ctr ? c->host_ctr : stack_ctr;
+        CK(cudaMemcpyAsync(host_ctr, ctr, sizeof(unsigned long long) * n_counters, cudaMemcpyDeviceToHost, c->stream));
         e = cudaStreamSynchronize(c->stream);
         if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel: %s", cudaGetErrorString(e)));
         float ms = 0;
@@ -679,6 +754,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         cudaFree(res->d_t);
         cudaFree(res->d_s);
         cudaFree(res->d_r);
+        res->d_t = res->d_s = res->d_r = nullptr;
         cap = rows;
     }
     *out = res;
@@ -730,6 +806,16 @@ int rb_result_stats(const rb_result* r, rb_stats* out) {
 
 int rb_result_destroy(rb_result* r) {
     if (!r) return RB_OK;
+    rb_ctx* c = r->ctx;
+    if (c && r->d_t && r->cap > c->pool_cap) {  // keep the larger buffers for the next run
+        for (int k = 0; k < 3; k++)
+            if (c->pool[k]) cudaFree(c->pool[k]);
+        c->pool[0] = r->d_t;
+        c->pool[1] = r->d_s;
+        c->pool[2] = r->d_r;
+        c->pool_cap = r->cap;
+        r->d_t = r->d_s = r->d_r = nullptr;
+    }
     if (r->d_t) cudaFree(r->d_t);
     if (r->d_s) cudaFree(r->d_s);
     if (r->d_r) cudaFree(r->d_r);

@@ -102,7 +102,7 @@ struct FSlot {
     int32_t kind;
     int32_t off0, cap0;
     int32_t off1, cap1;
-    int32_t pad;
+    int32_t w2;  // jaccard in 2-D mode: need[n][m] at off0 + n*w2 + (m+1)
 };
 
 // Phase-1 filter program.  Per pair the kernel keeps the set of rules that
@@ -111,7 +111,9 @@ struct FSlot {
 // exact-safe bounds.  Survivors are re-evaluated exactly.
 struct FilterPlan {
     int32_t n_eq, n_tok, n_str, n_const, n_rules, n_tab;
-    int32_t full_tab, pad_;  // full_tab: every shared table covers its column's longest row
+    int32_t full_tab;  // every shared table covers its column's longest row
+    int32_t rows;      // outer rows per thread of the kernel that will run (items cover BLOCK * rows)
+    int32_t tok2d;     // jaccard thresholds as one 2-D table need[n][m] per slot (see FSlot)
     uint64_t all_rules;
     const int32_t* tab_src;  // n_tab int32 entries copied to shared memory
     const int32_t* eq_outer[MAX_EQ];
@@ -128,7 +130,9 @@ struct FilterPlan {
     const uint2* tok_ihash[MAX_TOK];
     int32_t tok_nslots[MAX_TOK];  // slots on the feature: the first tok_njac are jaccard, the rest exact_token
     int32_t tok_njac[MAX_TOK];
+    int32_t tok_always[MAX_TOK];  // some rule reaches this feature with nothing filtered before it
     uint64_t tok_rules[MAX_TOK];
+    uint64_t tok_kill[MAX_TOK];  // OR of the feature's slot kills: an outer row without tokens fails them all
     FSlot tok_slot[MAX_TOK][MAX_FSLOTS];
     const int32_t* str_olen[MAX_STR];
     const uint4* str_obag[MAX_STR];
@@ -136,6 +140,7 @@ struct FilterPlan {
     const uint4* str_ibag[MAX_STR];
     int32_t str_nslots[MAX_STR];
     uint64_t str_rules[MAX_STR];
+    uint64_t str_kill[MAX_STR];  // a missing outer string fails every slot on the feature
     FSlot str_slot[MAX_STR][MAX_FSLOTS];
 };
 
@@ -382,8 +387,10 @@ struct __align__(16) Tile {
 #define RB_NSTR SPEC_NSTR
 #define RB_TOK_NS(f) ((f) == 0 ? SPEC_TOK0_NS : SPEC_TOK1_NS)
 #define RB_TOK_NJ(f) ((f) == 0 ? SPEC_TOK0_NJ : SPEC_TOK1_NJ)
+#define RB_TOK_ALWAYS(f) ((f) == 0 ? SPEC_TOK0_ALWAYS : SPEC_TOK1_ALWAYS)
 #define RB_STR_NS(f) ((f) == 0 ? SPEC_STR0_NS : SPEC_STR1_NS)
 #define RB_FULLTAB SPEC_FULLTAB
+#define RB_TOK2D SPEC_TOK2D
 #else
 #define RB_NEQ F.n_eq
 #define RB_NCONST F.n_const
@@ -391,56 +398,44 @@ struct __align__(16) Tile {
 #define RB_NSTR F.n_str
 #define RB_TOK_NS(f) F.tok_nslots[f]
 #define RB_TOK_NJ(f) F.tok_njac[f]
+#define RB_TOK_ALWAYS(f) F.tok_always[f]
 #define RB_STR_NS(f) F.str_nslots[f]
 #define RB_FULLTAB F.full_tab
+#define RB_TOK2D F.tok2d
 #endif
 
 // Shared tables start at TAB_BASE so that the (discarded) lookups of pairs
 // with a missing side, whose lengths are -1, stay inside the array.
 constexpr int TAB_BASE = 2;
 
-// Mask = uint32_t when the path has <= 32 checkpoints, else uint64_t.
+template <bool B>
+struct BoolC {
+    static constexpr bool value = B;
+};
+
+// One outer tuple held in registers for a whole work item.
 template <typename Mask>
-__device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg& V, const RunParams& R) {
-    __shared__ Tile T;
-    __shared__ int2 queue[NWARPS][QCAP];
-    __shared__ int32_t tab[SMEM_TAB];
-    __shared__ int cp_rule[MAX_RULES];
-    __shared__ int s_item;
+struct Outer {
+    int64_t i;
+    int32_t ti;
+    bool ok;
+    Mask alive0;  // rules still possible after the t-only tests
+    int32_t jj_lo, jj_skip;
+    int32_t ocode[MAX_EQ];
+    int32_t olen[MAX_TOK], orem[MAX_TOK];
+    int32_t orow[MAX_TOK][MAX_FSLOTS];
+    uint32_t lev[MAX_TOK][4];
+    uint2 ohash[MAX_TOK];
+    int32_t oslen[MAX_STR];
+    uint4 obag[MAX_STR];
 
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const unsigned FULL = 0xffffffffu;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    int2* q = queue[warp];
-    int qn = 0;
-    unsigned long long my_pairs = 0, my_surv = 0;
-    int32_t* scratch = R.scratch + (int64_t)(blockIdx.x * BLOCK + threadIdx.x) * R.scratch_stride;
-
-    for (int k = threadIdx.x; k < MAX_RULES; k += BLOCK) cp_rule[k] = V.cp_rule[k];
-    for (int k = threadIdx.x; k < F.n_tab; k += BLOCK) tab[k] = F.tab_src[k];
-
-    for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_item = (int)atomicAdd(R.item_counter, 1u);
-        __syncthreads();
-        const int it = s_item;
-        if (it >= R.n_items) break;
-        const int4 item = R.items[it];
-        const int64_t i = (int64_t)item.x + threadIdx.x;
-        const int64_t col0 = item.y, col1 = item.z;
-        const bool row_ok = i < (int64_t)item.w;
-
-        // ---- outer tuple -> registers
-        int32_t ti = 0;
-        Mask alive0 = 0;
-        int32_t ocode[MAX_EQ];
-        int32_t olen[MAX_TOK], orem[MAX_TOK];
-        uint32_t lev[MAX_TOK][4];
-        uint2 ohash[MAX_TOK];
-        int32_t oslen[MAX_STR];
-        uint4 obag[MAX_STR];
-        if (row_ok) {
+    __device__ __forceinline__ void load(const FilterPlan& F, const RunParams& R, int64_t i_, int64_t row_hi,
+                                         int64_t col0, int64_t col1, unsigned long long& my_pairs) {
+        i = i_;
+        ok = i < row_hi;
+        ti = 0;
+        alive0 = 0;
+        if (ok) {
             ti = R.refs ? R.refs[i] : (int32_t)i;
             alive0 = (Mask)F.all_rules;
             if (R.mode == MODE_SYM) {
@@ -455,7 +450,7 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
 #pragma unroll
         for (int f = 0; f < MAX_EQ; f++) {
             ocode[f] = INT_MIN;  // never equals an inner code (those are >= -2)
-            if (f < RB_NEQ && row_ok) {
+            if (f < RB_NEQ && ok) {
                 const int32_t c = __ldg(F.eq_outer[f] + ti);
                 if (c >= 0)
                     ocode[f] = c;
@@ -465,7 +460,7 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
         }
 #pragma unroll
         for (int k = 0; k < MAX_CONST; k++)
-            if (k < RB_NCONST && row_ok && !__ldg(F.const_mask[k] + ti)) alive0 &= ~(Mask)F.const_kill[k];
+            if (k < RB_NCONST && ok && !__ldg(F.const_mask[k] + ti)) alive0 &= ~(Mask)F.const_kill[k];
 #pragma unroll
         for (int f = 0; f < MAX_TOK; f++) {
             olen[f] = -1;
@@ -473,9 +468,19 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
             ohash[f] = make_uint2(0, 0);
 #pragma unroll
             for (int w = 0; w < 4; w++) lev[f][w] = 0;
-            if (f < RB_NTOK && row_ok) {
+#pragma unroll
+            for (int z = 0; z < MAX_FSLOTS; z++) orow[f][z] = 0;
+            if (f < RB_NTOK && ok) {
                 olen[f] = __ldg(F.tok_olen[f] + ti);
                 ohash[f] = __ldg(F.tok_ohash[f] + ti);
+                // jaccard and exact_token are false for a missing or empty t side
+                if (olen[f] <= 0) alive0 &= ~(Mask)F.tok_kill[f];
+                if (RB_TOK2D) {
+                    const int nn = olen[f] > 0 ? olen[f] : 0;
+#pragma unroll
+                    for (int z = 0; z < MAX_FSLOTS; z++)
+                        if (z < RB_TOK_NJ(f)) orow[f][z] = F.tok_slot[f][z].off0 + nn * F.tok_slot[f][z].w2 + 1;
+                }
                 const int64_t a = __ldg(F.tok_ooff[f] + ti), b = __ldg(F.tok_ooff[f] + ti + 1);
                 for (int64_t k = a; k < b; k++) {
                     const uint32_t bit = sig_bit(__ldg(F.tok_oids[f] + k));
@@ -495,13 +500,180 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
         for (int f = 0; f < MAX_STR; f++) {
             oslen[f] = -1;
             obag[f] = make_uint4(0, 0, 0, 0);
-            if (f < RB_NSTR && row_ok) {
+            if (f < RB_NSTR && ok) {
                 oslen[f] = __ldg(F.str_olen[f] + ti);
                 obag[f] = __ldg(F.str_obag[f] + ti);
+                if (oslen[f] < 0) alive0 &= ~(Mask)F.str_kill[f];  // missing t side: edit is false
+            }
+        }
+    }
+
+    // valid(jj) <=> jj >= jj_lo && jj != jj_skip, for the tile starting at jt
+    __device__ __forceinline__ bool tile(const RunParams& R, int64_t jt) {
+        jj_lo = 0;
+        jj_skip = -1;
+        if (!ok) {
+            jj_lo = TJ + 1;
+        } else if (R.mode == MODE_SYM) {
+            const int64_t d = i - jt + 1;
+            jj_lo = d < 0 ? 0 : (d > TJ + 1 ? TJ + 1 : (int)d);
+        } else if (R.mode == MODE_ASYM) {
+            const int64_t d = i - jt;
+            jj_skip = (d >= 0 && d < TJ) ? (int)d : -1;
+        }
+        return jj_lo == 0 && jj_skip < 0;
+    }
+};
+
+// The per-pair filter over one shared tile for ROWS outer tuples per thread.
+// AllValid: every (outer, jj) pair of the warp is inside the pair space.
+template <typename Mask, int ROWS, bool AllValid>
+__device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg& V, const RunParams& R, const Tile& T,
+                                          const int32_t* tab, Outer<Mask> (&o)[ROWS], int tn, int2* q, int& qn,
+                                          const int* cp_rule, int32_t* scratch, unsigned long long& my_surv) {
+    const unsigned FULL = 0xffffffffu;
+    const unsigned lt_mask = (1u << (threadIdx.x & 31)) - 1u;
+    for (int jj = 0; jj < tn; jj++) {
+        Mask alive[ROWS];
+#pragma unroll
+        for (int r = 0; r < ROWS; r++) {
+            alive[r] = (AllValid || (jj >= o[r].jj_lo && jj != o[r].jj_skip)) ? o[r].alive0 : (Mask)0;
+#pragma unroll
+            for (int f = 0; f < MAX_EQ; f++)
+                if (f < RB_NEQ && o[r].ocode[f] != T.eq[f][jj]) alive[r] &= ~(Mask)F.eq_kill[f];
+        }
+
+#pragma unroll
+        for (int f = 0; f < MAX_TOK; f++) {
+            if (f >= RB_NTOK) continue;
+            Mask need = 0;
+#pragma unroll
+            for (int r = 0; r < ROWS; r++) need |= alive[r];
+            if (!RB_TOK_ALWAYS(f) && !__any_sync(FULL, (need & (Mask)F.tok_rules[f]) != 0)) continue;
+            const int m = T.toklen[f][jj];
+            const uint4 is = T.toksig[f][jj];
+            const uint2 h = T.tokhash[f][jj];
+#pragma unroll
+            for (int r = 0; r < ROWS; r++) {
+                // u >= |A n B| (see the header); rows with n <= 0 were killed at load
+                const int u = __popc(o[r].lev[f][0] & is.x) + __popc(o[r].lev[f][1] & is.y) +
+                              __popc(o[r].lev[f][2] & is.z) + __popc(o[r].lev[f][3] & is.w) + o[r].orem[f];
+                const int n = o[r].olen[f];
+#pragma unroll
+                for (int z = 0; z < MAX_FSLOTS; z++) {
+                    if (z < RB_TOK_NS(f)) {
+                        const FSlot& fs = F.tok_slot[f][z];
+                        bool ok;
+                        if (z < RB_TOK_NJ(f)) {  // jaccard: exact integer tables
+                            if (RB_TOK2D) {
+                                // need[n][m]: INF unless the length tests pass, else mink[n+m]
+                                ok = u >= tab[o[r].orow[f][z] + m];
+                            } else {
+                                const bool live = m >= 0;
+                                const int small = min(n, m), big = max(n, m);
+                                const int ms =
+                                    (RB_FULLTAB || (unsigned)big < (unsigned)fs.cap0) ? tab[fs.off0 + big] : 0;
+                                const int mk =
+                                    (RB_FULLTAB || (unsigned)(n + m) < (unsigned)fs.cap1) ? tab[fs.off1 + n + m] : 0;
+                                ok = live & (small >= ms) & (min(u, small) >= mk);
+                            }
+                        } else {  // exact_token: the id-list hash (seeded with the length) must match
+                            ok = (h.x == o[r].ohash[f].x) & (h.y == o[r].ohash[f].y);
+                        }
+                        if (!ok) alive[r] &= ~(Mask)fs.kill;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < MAX_STR; f++) {
+            if (f >= RB_NSTR) continue;
+            Mask need = 0;
+#pragma unroll
+            for (int r = 0; r < ROWS; r++) need |= alive[r];
+            if (!__any_sync(FULL, (need & (Mask)F.str_rules[f]) != 0)) continue;
+            const int lb = T.strlen_[f][jj];
+            const uint4 ib = T.strbag[f][jj];
+#pragma unroll
+            for (int r = 0; r < ROWS; r++) {
+                const int la = o[r].oslen[f];
+                const int L = max(la, lb);
+                const int gap = abs(la - lb);
+                const int D = (int)(__vsadu4(o[r].obag[f].x, ib.x) + __vsadu4(o[r].obag[f].y, ib.y) +
+                                    __vsadu4(o[r].obag[f].z, ib.z) + __vsadu4(o[r].obag[f].w, ib.w));
+                const int lower = max(gap, (D + gap + 1) >> 1);
+                const bool present = lb >= 0;  // a missing t side was killed at load
+#pragma unroll
+                for (int z = 0; z < MAX_FSLOTS; z++) {
+                    if (z < RB_STR_NS(f)) {
+                        const FSlot& fs = F.str_slot[f][z];
+                        const int mg = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap0) ? tab[fs.off0 + L] : INT_MAX;
+                        const int md = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap1) ? tab[fs.off1 + L] : INT_MAX;
+                        const bool ok = present & ((L == 0) | ((gap <= mg) & (lower <= md)));
+                        if (!ok) alive[r] &= ~(Mask)fs.kill;
+                    }
+                }
             }
         }
 
-        // ---- stream inner tiles
+        // ---- survivors -> the warp's queue (ballot + popc compaction)
+        bool any_surv = false;
+#pragma unroll
+        for (int r = 0; r < ROWS; r++) any_surv |= alive[r] != 0;
+        if (__any_sync(FULL, any_surv)) {
+#pragma unroll
+            for (int r = 0; r < ROWS; r++) {
+                const bool surv = alive[r] != 0;
+                const unsigned bal = __ballot_sync(FULL, surv);
+                if (surv) q[qn + __popc(bal & lt_mask)] = make_int2(o[r].ti, T.tid[jj]);
+                qn += __popc(bal);
+                my_surv += surv ? 1 : 0;
+            }
+            if (qn > QCAP - 32 * ROWS) {
+                __syncwarp();
+                drain_queue(V, R, q, qn, cp_rule, scratch);
+                __syncwarp();
+                qn = 0;
+            }
+        }
+    }
+}
+
+// Mask = uint32_t when the path has <= 32 checkpoints, else uint64_t.
+// ROWS outer tuples per thread: a work item covers BLOCK * ROWS outer rows.
+template <typename Mask, int ROWS>
+__device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg& V, const RunParams& R) {
+    __shared__ Tile T;
+    __shared__ int2 queue[NWARPS][QCAP];
+    __shared__ int32_t tab[SMEM_TAB];
+    __shared__ int cp_rule[MAX_RULES];
+    __shared__ int s_item;
+
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const unsigned FULL = 0xffffffffu;
+    int2* q = queue[warp];
+    int qn = 0;
+    unsigned long long my_pairs = 0, my_surv = 0;
+    int32_t* scratch = R.scratch + (int64_t)(blockIdx.x * BLOCK + threadIdx.x) * R.scratch_stride;
+
+    for (int k = threadIdx.x; k < MAX_RULES; k += BLOCK) cp_rule[k] = V.cp_rule[k];
+    for (int k = threadIdx.x; k < F.n_tab; k += BLOCK) tab[k] = F.tab_src[k];
+
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_item = (int)atomicAdd(R.item_counter, 1u);
+        __syncthreads();
+        const int it = s_item;
+        if (it >= R.n_items) break;
+        const int4 item = R.items[it];
+        const int64_t col0 = item.y, col1 = item.z;
+
+        Outer<Mask> o[ROWS];
+#pragma unroll
+        for (int r = 0; r < ROWS; r++)
+            o[r].load(F, R, (int64_t)item.x + r * BLOCK + threadIdx.x, (int64_t)item.w, col0, col1, my_pairs);
+
         for (int64_t jt = col0; jt < col1; jt += TJ) {
             const int tn = (int)(col1 - jt < TJ ? col1 - jt : TJ);
             __syncthreads();
@@ -528,91 +700,13 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
             }
             __syncthreads();
 
-            // valid(jj) <=> jj >= jj_lo && jj != jj_skip
-            int jj_lo = 0, jj_skip = -1;
-            if (!row_ok) {
-                jj_lo = TJ + 1;
-            } else if (R.mode == MODE_SYM) {
-                const int64_t d = i - jt + 1;
-                jj_lo = d < 0 ? 0 : (d > TJ + 1 ? TJ + 1 : (int)d);
-            } else if (R.mode == MODE_ASYM) {
-                const int64_t d = i - jt;
-                jj_skip = (d >= 0 && d < TJ) ? (int)d : -1;
-            }
-
-            for (int jj = 0; jj < tn; jj++) {
-                Mask alive = (jj >= jj_lo && jj != jj_skip) ? alive0 : (Mask)0;
+            bool all_valid = true;
 #pragma unroll
-                for (int f = 0; f < MAX_EQ; f++)
-                    if (f < RB_NEQ && ocode[f] != T.eq[f][jj]) alive &= ~(Mask)F.eq_kill[f];
-
-#pragma unroll
-                for (int f = 0; f < MAX_TOK; f++) {
-                    if (f < RB_NTOK && __any_sync(FULL, (alive & (Mask)F.tok_rules[f]) != 0)) {
-                        const int m = T.toklen[f][jj];
-                        const uint4 is = T.toksig[f][jj];
-                        const int n = olen[f];
-                        const bool live = (n >= 0) & (m >= 0) & ((n | m) != 0);
-                        const int small = min(n, m), big = max(n, m);
-                        int u = __popc(lev[f][0] & is.x) + __popc(lev[f][1] & is.y) + __popc(lev[f][2] & is.z) +
-                                __popc(lev[f][3] & is.w) + orem[f];
-                        u = min(u, small);
-#pragma unroll
-                        for (int z = 0; z < MAX_FSLOTS; z++) {
-                            if (z < RB_TOK_NS(f)) {
-                                const FSlot& fs = F.tok_slot[f][z];
-                                bool ok;
-                                if (z < RB_TOK_NJ(f)) {  // jaccard: exact integer tables
-                                    const int ms = (RB_FULLTAB || (unsigned)big < (unsigned)fs.cap0) ? tab[fs.off0 + big] : 0;
-                                    const int mk = (RB_FULLTAB || (unsigned)(n + m) < (unsigned)fs.cap1) ? tab[fs.off1 + n + m] : 0;
-                                    ok = live & (small >= ms) & (u >= mk);
-                                } else {  // exact_token
-                                    const uint2 h = T.tokhash[f][jj];
-                                    ok = live & (n == m) & (h.x == ohash[f].x) & (h.y == ohash[f].y);
-                                }
-                                if (!ok) alive &= ~(Mask)fs.kill;
-                            }
-                        }
-                    }
-                }
-#pragma unroll
-                for (int f = 0; f < MAX_STR; f++) {
-                    if (f < RB_NSTR && __any_sync(FULL, (alive & (Mask)F.str_rules[f]) != 0)) {
-                        const int la = oslen[f], lb = T.strlen_[f][jj];
-                        const uint4 ib = T.strbag[f][jj];
-                        const int L = max(la, lb);
-                        const int gap = abs(la - lb);
-                        const int D = (int)(__vsadu4(obag[f].x, ib.x) + __vsadu4(obag[f].y, ib.y) +
-                                            __vsadu4(obag[f].z, ib.z) + __vsadu4(obag[f].w, ib.w));
-                        const int lower = max(gap, (D + gap + 1) >> 1);
-                        const bool present = (la >= 0) & (lb >= 0);
-#pragma unroll
-                        for (int z = 0; z < MAX_FSLOTS; z++) {
-                            if (z < RB_STR_NS(f)) {
-                                const FSlot& fs = F.str_slot[f][z];
-                                const int mg = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap0) ? tab[fs.off0 + L] : INT_MAX;
-                                const int md = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap1) ? tab[fs.off1 + L] : INT_MAX;
-                                const bool ok = present & ((L == 0) | ((gap <= mg) & (lower <= md)));
-                                if (!ok) alive &= ~(Mask)fs.kill;
-                            }
-                        }
-                    }
-                }
-
-                const bool surv = alive != 0;
-                const unsigned bal = __ballot_sync(FULL, surv);
-                if (bal) {
-                    if (surv) q[qn + __popc(bal & lt_mask)] = make_int2(ti, T.tid[jj]);
-                    qn += __popc(bal);
-                    my_surv += surv ? 1 : 0;
-                    if (qn > QCAP - 32) {
-                        __syncwarp();
-                        drain_queue(V, R, q, qn, cp_rule, scratch);
-                        __syncwarp();
-                        qn = 0;
-                    }
-                }
-            }
+            for (int r = 0; r < ROWS; r++) all_valid &= o[r].tile(R, jt);
+            if (__all_sync(FULL, all_valid))
+                tile_loop<Mask, ROWS, true>(F, V, R, T, tab, o, tn, q, qn, cp_rule, scratch, my_surv);
+            else
+                tile_loop<Mask, ROWS, false>(F, V, R, T, tab, o, tn, q, qn, cp_rule, scratch, my_surv);
         }
         if (qn) {
             __syncwarp();
@@ -624,9 +718,9 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
 
     // ---- statistics
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        my_pairs += __shfl_down_sync(FULL, my_pairs, o);
-        my_surv += __shfl_down_sync(FULL, my_surv, o);
+    for (int o2 = 16; o2 > 0; o2 >>= 1) {
+        my_pairs += __shfl_down_sync(FULL, my_pairs, o2);
+        my_surv += __shfl_down_sync(FULL, my_surv, o2);
     }
     if (lane == 0) {
         atomicAdd(R.stat_pairs, my_pairs);
@@ -640,6 +734,6 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
 extern "C" __global__ void __launch_bounds__(rb::BLOCK, SPEC_MINBLOCKS)
     rb_pair_kernel_spec(const __grid_constant__ rb::FilterPlan F, const __grid_constant__ rb::VerifyProg V,
                         const __grid_constant__ rb::RunParams R) {
-    rb::pair_body<SPEC_MASK>(F, V, R);
+    rb::pair_body<SPEC_MASK, SPEC_ROWS>(F, V, R);
 }
 #endif

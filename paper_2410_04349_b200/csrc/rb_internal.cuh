@@ -28,6 +28,7 @@ struct JitKernel {
     bool ok = false;
     cudaKernel_t kernel = nullptr;
     int blocks_per_sm = 1;
+    int rows = 1;  // outer rows per thread
     double compile_ms = 0;
     std::string key;
     std::string log;

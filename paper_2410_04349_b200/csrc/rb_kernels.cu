@@ -88,10 +88,10 @@ cudaError_t launch_char_features(const int64_t* offsets, const void* chars, int3
 // the generic pair kernel (shape read from the kernel parameters)
 
 template <typename Mask>
-__global__ void __launch_bounds__(BLOCK, 3)
+__global__ void __launch_bounds__(BLOCK, 2)
     pair_kernel(const __grid_constant__ FilterPlan F, const __grid_constant__ VerifyProg V,
                 const __grid_constant__ RunParams R) {
-    pair_body<Mask>(F, V, R);
+    pair_body<Mask, 1>(F, V, R);
 }
 
 int pair_kernel_blocks_per_sm() {
