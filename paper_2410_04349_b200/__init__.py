@@ -17,6 +17,8 @@ from .engine import (
     context,
     run_cross,
     run_partition,
+    run_partition_rows,
+    split_rows_by_pairs,
 )
 from .errors import ConfigError, DataParseError, RuleBlockError, RuleParseError, SchemaError, ValidationError
 from .plan import Checkpoint, EvalPredicate, ExecutionPath, plan_from_stats
@@ -30,5 +32,5 @@ __all__ = [
     "EngineConfig", "EvalPredicate", "ExecutionPath", "Kind", "MDRule", "MISSING", "PathProgram", "Predicate",
     "Relation", "RelationEncoding", "RuleBlockError", "RuleParseError", "RuleSet", "RunStats", "Schema",
     "SchemaError", "TupleRecord", "ValidationError", "compile_program", "context", "parse_ruleset",
-    "plan_from_stats", "predicate_universe", "relation_from_rows", "run_cross", "run_partition",
+    "plan_from_stats", "predicate_universe", "relation_from_rows", "run_cross", "run_partition", "run_partition_rows", "split_rows_by_pairs",
 ]

@@ -295,7 +295,7 @@ class PathProgram:
             check(L.rb_run_cross(self.ctx.handle, self.drel.handle, self.handle, ptr(np.ascontiguousarray(left)),
                                  len(left), ptr(np.ascontiguousarray(right)), len(right), flags,
                                  _lib.ctypes.byref(res)))
-        elif row_lo == 0 and (row_hi is None or row_hi >= n):
+        elif row_lo <= 0 and (row_hi is None or row_hi >= n):
             check(L.rb_run_partition(self.ctx.handle, self.drel.handle, self.handle, ptr(refs_a), n, flags,
                                      _lib.ctypes.byref(res)))
         else:
@@ -409,6 +409,50 @@ def run_partition(partition, relation, path, cfg=None, reg=None, encoded=None, p
     refs = _refs_array(partition)
     rows, st = prog.run_raw(refs, len(refs), cfg.flags())
     return _candidates(prog, rows, st, cfg, len(refs), time.perf_counter() - started)
+
+
+def split_rows_by_pairs(n: int, parts: int, symmetric: bool = True) -> list[tuple[int, int]]:
+    """Cut outer positions [0, n) into `parts` contiguous ranges of (nearly)
+    equal pair counts -- row i owns n-1-i pairs in symmetric mode, n-1
+    otherwise.  The unit of multi-GPU sharding of one partition."""
+    if parts < 1:
+        raise ConfigError("parts must be >= 1")
+    if not symmetric:
+        cuts = [round(k * n / parts) for k in range(parts + 1)]
+    else:
+        total = n * (n - 1) // 2
+
+        def before(r: int) -> int:  # pairs owned by rows < r
+            return r * n - r * (r + 1) // 2
+
+        cuts = [0]
+        for k in range(1, parts):
+            goal = total * k // parts
+            lo, hi = cuts[-1], n
+            while lo < hi:
+                mid = (lo + hi) // 2
+                if before(mid) < goal:
+                    lo = mid + 1
+                else:
+                    hi = mid
+            cuts.append(lo)
+        cuts.append(n)
+    return [(cuts[k], cuts[k + 1]) for k in range(parts)]
+
+
+def run_partition_rows(partition, relation, path, row_lo: int, row_hi: int, cfg=None, reg=None, encoded=None,
+                       program=None) -> CandidateSet:
+    """The pairs of `partition` whose outer (t) position lies in [row_lo,
+    row_hi): one shard of run_partition.  The union over a split of [0, n)
+    equals run_partition exactly."""
+    cfg = cfg or EngineConfig()
+    if partition is None or len(partition.tuple_refs) == 0:
+        return CandidateSet(pairs=[])
+    started = time.perf_counter()
+    prog = _program_for(path, relation, reg, encoded, program)
+    refs = _refs_array(partition)
+    rows, st = prog.run_raw(refs, len(refs), cfg.flags(), row_lo=row_lo, row_hi=row_hi)
+    return _candidates(prog, rows, st, cfg, max(0, row_hi - row_lo), time.perf_counter() - started)
 
 
 def run_cross(left, right, relation, path, cfg=None, reg=None, encoded=None, program=None) -> CandidateSet:
