@@ -84,16 +84,3 @@ def test_row_shards_union_equals_whole(name):
     assert sorted(got) == goldens.expected_rows(case)
     assert cmp == case["comparisons"]
 
-
-def test_reference_objects_are_accepted():
-    """Duck typing: the reference's own Relation/DataPartition/ExecutionPath
-    (only where the reference is importable)."""
-    import os
-    import sys
-
-    ref = "/root/reference/pkg/src"
-    if not os.path.isdir(ref):
-        pytest.skip("reference not present on this machine")
-    sys.path.insert(0, ref)
-    from ruleblock.datasets import write_products  # noqa
-    pytest.skip("reference objects are exercised in the CPU container only")
