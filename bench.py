@@ -38,6 +38,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "tuple pairs evaluated/sec and blocking wall-time at 1/2/4/8 B200 vs CPU ref"
+WORKLOAD_DESC = {
+    "citation3": "BASELINE config 2: 3 rules mixing eq, jaccard and edit",
+    "edit_heavy": "BASELINE config 3: edit-distance-heavy rules, 64-256-char strings, maxd 2-5",
+}
 UNIT = "pairs/s"
 
 
@@ -175,7 +179,7 @@ def run_reference(args, rank, world):
         "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{w.name} n={w.n} (BASELINE config 2), one symmetric partition",
+        "config": {"workload": f"{w.name} n={w.n} ({WORKLOAD_DESC.get(w.name, w.name)}), one symmetric partition",
                    "pairs_per_step_full": total_pairs, "sample_pairs_per_step": pairs // args.steps},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{len(rows)} outer-row slices, {pairs // args.steps} pairs per step; "
@@ -310,8 +314,10 @@ def main():
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tfile):
-            try:
-                traffic = json.load(open(tfile)).get("bytes_per_launch")
+            try:  # ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, same workload and size
+                entry = json.load(open(tfile)).get(w.name, {})
+                if entry.get("n") == w.n:
+                    traffic = entry.get("bytes_per_launch")
             except Exception:
                 traffic = None
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -325,7 +331,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": f"{w.name} n={w.n} per GPU (BASELINE config 2: eq + jaccard + edit, 3 rules), "
+            "config": {"workload": f"{w.name} n={w.n} per GPU ({WORKLOAD_DESC.get(w.name, w.name)}), "
                                    "one symmetric partition per GPU",
                        "pairs_per_step_per_gpu": pairs_step, "rows_per_step_per_gpu": n_rows,
                        "l2": "flushed (512 MiB write) between timed steps", "parallelism": f"partition-per-gpu x{world}"},

@@ -142,8 +142,19 @@ int rb_run_partition_rows(rb_ctx* ctx, rb_rel* rel, rb_prog* prog, const int32_t
 int rb_run_cross(rb_ctx* ctx, rb_rel* rel, rb_prog* prog, const int32_t* left, int64_t nl, const int32_t* right,
                  int64_t nr, uint32_t flags, rb_result** out);
 
+/* batched run: n_parts partitions laid out back to back in refs, part k =
+ * refs[offsets[k] .. offsets[k+1]); splits[k] < 0 (or splits == NULL)
+ * evaluates part k as a partition (run_partition semantics), splits[k] >= 0
+ * as a cross run with left = its first splits[k] refs.  One launch for the
+ * whole batch; rb_result_copy_parts returns each row's part index.  This is
+ * the many-small-partitions shape of the reference pipeline
+ * (pipeline.py:177-209 running run_partition per task). */
+int rb_run_batch(rb_ctx* ctx, rb_rel* rel, rb_prog* prog, const int32_t* refs, const int64_t* offsets,
+                 const int64_t* splits, int32_t n_parts, uint32_t flags, rb_result** out);
+
 int rb_result_count(const rb_result* res, int64_t* rows);
 int rb_result_copy(const rb_result* res, int32_t* t, int32_t* s, int32_t* rule);
+int rb_result_copy_parts(const rb_result* res, int32_t* part);
 int rb_result_stats(const rb_result* res, rb_stats* out);
 int rb_result_destroy(rb_result* res);
 

@@ -16,7 +16,9 @@ from .engine import (
     RunStats,
     context,
     run_cross,
+    run_crosses,
     run_partition,
+    run_partitions,
     run_partition_rows,
     split_rows_by_pairs,
 )
@@ -32,5 +34,5 @@ __all__ = [
     "EngineConfig", "EvalPredicate", "ExecutionPath", "Kind", "MDRule", "MISSING", "PathProgram", "Predicate",
     "Relation", "RelationEncoding", "RuleBlockError", "RuleParseError", "RuleSet", "RunStats", "Schema",
     "SchemaError", "TupleRecord", "ValidationError", "compile_program", "context", "parse_ruleset",
-    "plan_from_stats", "predicate_universe", "relation_from_rows", "run_cross", "run_partition", "run_partition_rows", "split_rows_by_pairs",
+    "plan_from_stats", "predicate_universe", "relation_from_rows", "run_cross", "run_crosses", "run_partition", "run_partitions", "run_partition_rows", "split_rows_by_pairs",
 ]

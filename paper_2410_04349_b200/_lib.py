@@ -73,7 +73,9 @@ _SIGNATURES = {
         ctypes.c_int,
         [c_vp, c_vp, c_vp, c_vp, ctypes.c_int64, c_vp, ctypes.c_int64, ctypes.c_uint32, c_vpp],
     ),
+    "rb_run_batch": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int32, ctypes.c_uint32, c_vpp]),
     "rb_result_count": (ctypes.c_int, [c_vp, c_i64p]),
+    "rb_result_copy_parts": (ctypes.c_int, [c_vp, c_vp]),
     "rb_result_copy": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "rb_result_stats": (ctypes.c_int, [c_vp, ctypes.POINTER(RbStats)]),
     "rb_result_destroy": (ctypes.c_int, [c_vp]),

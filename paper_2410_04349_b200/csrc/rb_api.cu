@@ -108,6 +108,7 @@ struct rb_result {
     int32_t* d_t = nullptr;
     int32_t* d_s = nullptr;
     int32_t* d_r = nullptr;
+    int32_t* d_p = nullptr;  // batched runs: partition index per row
     cudaStream_t stream = nullptr;
     rb_stats stats{};
 };
@@ -431,7 +432,9 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
     std::vector<TabReq> treq;
     std::map<std::pair<int, int>, int> eqf, tokf, strf;
     std::map<int, int> constf;
-    std::vector<int> cls(n_slots, -1);  // 0: eq/const filter, 1+f: token feature f, -1: not filtered
+    // filter class of each slot, in evaluation order: 0 eq/const, 1+f token
+    // feature f, 1+MAX_TOK+f string feature f; -1 not filtered
+    std::vector<int> cls(n_slots, -1);
     for (int s = 0; s < n_slots; s++) {
         const rb_slot& sl = slots[s];
         const uint64_t kill = kill_of(s);
@@ -519,6 +522,7 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             treq.push_back({false, f, at, sl.tab0, sl.len0, sl.tab1, sl.len1, 0, 0});
             F.str_rules[f] |= kill;
             F.str_kill[f] |= kill;
+            cls[s] = 1 + MAX_TOK + f;
         }
     }
     // a token feature is "always" needed when some rule using it has no slot
@@ -532,6 +536,17 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                 if (cls[s] >= 0 && cls[s] < 1 + f) earlier = true;
             }
             if (uses && !earlier) F.tok_always[f] = 1;
+        }
+    }
+    for (int f = 0; f < F.n_str; f++) {
+        for (size_t r = 0; r < need.size(); r++) {
+            bool uses = false, earlier = false;
+            for (int s = 0; s < n_slots; s++) {
+                if (!(need[r] & (1ull << s))) continue;
+                if (cls[s] == 1 + MAX_TOK + f) uses = true;
+                if (cls[s] >= 0 && cls[s] < 1 + MAX_TOK + f) earlier = true;
+            }
+            if (uses && !earlier) F.str_always[f] = 1;
         }
     }
     std::vector<int32_t> stab(TAB_BASE, 0);  // guard entries: lookups of missing (-1) lengths land here
@@ -617,18 +632,22 @@ int rb_program_destroy(rb_prog* P) {
 // ---------------------------------------------------------------------------
 // runs
 
-static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t n, int64_t split, int64_t row_lo,
-               int64_t row_hi, uint32_t flags, rb_result** out) {
+struct Part {
+    int64_t base, n, split;  // split < 0: a partition; else cross, left = [base, base+split)
+};
+
+static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
+               int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out) {
     if (!c || !rel || !P || !out) return fail(RB_ERR_INVALID, "run: null argument");
     if (P->rel != rel || rel->ctx != c) return fail(RB_ERR_INVALID, "run: program/relation/context mismatch");
-    if (n < 0 || n > INT32_MAX) return fail(RB_ERR_INVALID, "run: partition size out of range");
+    if (total < 0 || total > INT32_MAX) return fail(RB_ERR_INVALID, "run: partition size out of range");
     if (refs) {
-        for (int64_t k = 0; k < n; k++)
+        for (int64_t k = 0; k < total; k++)
             if (refs[k] < 0 || refs[k] >= rel->n)
                 return fail(RB_ERR_INVALID, "tuple ref %d at position %lld outside the relation",
                             refs[k], (long long)k);
-    } else if (n > rel->n) {
-        return fail(RB_ERR_INVALID, "identity partition of %lld tuples exceeds the relation", (long long)n);
+    } else if (total > rel->n) {
+        return fail(RB_ERR_INVALID, "identity partition of %lld tuples exceeds the relation", (long long)total);
     }
     *out = nullptr;
     CK(cudaSetDevice(c->device));
@@ -639,30 +658,44 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         if (res->d_t) cudaFree(res->d_t);
         if (res->d_s) cudaFree(res->d_s);
         if (res->d_r) cudaFree(res->d_r);
+        if (res->d_p) cudaFree(res->d_p);
         delete res;
         return rc;
     };
 
-    const int32_t mode = split >= 0 ? MODE_CROSS : ((flags & RB_SYMMETRIC) ? MODE_SYM : MODE_ASYM);
-    row_lo = std::max<int64_t>(0, row_lo);
-    row_hi = std::min<int64_t>(row_hi, split >= 0 ? split : n);
-
-    // ---- work items: BLOCK * rows outer rows x CHUNK inner columns
+    // ---- work items: BLOCK * rows outer rows x CHUNK inner columns, per part
     const int64_t rows_per_item = (int64_t)BLOCK * (P->jit.ok ? P->jit.rows : 1);
-    std::vector<int4> items;
-    for (int64_t r0 = row_lo; r0 < row_hi; r0 += rows_per_item) {
-        const int64_t rhi = std::min<int64_t>(r0 + rows_per_item, row_hi);
-        int64_t c0 = mode == MODE_CROSS ? split : (mode == MODE_SYM ? r0 + 1 : 0);
-        for (; c0 < n; c0 += CHUNK)
-            items.push_back(make_int4((int)r0, (int)c0, (int)std::min<int64_t>(c0 + CHUNK, n), (int)rhi));
+    std::vector<Item> items;
+    for (size_t pi = 0; pi < parts.size(); pi++) {
+        const Part& pt = parts[pi];
+        const bool cross = pt.split >= 0;
+        const int32_t mode = cross ? MODE_CROSS : ((flags & RB_SYMMETRIC) ? MODE_SYM : MODE_ASYM);
+        const int64_t end = pt.base + pt.n;
+        const int64_t rlo = pt.base + std::max<int64_t>(0, row_lo);
+        const int64_t rhi = pt.base + std::min<int64_t>(row_hi, cross ? pt.split : pt.n);
+        for (int64_t r0 = rlo; r0 < rhi; r0 += rows_per_item) {
+            const int64_t rend = std::min<int64_t>(r0 + rows_per_item, rhi);
+            int64_t c0 = cross ? pt.base + pt.split : (mode == MODE_SYM ? r0 + 1 : pt.base);
+            for (; c0 < end; c0 += CHUNK) {
+                Item it{};
+                it.row0 = (int32_t)r0;
+                it.col0 = (int32_t)c0;
+                it.col1 = (int32_t)std::min<int64_t>(c0 + CHUNK, end);
+                it.row_hi = (int32_t)rend;
+                it.mode = mode;
+                it.part = (int32_t)pi;
+                items.push_back(it);
+            }
+        }
     }
     const int n_items = (int)items.size();
+    const int64_t n = total;
     if (n_items == 0) {
         *out = res;
         return RB_OK;
     }
 
-    if (cudaError_t e = c->items.grow(sizeof(int4) * items.size())) return cleanup(fail(RB_ERR_CUDA, "items: %s", cudaGetErrorString(e)));
+    if (cudaError_t e = c->items.grow(sizeof(Item) * items.size())) return cleanup(fail(RB_ERR_CUDA, "items: %s", cudaGetErrorString(e)));
     if (refs)
         if (cudaError_t e = c->refs.grow(sizeof(int32_t) * n)) return cleanup(fail(RB_ERR_CUDA, "refs: %s", cudaGetErrorString(e)));
     // counters: [0] item counter (u32, padded), [1] out_count, [2] pairs, [3] survivors, [4..68) slot evals
@@ -680,7 +713,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
                                 (long long)(sizeof(int32_t) * stride * (size_t)grid * BLOCK), cudaGetErrorString(e)));
     }
 
-    CK(cudaMemcpyAsync(c->items.p, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->items.p, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice, c->stream));
     if (refs) CK(cudaMemcpyAsync(c->refs.p, refs, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
 
     long long cap = std::max<long long>(1 << 20, P->last_rows + P->last_rows / 4);
@@ -702,20 +735,24 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             if (e) return cleanup(fail(RB_ERR_OOM, "output buffer of %lld rows: %s", cap, cudaGetErrorString(e)));
         }
         res->cap = cap;
-        cudaError_t e;
+        cudaError_t e = cudaSuccess;
+        if (want_parts) {
+            e = cudaMalloc(&res->d_p, sizeof(int32_t) * cap);
+            if (e) return cleanup(fail(RB_ERR_OOM, "part buffer of %lld rows: %s", cap, cudaGetErrorString(e)));
+        }
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * n_counters, c->stream));
 
         RunParams R{};
         R.refs = refs ? (const int32_t*)c->refs.p : nullptr;
         R.n = n;
-        R.mode = mode;
         R.flags = flags;
-        R.items = (const int4*)c->items.p;
+        R.items = (const Item*)c->items.p;
         R.n_items = n_items;
         R.item_counter = (unsigned int*)&ctr[0];
         R.out_t = res->d_t;
         R.out_s = res->d_s;
         R.out_r = res->d_r;
+        R.out_p = res->d_p;
         R.out_count = &ctr[1];
         R.cap = cap;
         R.stat_pairs = &ctr[2];
@@ -754,7 +791,8 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         cudaFree(res->d_t);
         cudaFree(res->d_s);
         cudaFree(res->d_r);
-        res->d_t = res->d_s = res->d_r = nullptr;
+        if (res->d_p) cudaFree(res->d_p);
+        res->d_t = res->d_s = res->d_r = res->d_p = nullptr;
         cap = rows;
     }
     *out = res;
@@ -763,12 +801,12 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
 
 int rb_run_partition(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t n, uint32_t flags,
                      rb_result** out) {
-    return run(c, rel, P, refs, n, -1, 0, n, flags, out);
+    return run(c, rel, P, refs, n, {Part{0, n, -1}}, 0, n, flags, false, out);
 }
 
 int rb_run_partition_rows(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t n, int64_t row_lo,
                           int64_t row_hi, uint32_t flags, rb_result** out) {
-    return run(c, rel, P, refs, n, -1, row_lo, row_hi, flags, out);
+    return run(c, rel, P, refs, n, {Part{0, n, -1}}, row_lo, row_hi, flags, false, out);
 }
 
 int rb_run_cross(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* left, int64_t nl, const int32_t* right,
@@ -777,7 +815,34 @@ int rb_run_cross(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* left, int64_
     std::vector<int32_t> both((size_t)(nl + nr));
     if (nl) memcpy(both.data(), left, sizeof(int32_t) * nl);
     if (nr) memcpy(both.data() + nl, right, sizeof(int32_t) * nr);
-    return run(c, rel, P, both.data(), nl + nr, nl, 0, nl, flags, out);
+    return run(c, rel, P, both.data(), nl + nr, {Part{0, nl + nr, nl}}, 0, nl + nr, flags, false, out);
+}
+
+int rb_run_batch(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, const int64_t* offsets,
+                 const int64_t* splits, int32_t n_parts, uint32_t flags, rb_result** out) {
+    if (n_parts < 0 || (n_parts && (!offsets || !refs))) return fail(RB_ERR_INVALID, "rb_run_batch: bad arguments");
+    std::vector<Part> parts;
+    parts.reserve(n_parts);
+    if (n_parts && offsets[0] != 0) return fail(RB_ERR_INVALID, "rb_run_batch: offsets[0] must be 0");
+    for (int32_t k = 0; k < n_parts; k++) {
+        const int64_t len = offsets[k + 1] - offsets[k];
+        if (len < 0) return fail(RB_ERR_INVALID, "rb_run_batch: offsets not monotone at %d", k);
+        const int64_t sp = splits ? splits[k] : -1;
+        if (sp > len) return fail(RB_ERR_INVALID, "rb_run_batch: split %lld beyond part %d", (long long)sp, k);
+        parts.push_back(Part{offsets[k], len, sp});
+    }
+    const int64_t total = n_parts ? offsets[n_parts] : 0;
+    return run(c, rel, P, refs, total, parts, 0, INT64_MAX, flags, true, out);
+}
+
+int rb_result_copy_parts(const rb_result* r, int32_t* part) {
+    if (!r) return fail(RB_ERR_INVALID, "rb_result_copy_parts: null result");
+    if (r->count == 0) return RB_OK;
+    if (!r->d_p) return fail(RB_ERR_INVALID, "rb_result_copy_parts: not a batched result");
+    if (!part) return fail(RB_ERR_INVALID, "rb_result_copy_parts: null output array");
+    CK(cudaMemcpyAsync(part, r->d_p, sizeof(int32_t) * r->count, cudaMemcpyDeviceToHost, r->stream));
+    CK(cudaStreamSynchronize(r->stream));
+    return RB_OK;
 }
 
 int rb_result_count(const rb_result* r, int64_t* rows) {
@@ -819,6 +884,7 @@ int rb_result_destroy(rb_result* r) {
     if (r->d_t) cudaFree(r->d_t);
     if (r->d_s) cudaFree(r->d_s);
     if (r->d_r) cudaFree(r->d_r);
+    if (r->d_p) cudaFree(r->d_p);
     delete r;
     return RB_OK;
 }

@@ -141,6 +141,7 @@ struct FilterPlan {
     int32_t str_nslots[MAX_STR];
     uint64_t str_rules[MAX_STR];
     uint64_t str_kill[MAX_STR];  // a missing outer string fails every slot on the feature
+    int32_t str_always[MAX_STR];
     FSlot str_slot[MAX_STR][MAX_FSLOTS];
 };
 
@@ -154,17 +155,26 @@ struct VerifyProg {
     int32_t n_slots;
 };
 
+// One work item: outer rows [row0, row_hi) x inner columns [col0, col1) of
+// the concatenated refs array, in one partition's pair space.
+struct __align__(16) Item {
+    int32_t row0, col0, col1, row_hi;
+    int32_t mode;  // RunMode of the item's partition
+    int32_t part;  // index of the partition in the batch
+    int32_t pad0, pad1;
+};
+
 struct RunParams {
     const int32_t* refs;  // position -> tid; nullptr = identity
     int64_t n;
-    int32_t mode;
     uint32_t flags;
-    const int4* items;  // {row0, col0, col1, row_hi}
+    const Item* items;
     int32_t n_items;
     unsigned int* item_counter;
     int32_t* out_t;
     int32_t* out_s;
     int32_t* out_r;
+    int32_t* out_p;  // partition index per row (batched runs), may be null
     unsigned long long* out_count;
     long long cap;
     unsigned long long* stat_pairs;
@@ -320,7 +330,7 @@ static __device__ uint64_t interpret(const VerifyProg& V, int32_t ti, int32_t si
     return hit;
 }
 
-static __device__ __noinline__ void drain_queue(const VerifyProg& V, const RunParams& R, const int2* q, int qn, const int* cp_rule,
+static __device__ __noinline__ void drain_queue(const VerifyProg& V, const RunParams& R, const int2* q, int qn, int part, const int* cp_rule,
                             int32_t* scratch) {
     const int lane = threadIdx.x & 31;
     const bool enumerate = (R.flags & RB_ENUMERATE) != 0;
@@ -359,6 +369,7 @@ static __device__ __noinline__ void drain_queue(const VerifyProg& V, const RunPa
                 R.out_t[at] = a;
                 R.out_s[at] = b;
                 R.out_r[at] = cp_rule[ord];
+                if (R.out_p) R.out_p[at] = part;
             }
             at++;
         }
@@ -389,6 +400,7 @@ struct __align__(16) Tile {
 #define RB_TOK_NJ(f) ((f) == 0 ? SPEC_TOK0_NJ : SPEC_TOK1_NJ)
 #define RB_TOK_ALWAYS(f) ((f) == 0 ? SPEC_TOK0_ALWAYS : SPEC_TOK1_ALWAYS)
 #define RB_STR_NS(f) ((f) == 0 ? SPEC_STR0_NS : SPEC_STR1_NS)
+#define RB_STR_ALWAYS(f) ((f) == 0 ? SPEC_STR0_ALWAYS : SPEC_STR1_ALWAYS)
 #define RB_FULLTAB SPEC_FULLTAB
 #define RB_TOK2D SPEC_TOK2D
 #else
@@ -400,6 +412,7 @@ struct __align__(16) Tile {
 #define RB_TOK_NJ(f) F.tok_njac[f]
 #define RB_TOK_ALWAYS(f) F.tok_always[f]
 #define RB_STR_NS(f) F.str_nslots[f]
+#define RB_STR_ALWAYS(f) F.str_always[f]
 #define RB_FULLTAB F.full_tab
 #define RB_TOK2D F.tok2d
 #endif
@@ -429,8 +442,8 @@ struct Outer {
     int32_t oslen[MAX_STR];
     uint4 obag[MAX_STR];
 
-    __device__ __forceinline__ void load(const FilterPlan& F, const RunParams& R, int64_t i_, int64_t row_hi,
-                                         int64_t col0, int64_t col1, unsigned long long& my_pairs) {
+    __device__ __forceinline__ void load(const FilterPlan& F, const RunParams& R, int mode, int64_t i_,
+                                         int64_t row_hi, int64_t col0, int64_t col1, unsigned long long& my_pairs) {
         i = i_;
         ok = i < row_hi;
         ti = 0;
@@ -438,10 +451,10 @@ struct Outer {
         if (ok) {
             ti = R.refs ? R.refs[i] : (int32_t)i;
             alive0 = (Mask)F.all_rules;
-            if (R.mode == MODE_SYM) {
+            if (mode == MODE_SYM) {
                 const int64_t lo = col0 > i + 1 ? col0 : i + 1;
                 my_pairs += (unsigned long long)(col1 > lo ? col1 - lo : 0);
-            } else if (R.mode == MODE_ASYM) {
+            } else if (mode == MODE_ASYM) {
                 my_pairs += (unsigned long long)((col1 - col0) - ((i >= col0 && i < col1) ? 1 : 0));
             } else {
                 my_pairs += (unsigned long long)(col1 - col0);
@@ -509,15 +522,15 @@ struct Outer {
     }
 
     // valid(jj) <=> jj >= jj_lo && jj != jj_skip, for the tile starting at jt
-    __device__ __forceinline__ bool tile(const RunParams& R, int64_t jt) {
+    __device__ __forceinline__ bool tile(int mode, int64_t jt) {
         jj_lo = 0;
         jj_skip = -1;
         if (!ok) {
             jj_lo = TJ + 1;
-        } else if (R.mode == MODE_SYM) {
+        } else if (mode == MODE_SYM) {
             const int64_t d = i - jt + 1;
             jj_lo = d < 0 ? 0 : (d > TJ + 1 ? TJ + 1 : (int)d);
-        } else if (R.mode == MODE_ASYM) {
+        } else if (mode == MODE_ASYM) {
             const int64_t d = i - jt;
             jj_skip = (d >= 0 && d < TJ) ? (int)d : -1;
         }
@@ -530,7 +543,8 @@ struct Outer {
 template <typename Mask, int ROWS, bool AllValid>
 __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg& V, const RunParams& R, const Tile& T,
                                           const int32_t* tab, Outer<Mask> (&o)[ROWS], int tn, int2* q, int& qn,
-                                          const int* cp_rule, int32_t* scratch, unsigned long long& my_surv) {
+                                          int part, const int* cp_rule, int32_t* scratch,
+                                          unsigned long long& my_surv) {
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << (threadIdx.x & 31)) - 1u;
     for (int jj = 0; jj < tn; jj++) {
@@ -591,7 +605,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
             Mask need = 0;
 #pragma unroll
             for (int r = 0; r < ROWS; r++) need |= alive[r];
-            if (!__any_sync(FULL, (need & (Mask)F.str_rules[f]) != 0)) continue;
+            if (!RB_STR_ALWAYS(f) && !__any_sync(FULL, (need & (Mask)F.str_rules[f]) != 0)) continue;
             const int lb = T.strlen_[f][jj];
             const uint4 ib = T.strbag[f][jj];
 #pragma unroll
@@ -631,7 +645,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
             }
             if (qn > QCAP - 32 * ROWS) {
                 __syncwarp();
-                drain_queue(V, R, q, qn, cp_rule, scratch);
+                drain_queue(V, R, q, qn, part, cp_rule, scratch);
                 __syncwarp();
                 qn = 0;
             }
@@ -666,13 +680,15 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
         __syncthreads();
         const int it = s_item;
         if (it >= R.n_items) break;
-        const int4 item = R.items[it];
-        const int64_t col0 = item.y, col1 = item.z;
+        const Item item = R.items[it];
+        const int64_t col0 = item.col0, col1 = item.col1;
+        const int part = item.part;
 
         Outer<Mask> o[ROWS];
 #pragma unroll
         for (int r = 0; r < ROWS; r++)
-            o[r].load(F, R, (int64_t)item.x + r * BLOCK + threadIdx.x, (int64_t)item.w, col0, col1, my_pairs);
+            o[r].load(F, R, item.mode, (int64_t)item.row0 + r * BLOCK + threadIdx.x, (int64_t)item.row_hi, col0, col1,
+                      my_pairs);
 
         for (int64_t jt = col0; jt < col1; jt += TJ) {
             const int tn = (int)(col1 - jt < TJ ? col1 - jt : TJ);
@@ -702,15 +718,15 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
 
             bool all_valid = true;
 #pragma unroll
-            for (int r = 0; r < ROWS; r++) all_valid &= o[r].tile(R, jt);
+            for (int r = 0; r < ROWS; r++) all_valid &= o[r].tile(item.mode, jt);
             if (__all_sync(FULL, all_valid))
-                tile_loop<Mask, ROWS, true>(F, V, R, T, tab, o, tn, q, qn, cp_rule, scratch, my_surv);
+                tile_loop<Mask, ROWS, true>(F, V, R, T, tab, o, tn, q, qn, part, cp_rule, scratch, my_surv);
             else
-                tile_loop<Mask, ROWS, false>(F, V, R, T, tab, o, tn, q, qn, cp_rule, scratch, my_surv);
+                tile_loop<Mask, ROWS, false>(F, V, R, T, tab, o, tn, q, qn, part, cp_rule, scratch, my_surv);
         }
         if (qn) {
             __syncwarp();
-            drain_queue(V, R, q, qn, cp_rule, scratch);
+            drain_queue(V, R, q, qn, part, cp_rule, scratch);
             __syncwarp();
             qn = 0;
         }

@@ -285,6 +285,30 @@ class PathProgram:
 
     # -- raw runs ---------------------------------------------------------
 
+    def run_batch(self, refs, offsets, splits, flags: int):
+        """One launch over many partitions / cross blocks laid out back to
+        back (rb_run_batch).  Returns ((t, s, rule, part) int32 arrays, rb_stats)."""
+        L = lib()
+        res = _lib.c_vp()
+        refs_a = i32(refs)
+        offs = np.ascontiguousarray(offsets, dtype=np.int64)
+        spl = None if splits is None else np.ascontiguousarray(splits, dtype=np.int64)
+        check(L.rb_run_batch(self.ctx.handle, self.drel.handle, self.handle, ptr(refs_a), ptr(offs), ptr(spl),
+                             len(offs) - 1, flags, _lib.ctypes.byref(res)))
+        try:
+            cnt = _lib.ctypes.c_int64(0)
+            check(L.rb_result_count(res, _lib.ctypes.byref(cnt)))
+            k = cnt.value
+            t, s, r, p = (np.empty(k, dtype=np.int32) for _ in range(4))
+            if k:
+                check(L.rb_result_copy(res, ptr(t), ptr(s), ptr(r)))
+                check(L.rb_result_copy_parts(res, ptr(p)))
+            st = _lib.RbStats()
+            check(L.rb_result_stats(res, _lib.ctypes.byref(st)))
+        finally:
+            L.rb_result_destroy(res)
+        return (t, s, r, p), st
+
     def run_raw(self, refs, n: int, flags: int, *, split: int = -1, row_lo: int = 0, row_hi: Optional[int] = None):
         """Evaluate on the device.  Returns ((t, s, rule) int32 arrays, rb_stats)."""
         L = lib()
@@ -453,6 +477,67 @@ def run_partition_rows(partition, relation, path, row_lo: int, row_hi: int, cfg=
     refs = _refs_array(partition)
     rows, st = prog.run_raw(refs, len(refs), cfg.flags(), row_lo=row_lo, row_hi=row_hi)
     return _candidates(prog, rows, st, cfg, max(0, row_hi - row_lo), time.perf_counter() - started)
+
+
+def _batch(prog: PathProgram, blocks, cfg: EngineConfig):
+    """blocks: list of (refs int32 array, split or -1).  One launch; returns
+    one CandidateSet per block."""
+    started = time.perf_counter()
+    sizes = [len(r) for r, _ in blocks]
+    offsets = np.zeros(len(blocks) + 1, dtype=np.int64)
+    np.cumsum(sizes, out=offsets[1:])
+    refs = np.concatenate([r for r, _ in blocks]) if blocks else np.zeros(0, np.int32)
+    splits = np.array([sp for _, sp in blocks], dtype=np.int64)
+    (t, s, r, p), st = prog.run_batch(refs, offsets, splits, cfg.flags())
+    wall = time.perf_counter() - started
+    order = np.argsort(p, kind="stable")
+    t, s, r, p = t[order], s[order], r[order], p[order]
+    bounds = np.searchsorted(p, np.arange(len(blocks) + 1))
+    out = []
+    for k, (refs_k, sp) in enumerate(blocks):
+        a, b = bounds[k], bounds[k + 1]
+        n = len(refs_k)
+        if sp >= 0:
+            cmp = sp * (n - sp)
+        elif cfg.symmetric_mode:
+            cmp = n * (n - 1) // 2
+        else:
+            cmp = n * (n - 1)
+        tt, ss, rr = _dedup(t[a:b], s[a:b], r[a:b], cfg.symmetric_mode, cfg.enumerate_witnesses)
+        block = BlockStats(block_id=0, intervals_processed=1, comparisons=int(cmp), emitted=int(b - a),
+                           slot_evals=np.zeros(prog.n_slots, dtype=np.int64))
+        stats = RunStats(blocks=[block], wall_s=wall, n_intervals=1, kernel_ms=float(st.kernel_ms),
+                         launches=int(st.launches), specialized=bool(st.specialized), jit_log=prog.jit_log)
+        out.append(CandidateSet(stats=stats, arrays=(tt, ss, rr), rule_ids=prog.rule_ids))
+    if sum(b.stats.total_comparisons() for b in out) != int(st.comparisons):
+        raise ConfigError("device pair count disagrees with the batch layout")
+    return out
+
+
+def run_partitions(partitions, relation, path, cfg=None, reg=None, encoded=None, program=None) -> list:
+    """run_partition over many partitions in ONE device launch (the
+    pipeline's per-task loop, pipeline.py:177-209, batched).  Returns one
+    CandidateSet per partition, each identical to run_partition's."""
+    cfg = cfg or EngineConfig()
+    live = [p for p in partitions if p is not None and len(p.tuple_refs)]
+    prog = _program_for(path, relation, reg, encoded, program)
+    res = iter(_batch(prog, [(_refs_array(p), -1) for p in live], cfg)) if live else iter(())
+    return [next(res) if (p is not None and len(p.tuple_refs)) else CandidateSet(pairs=[]) for p in partitions]
+
+
+def run_crosses(pairs, relation, path, cfg=None, reg=None, encoded=None, program=None) -> list:
+    """run_cross over many (left, right) partition pairs in one launch --
+    e.g. the per-block record-linkage runs of BASELINE config 5."""
+    cfg = cfg or EngineConfig()
+    prog = _program_for(path, relation, reg, encoded, program)
+    blocks = []
+    for left, right in pairs:
+        lr, rr = _refs_array(left), _refs_array(right)
+        both = np.concatenate([lr, rr])
+        if len(np.unique(both)) != len(both):
+            raise SchemaError("partition -1 has duplicate tuple refs")
+        blocks.append((both, len(lr)))
+    return _batch(prog, blocks, cfg)
 
 
 def run_cross(left, right, relation, path, cfg=None, reg=None, encoded=None, program=None) -> CandidateSet:

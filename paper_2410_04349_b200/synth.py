@@ -186,4 +186,82 @@ def data_aware_plan(enc: Encoded, rules, sample: int = 200_000, seed: int = 0):
     return plan_from_stats(rules, costs, sps)
 
 
-WORKLOADS = {"citation3": citation3}
+EDIT_HEAVY_RULES = [
+    {"id": "R1", "when": [
+        {"t_attr": "text", "op": "sim", "s_attr": "text", "measure": "edit", "threshold": 0.98}]},
+    {"id": "R2", "when": [
+        {"t_attr": "name", "op": "sim", "s_attr": "name", "measure": "edit", "threshold": 0.97},
+        {"t_attr": "zip", "op": "eq", "s_attr": "zip"}]},
+]
+
+ALPHA = b"abcdefghijklmnopqrstuvwxyz "
+
+
+def _perturb(rng, base: bytes, k: int) -> bytes:
+    """k random single-character substitutions / insertions / deletions
+    (rng: random.Random)."""
+    b = bytearray(base)
+    for _ in range(k):
+        op = rng.randrange(3)
+        p = rng.randrange(len(b))
+        c = ALPHA[rng.randrange(27)]
+        if op == 0:
+            b[p] = c
+        elif op == 1:
+            b.insert(p, c)
+        elif len(b) > 1:
+            del b[p]
+    return bytes(b)
+
+
+def _chars_column(strs: list) -> Column:
+    lens = np.fromiter((len(x) for x in strs), dtype=np.int64, count=len(strs))
+    off = np.zeros(len(strs) + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    data = np.frombuffer(b"".join(strs), dtype=np.uint8).copy()
+    return Column(COL_CHARS, data, off, np.zeros(len(strs), np.uint8))
+
+
+def edit_heavy(n: int = 1_000_000, seed: int = 11, plan_sample: int = 200_000) -> Workload:
+    """BASELINE config 3: long-string edit distance with thresholds whose
+    maxd[L] is 2-3: 64-256-char texts in groups of 2-50
+    near-duplicates (0-3 random substitutions / indels), a short name with
+    the same group structure and a Zipf zip code."""
+    import random
+
+    rng = random.Random(seed)
+    nrng = np.random.default_rng(seed)
+    zipf_p = 1.0 / np.arange(1, 100_001) ** 1.1
+    zip_draws = nrng.choice(100_000, size=2 * n, p=zipf_p / zipf_p.sum()).astype(np.int32).tolist()
+    zd = 0
+    texts, names, zips = [], [], []
+    while len(texts) < n:
+        g = rng.randint(2, 50)
+        base = bytes(ALPHA[rng.randrange(27)] for _ in range(rng.randint(64, 256)))
+        nb = f"{rng.choice(FIRST)} {rng.choice(LAST)}".encode()
+        z = zip_draws[zd]
+        zd += 1
+        for _ in range(min(g, n - len(texts))):
+            texts.append(_perturb(rng, base, rng.randint(0, 3)))
+            names.append(nb if rng.random() < 0.8 else _perturb(rng, nb, 1))
+            if rng.random() < 0.9:
+                zips.append(z)
+            else:
+                zips.append(zip_draws[zd])
+                zd += 1
+    order = nrng.permutation(n)
+    texts = [texts[k] for k in order]
+    names = [names[k] for k in order]
+    zips = np.asarray(zips, dtype=np.int32)[order]
+    enc = Encoded(n)
+    enc.add(("chars", "text"), _chars_column(texts))
+    enc.add(("chars", "name"), _chars_column(names))
+    enc.add(("codes", "zip"), Column(COL_CODES, zips))
+    import json
+
+    rules = parse_ruleset(json.dumps(EDIT_HEAVY_RULES))
+    path = data_aware_plan(enc, rules, sample=plan_sample, seed=seed)
+    return Workload("edit_heavy", enc, rules, path, n)
+
+
+WORKLOADS = {"citation3": citation3, "edit_heavy": edit_heavy}

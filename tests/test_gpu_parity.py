@@ -84,3 +84,44 @@ def test_row_shards_union_equals_whole(name):
     assert sorted(got) == goldens.expected_rows(case)
     assert cmp == case["comparisons"]
 
+
+
+def test_batched_partitions_equal_single_runs():
+    """run_partitions (one launch) == run_partition per partition, on a
+    mix of shuffled / tiny / empty partitions and every golden relation."""
+    import random
+
+    from paper_2410_04349_b200 import run_partitions
+
+    for name in ["random_052", "random_001", "citation", "edge_cross_attr", "products"]:
+        rel, path, cases = goldens.load(name)
+        rng = random.Random(7)
+        ids = list(range(len(rel)))
+        rng.shuffle(ids)
+        parts, k = [], 0
+        while k < len(ids):
+            size = rng.choice([1, 2, 3, 17, 60, 300, 700])
+            parts.append(DataPartition(len(parts), tuple(ids[k:k + size])))
+            k += size
+        parts.append(None)
+        for sym in (True, False):
+            cfg = EngineConfig(symmetric_mode=sym)
+            batched = run_partitions(parts, rel, path, cfg)
+            for p, cs in zip(parts, batched):
+                single = run_partition(p, rel, path, cfg)
+                assert sorted(cs.pairs) == sorted(single.pairs), name
+                assert cs.stats.total_comparisons() == single.stats.total_comparisons()
+
+
+def test_batched_crosses_equal_single_runs():
+    from paper_2410_04349_b200 import run_crosses
+
+    rel, path, _ = goldens.load("random_053")
+    n = len(rel)
+    pairs = [(DataPartition(0, tuple(range(0, k))), DataPartition(1, tuple(range(k, min(n, 2 * k + 5)))))
+             for k in (1, 5, 20, n // 3)]
+    batched = run_crosses(pairs, rel, path)
+    for (l, r), cs in zip(pairs, batched):
+        single = run_cross(l, r, rel, path)
+        assert sorted(cs.pairs) == sorted(single.pairs)
+        assert cs.stats.total_comparisons() == len(l) * len(r)
