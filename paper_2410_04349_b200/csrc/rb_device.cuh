@@ -421,6 +421,13 @@ struct __align__(16) Tile {
 // with a missing side, whose lengths are -1, stay inside the array.
 constexpr int TAB_BASE = 2;
 
+// 32-bit shared-memory load: the address is one register add away.
+static __device__ __forceinline__ int lds_s32(uint32_t addr) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 template <bool B>
 struct BoolC {
     static constexpr bool value = B;
@@ -436,14 +443,15 @@ struct Outer {
     int32_t jj_lo, jj_skip;
     int32_t ocode[MAX_EQ];
     int32_t olen[MAX_TOK], orem[MAX_TOK];
-    int32_t orow[MAX_TOK][MAX_FSLOTS];
+    uint32_t orow[MAX_TOK][MAX_FSLOTS];  // 2-D jaccard: shared-memory byte address of need[n][-1]
     uint32_t lev[MAX_TOK][4];
     uint2 ohash[MAX_TOK];
     int32_t oslen[MAX_STR];
     uint4 obag[MAX_STR];
 
-    __device__ __forceinline__ void load(const FilterPlan& F, const RunParams& R, int mode, int64_t i_,
-                                         int64_t row_hi, int64_t col0, int64_t col1, unsigned long long& my_pairs) {
+    __device__ __forceinline__ void load(const FilterPlan& F, const RunParams& R, const int32_t* tab, int mode,
+                                         int64_t i_, int64_t row_hi, int64_t col0, int64_t col1,
+                                         unsigned long long& my_pairs) {
         i = i_;
         ok = i < row_hi;
         ti = 0;
@@ -481,8 +489,10 @@ struct Outer {
             ohash[f] = make_uint2(0, 0);
 #pragma unroll
             for (int w = 0; w < 4; w++) lev[f][w] = 0;
+            // inactive rows still run the (discarded) lookups: point them at the guard entries
+            const uint32_t guard = (uint32_t)__cvta_generic_to_shared(tab + TAB_BASE);
 #pragma unroll
-            for (int z = 0; z < MAX_FSLOTS; z++) orow[f][z] = 0;
+            for (int z = 0; z < MAX_FSLOTS; z++) orow[f][z] = guard;
             if (f < RB_NTOK && ok) {
                 olen[f] = __ldg(F.tok_olen[f] + ti);
                 ohash[f] = __ldg(F.tok_ohash[f] + ti);
@@ -492,7 +502,9 @@ struct Outer {
                     const int nn = olen[f] > 0 ? olen[f] : 0;
 #pragma unroll
                     for (int z = 0; z < MAX_FSLOTS; z++)
-                        if (z < RB_TOK_NJ(f)) orow[f][z] = F.tok_slot[f][z].off0 + nn * F.tok_slot[f][z].w2 + 1;
+                        if (z < RB_TOK_NJ(f))
+                            orow[f][z] = (uint32_t)__cvta_generic_to_shared(
+                                tab + F.tok_slot[f][z].off0 + nn * F.tok_slot[f][z].w2 + 1);
                 }
                 const int64_t a = __ldg(F.tok_ooff[f] + ti), b = __ldg(F.tok_ooff[f] + ti + 1);
                 for (int64_t k = a; k < b; k++) {
@@ -565,6 +577,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
             for (int r = 0; r < ROWS; r++) need |= alive[r];
             if (!RB_TOK_ALWAYS(f) && !__any_sync(FULL, (need & (Mask)F.tok_rules[f]) != 0)) continue;
             const int m = T.toklen[f][jj];
+            const uint32_t m4 = (uint32_t)m << 2;  // byte offset of column m within a need[n][.] row
             const uint4 is = T.toksig[f][jj];
             const uint2 h = T.tokhash[f][jj];
 #pragma unroll
@@ -581,7 +594,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                         if (z < RB_TOK_NJ(f)) {  // jaccard: exact integer tables
                             if (RB_TOK2D) {
                                 // need[n][m]: INF unless the length tests pass, else mink[n+m]
-                                ok = u >= tab[o[r].orow[f][z] + m];
+                                ok = u >= lds_s32(o[r].orow[f][z] + m4);
                             } else {
                                 const bool live = m >= 0;
                                 const int small = min(n, m), big = max(n, m);
@@ -687,7 +700,7 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
         Outer<Mask> o[ROWS];
 #pragma unroll
         for (int r = 0; r < ROWS; r++)
-            o[r].load(F, R, item.mode, (int64_t)item.row0 + r * BLOCK + threadIdx.x, (int64_t)item.row_hi, col0, col1,
+            o[r].load(F, R, tab, item.mode, (int64_t)item.row0 + r * BLOCK + threadIdx.x, (int64_t)item.row_hi, col0, col1,
                       my_pairs);
 
         for (int64_t jt = col0; jt < col1; jt += TJ) {
