@@ -214,19 +214,28 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    ndev = max(1, torch.cuda.device_count())
+    dev = local % ndev
+    torch.cuda.set_device(dev)
+    # one rank per GPU over NCCL; ranks sharing a GPU (functional tests on a
+    # 1-GPU box) reduce over gloo instead
+    backend = "nccl" if world <= ndev else "gloo"
+    red_dev = "cuda" if backend == "nccl" else "cpu"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
 
     from paper_2410_04349_b200 import synth
     from paper_2410_04349_b200._lib import RB_SYMMETRIC
     from paper_2410_04349_b200.engine import DeviceRelation, PathProgram, context
 
     w = synth.WORKLOADS[args.workload](args.n, seed=args.seed + rank)
-    ctx = context(local)
+    ctx = context(dev)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
-    prog = PathProgram(w.path, w.enc, device=local)
+    prog = PathProgram(w.path, w.enc, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -240,7 +249,7 @@ def main():
     pairs_step = int(st.comparisons)
 
     times, kms = [], []
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev)
     with sampler:
         for _ in range(args.steps):
             flush.fill_(1)
@@ -259,8 +268,8 @@ def main():
                   f"survivors {st.survivors}, rows {len(rows[0])}", file=sys.stderr)
             assert st.comparisons == pairs_step and len(rows[0]) == n_rows
     barrier()
-    t_total = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
-    counts = torch.tensor([pairs_step * args.steps, n_rows], dtype=torch.float64, device="cuda")
+    t_total = torch.tensor([sum(times)], dtype=torch.float64, device=red_dev)
+    counts = torch.tensor([pairs_step * args.steps, n_rows], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t_total, op=dist.ReduceOp.MAX)
         dist.all_reduce(counts, op=dist.ReduceOp.SUM)
@@ -282,7 +291,7 @@ def main():
         p2.close()
         drel.close()
     torch.cuda.synchronize()
-    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device="cuda")
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = counts[0].item() / args.steps / e2e_s.item()
@@ -334,7 +343,8 @@ def main():
             "config": {"workload": f"{w.name} n={w.n} per GPU ({WORKLOAD_DESC.get(w.name, w.name)}), "
                                    "one symmetric partition per GPU",
                        "pairs_per_step_per_gpu": pairs_step, "rows_per_step_per_gpu": n_rows,
-                       "l2": "flushed (512 MiB write) between timed steps", "parallelism": f"partition-per-gpu x{world}"},
+                       "l2": "flushed (512 MiB write) between timed steps", "parallelism": f"partition-per-gpu x{world}",
+                       "collective": backend if world > 1 else None},
             "blocking_wall_s": ms_step / 1e3,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "blocking_wall_s": e2e_s.item()},

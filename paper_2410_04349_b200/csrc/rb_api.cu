@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -84,6 +85,7 @@ struct rb_rel {
     int64_t n = 0;
     std::vector<DevColumn> cols;
     std::vector<int64_t> max_len;
+    std::vector<double> mean_len;
     std::vector<void*> allocs;
     void* d_cols = nullptr;
     bool cols_dirty = true;
@@ -200,10 +202,11 @@ static cudaError_t upload(rb_rel* r, const void* src, size_t bytes, void** dst) 
     return cudaMemsetAsync(*dst, 0, bytes, r->ctx->stream);
 }
 
-static int add_column(rb_rel* r, const DevColumn& dc, int64_t max_len, int32_t* col) {
+static int add_column(rb_rel* r, const DevColumn& dc, int64_t max_len, int32_t* col, double mean_len = 0) {
     if ((int)r->cols.size() >= MAX_COLS) return fail(RB_ERR_LIMIT, "relation has more than %d columns", MAX_COLS);
     r->cols.push_back(dc);
     r->max_len.push_back(max_len);
+    r->mean_len.push_back(mean_len);
     r->cols_dirty = true;
     if (col) *col = (int32_t)r->cols.size() - 1;
     return RB_OK;
@@ -268,7 +271,7 @@ int rb_relation_add_tokens(rb_rel* r, const int64_t* offsets, const int32_t* ids
     dc.len = (const int32_t*)d_len;
     dc.sig = (const uint4*)d_sig;
     dc.hash = (const uint2*)d_hash;
-    return add_column(r, dc, max_len, col);
+    return add_column(r, dc, max_len, col, r->n ? (double)nnz / (double)r->n : 0.0);
 }
 
 int rb_relation_add_chars(rb_rel* r, const int64_t* offsets, const void* chars, int32_t width,
@@ -501,6 +504,13 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             F.tok_rules[f] |= kill;
             F.tok_kill[f] |= kill;
             cls[s] = 1 + f;
+            // fold to 64-bit signatures when rows are short on both sides (<= 12
+            // tokens on average): half the popcounts, few extra maybe-pairs
+            {
+                const double tl = rel->mean_len[sl.lhs], tr = rel->mean_len[sl.rhs];
+                const char* env = std::getenv("RB_SIG64");
+                F.tok_sig64[f] = env ? (env[0] == '1') : (tl <= 12.0 && tr <= 12.0);
+            }
         } else if (sl.kind == RB_SLOT_EDIT) {
             auto it = strf.find(key);
             int f;

@@ -24,6 +24,8 @@
 //    + (|t| - popc(sig_t)) counts every outer token whose bit is present in
 //    the inner signature plus every outer token that shares its bit with an
 //    earlier one, so u >= |A n B|; u < mink[n+m] proves jaccard < delta.
+//    For short token rows both signatures are folded to 64 bits (bit b and
+//    b+64 merged) -- the same argument holds on the folded bits.
 //  * id-list hash: different hashes prove different lists (exact_token).
 //  * character histogram: 16 buckets of saturating u8 counts; saturation is
 //    1-Lipschitz so D' = sum |ha-hb| <= D, and lev >= ceil((D'+|la-lb|)/2)
@@ -131,6 +133,7 @@ struct FilterPlan {
     int32_t tok_nslots[MAX_TOK];  // slots on the feature: the first tok_njac are jaccard, the rest exact_token
     int32_t tok_njac[MAX_TOK];
     int32_t tok_always[MAX_TOK];  // some rule reaches this feature with nothing filtered before it
+    int32_t tok_sig64[MAX_TOK];   // short token rows: fold the signature to 64 bits (half the popcounts)
     uint64_t tok_rules[MAX_TOK];
     uint64_t tok_kill[MAX_TOK];  // OR of the feature's slot kills: an outer row without tokens fails them all
     FSlot tok_slot[MAX_TOK][MAX_FSLOTS];
@@ -399,6 +402,7 @@ struct __align__(16) Tile {
 #define RB_TOK_NS(f) ((f) == 0 ? SPEC_TOK0_NS : SPEC_TOK1_NS)
 #define RB_TOK_NJ(f) ((f) == 0 ? SPEC_TOK0_NJ : SPEC_TOK1_NJ)
 #define RB_TOK_ALWAYS(f) ((f) == 0 ? SPEC_TOK0_ALWAYS : SPEC_TOK1_ALWAYS)
+#define RB_TOK_SIG64(f) ((f) == 0 ? SPEC_TOK0_SIG64 : SPEC_TOK1_SIG64)
 #define RB_STR_NS(f) ((f) == 0 ? SPEC_STR0_NS : SPEC_STR1_NS)
 #define RB_STR_ALWAYS(f) ((f) == 0 ? SPEC_STR0_ALWAYS : SPEC_STR1_ALWAYS)
 #define RB_FULLTAB SPEC_FULLTAB
@@ -411,6 +415,7 @@ struct __align__(16) Tile {
 #define RB_TOK_NS(f) F.tok_nslots[f]
 #define RB_TOK_NJ(f) F.tok_njac[f]
 #define RB_TOK_ALWAYS(f) F.tok_always[f]
+#define RB_TOK_SIG64(f) F.tok_sig64[f]
 #define RB_STR_NS(f) F.str_nslots[f]
 #define RB_STR_ALWAYS(f) F.str_always[f]
 #define RB_FULLTAB F.full_tab
@@ -507,10 +512,11 @@ struct Outer {
                                 tab + F.tok_slot[f][z].off0 + nn * F.tok_slot[f][z].w2 + 1);
                 }
                 const int64_t a = __ldg(F.tok_ooff[f] + ti), b = __ldg(F.tok_ooff[f] + ti + 1);
+                const uint32_t fold = RB_TOK_SIG64(f) ? 1u : 3u;  // 64-bit mode: bit b and b+64 coincide
                 for (int64_t k = a; k < b; k++) {
                     const uint32_t bit = sig_bit(__ldg(F.tok_oids[f] + k));
                     const uint32_t m = 1u << (bit & 31);
-                    const uint32_t wsel = bit >> 5;
+                    const uint32_t wsel = (bit >> 5) & fold;
 #pragma unroll
                     for (int w = 0; w < 4; w++) {
                         if (w == (int)wsel) {
@@ -583,8 +589,10 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
 #pragma unroll
             for (int r = 0; r < ROWS; r++) {
                 // u >= |A n B| (see the header); rows with n <= 0 were killed at load
-                const int u = __popc(o[r].lev[f][0] & is.x) + __popc(o[r].lev[f][1] & is.y) +
-                              __popc(o[r].lev[f][2] & is.z) + __popc(o[r].lev[f][3] & is.w) + o[r].orem[f];
+                const int u = RB_TOK_SIG64(f)
+                                  ? __popc(o[r].lev[f][0] & is.x) + __popc(o[r].lev[f][1] & is.y) + o[r].orem[f]
+                                  : __popc(o[r].lev[f][0] & is.x) + __popc(o[r].lev[f][1] & is.y) +
+                                        __popc(o[r].lev[f][2] & is.z) + __popc(o[r].lev[f][3] & is.w) + o[r].orem[f];
                 const int n = o[r].olen[f];
 #pragma unroll
                 for (int z = 0; z < MAX_FSLOTS; z++) {
@@ -604,8 +612,9 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                                     (RB_FULLTAB || (unsigned)(n + m) < (unsigned)fs.cap1) ? tab[fs.off1 + n + m] : 0;
                                 ok = live & (small >= ms) & (min(u, small) >= mk);
                             }
-                        } else {  // exact_token: the id-list hash (seeded with the length) must match
-                            ok = (h.x == o[r].ohash[f].x) & (h.y == o[r].ohash[f].y);
+                        } else {  // exact_token: the id-list hash (seeded with the length) must match;
+                            // 32 of its bits suffice to drop all but ~2^-32 of the unequal pairs
+                            ok = h.x == o[r].ohash[f].x;
                         }
                         if (!ok) alive[r] &= ~(Mask)fs.kill;
                     }
@@ -717,7 +726,9 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
                 for (int f = 0; f < MAX_TOK; f++)
                     if (f < RB_NTOK) {
                         T.toklen[f][k] = __ldg(F.tok_ilen[f] + sj);
-                        T.toksig[f][k] = __ldg(F.tok_isig[f] + sj);
+                        uint4 sg = __ldg(F.tok_isig[f] + sj);
+                        if (RB_TOK_SIG64(f)) sg = make_uint4(sg.x | sg.z, sg.y | sg.w, 0u, 0u);
+                        T.toksig[f][k] = sg;
                         T.tokhash[f][k] = __ldg(F.tok_ihash[f] + sj);
                     }
 #pragma unroll

@@ -27,14 +27,19 @@ def gpu_rows(rel, path, case, prog=None):
     return sorted(cs.pairs), cs
 
 
-@pytest.fixture(params=["specialized", "generic"])
+@pytest.fixture(params=["specialized", "generic", "sig64", "sig128"])
 def kernel_flavour(request, monkeypatch):
-    """Run every case through the NVRTC-specialised kernel and through the
-    generic (statically built) kernel."""
+    """Run every case through the NVRTC-specialised kernel, the generic
+    (statically built) kernel, and with the token signature forced to the
+    folded 64-bit and the full 128-bit form."""
+    monkeypatch.delenv("RB_JIT", raising=False)
+    monkeypatch.delenv("RB_SIG64", raising=False)
     if request.param == "generic":
         monkeypatch.setenv("RB_JIT", "0")
-    else:
-        monkeypatch.delenv("RB_JIT", raising=False)
+    elif request.param == "sig64":
+        monkeypatch.setenv("RB_SIG64", "1")
+    elif request.param == "sig128":
+        monkeypatch.setenv("RB_SIG64", "0")
     return request.param
 
 
@@ -47,7 +52,7 @@ def test_gpu_matches_reference_golden(name, kernel_flavour):
         assert cs.stats.total_comparisons() == case["comparisons"], f"{name}/{case['name']}"
         evals = cs.stats.blocks[0].slot_evals
         assert (evals <= cs.stats.total_comparisons()).all()
-        assert cs.stats.specialized == (kernel_flavour == "specialized"), cs.stats.jit_log
+        assert cs.stats.specialized == (kernel_flavour != "generic"), cs.stats.jit_log
 
 
 def test_empty_and_singleton_partitions():
