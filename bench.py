@@ -41,6 +41,7 @@ METRIC = "tuple pairs evaluated/sec and blocking wall-time at 1/2/4/8 B200 vs CP
 WORKLOAD_DESC = {
     "citation3": "BASELINE config 2: 3 rules mixing eq, jaccard and edit",
     "edit_heavy": "BASELINE config 3: edit-distance-heavy rules, 64-256-char strings, maxd 2-5",
+    "linkage": "BASELINE config 5: two-table linkage, Zipf(1.3) blocks, one cross run per block, batched",
 }
 UNIT = "pairs/s"
 
@@ -154,6 +155,91 @@ def sample_rows(n, budget_pairs, k=8):
     return out
 
 
+def blocks_cpu_parity(w, prog, budget, kms, pairs_step, n_rows):
+    """Block workloads: oracle on a seeded sample of whole blocks (CPU
+    baseline), the same blocks re-run on the GPU for bit-exact parity."""
+    from oracle import oracle
+    from paper_2410_04349_b200._lib import RB_SYMMETRIC
+
+    rng = np.random.default_rng(0)
+    order = rng.permutation(len(w.blocks))
+    chosen, pairs = [], 0
+    for k in order:
+        refs, sp = w.blocks[k]
+        c = sp * (len(refs) - sp) if sp >= 0 else len(refs) * (len(refs) - 1) // 2
+        if c > budget // 4 or pairs + c > budget:
+            continue
+        chosen.append(k)
+        pairs += c
+    cores = os.cpu_count() or 1
+    secs, cmp_total, ok = 0.0, 0, True
+    evals = np.zeros(prog.n_slots, dtype=np.int64)
+    sub = [w.blocks[k] for k in chosen]
+    refs = np.concatenate([r for r, _ in sub]).astype(np.int32)
+    offs = np.zeros(len(sub) + 1, dtype=np.int64)
+    np.cumsum([len(r) for r, _ in sub], out=offs[1:])
+    (gt, gs, gr, gp), _ = prog.run_batch(refs, offs, np.array([sp for _, sp in sub], dtype=np.int64), RB_SYMMETRIC)
+    got = sorted(zip(gp.tolist(), gt.tolist(), gs.tolist(), gr.tolist()))
+    want = []
+    for bi, (r, sp) in enumerate(sub):
+        t0 = time.perf_counter()
+        rows, cmp, ev = oracle.run(w.enc, prog.program, r, len(r), split=sp, flags=1, nthreads=cores)
+        secs += time.perf_counter() - t0
+        cmp_total += cmp
+        evals += ev
+        want += [(bi, int(a), int(b), int(c)) for a, b, c in rows]
+    ok = sorted(want) == got
+    cpu = {"value": cmp_total / secs, "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"{len(sub)} whole cross blocks, {cmp_total} pairs (oracle/rb_oracle.c, OpenMP {cores} threads)"}
+    parity = {"blocks_checked": len(sub), "rows_checked": len(want), "pairs_checked": cmp_total, "bit_exact": ok}
+    peak, peak_kind = measured_peak()
+    bpp, terms = algorithmic_bytes_per_pair(w.enc, w.path, evals / max(1, cmp_total), n_rows / max(1, pairs_step))
+    k_ms = float(np.mean(kms))
+    achieved = bpp * pairs_step / (k_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None, "peak_kind": peak_kind, "bytes_per_pair": bpp, "kernel_ms": k_ms, "terms": terms,
+            "model": "SURVEY 8d streaming bytes: sum_s E_s*b_s + 10 B per row; E_s from oracle first-touch counts"}
+    return cpu, parity, roof
+
+
+def run_reference_blocks(args, w, prog, cores, world):
+    from oracle import oracle
+
+    rng = np.random.default_rng(0)
+    chosen, pairs = [], 0
+    for k in rng.permutation(len(w.blocks)):
+        refs, sp = w.blocks[k]
+        c = sp * (len(refs) - sp)
+        if c <= args.cpu_pairs // 4 and pairs + c <= args.cpu_pairs:
+            chosen.append(k)
+            pairs += c
+    secs = cmp = 0
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        c_it = 0
+        for k in chosen[: (4 if it < args.warmup else None)]:
+            refs, sp = w.blocks[k]
+            _, c, _ = oracle.run(w.enc, prog, refs, len(refs), split=sp, flags=1, nthreads=cores)
+            c_it += c
+        if it >= args.warmup:
+            secs += time.perf_counter() - t0
+            cmp += c_it
+    v = cmp / secs
+    total = w.pairs()
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"{w.name} n={w.n} ({WORKLOAD_DESC.get(w.name, w.name)}), {len(w.blocks)} blocks",
+                   "pairs_per_step_full": total, "sample_pairs_per_step": cmp // args.steps},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{len(chosen)} whole cross blocks, {cmp // args.steps} pairs per step"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "blocking_wall_s_full_extrapolated": total / v,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference CPU engine restated in C (oracle), all
     host threads, bounded sample per step; rank 0 only."""
@@ -165,6 +251,8 @@ def run_reference(args, rank, world):
     w = synth.WORKLOADS[args.workload](args.n, seed=args.seed)
     prog = compile_program(w.path, w.enc)
     cores = os.cpu_count() or 1
+    if w.blocks is not None:
+        return run_reference_blocks(args, w, prog, cores, world)
     rows = sample_rows(w.n, args.cpu_pairs)
     for _ in range(args.warmup):
         cpu_sample(w, prog, rows[:1], cores)
@@ -243,8 +331,21 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    if w.blocks is not None:  # many cross blocks / partitions: one batched launch per step
+        b_refs = np.concatenate([r for r, _ in w.blocks]).astype(np.int32)
+        b_offs = np.zeros(len(w.blocks) + 1, dtype=np.int64)
+        np.cumsum([len(r) for r, _ in w.blocks], out=b_offs[1:])
+        b_splits = np.array([sp for _, sp in w.blocks], dtype=np.int64)
+
+        def step(p):
+            (t, s, r, _), st_ = p.run_batch(b_refs, b_offs, b_splits, RB_SYMMETRIC)
+            return (t, s, r), st_
+    else:
+        def step(p):
+            return p.run_raw(None, w.n, RB_SYMMETRIC)
+
     for _ in range(args.warmup):
-        rows, st = prog.run_raw(None, w.n, RB_SYMMETRIC)
+        rows, st = step(prog)
     n_rows = len(rows[0])
     pairs_step = int(st.comparisons)
 
@@ -258,7 +359,7 @@ def main():
             e1 = torch.cuda.Event(enable_timing=True)
             h0 = time.perf_counter()
             e0.record(stream)
-            rows, st = prog.run_raw(None, w.n, RB_SYMMETRIC)
+            rows, st = step(prog)
             e1.record(stream)
             torch.cuda.synchronize()
             h1 = time.perf_counter()
@@ -286,7 +387,7 @@ def main():
     for _ in range(e2e_steps):
         drel = DeviceRelation(ctx, w.enc)  # H2D of every encoded column
         p2 = PathProgram(w.path, w.enc, compiled=prog.program, drel=drel)  # H2D of the program
-        rows2, st2 = p2.run_raw(None, w.n, RB_SYMMETRIC)  # evaluate + D2H of the rows
+        rows2, st2 = step(p2)  # evaluate + D2H of the rows
         assert len(rows2[0]) == n_rows
         p2.close()
         drel.close()
@@ -302,7 +403,9 @@ def main():
     parity = None
     roof = None
     peak, peak_kind = measured_peak()
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and w.blocks is not None:
+        cpu, parity, roof = blocks_cpu_parity(w, prog, args.cpu_pairs, kms, pairs_step, n_rows)
+    elif rank == 0 and world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
         srows = sample_rows(w.n, args.cpu_pairs)
         orc_rows, orc_pairs, orc_s, orc_evals = cpu_sample(w, prog.program, srows, cores)
@@ -341,7 +444,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": f"{w.name} n={w.n} per GPU ({WORKLOAD_DESC.get(w.name, w.name)}), "
-                                   "one symmetric partition per GPU",
+                                   + (f"{len(w.blocks)} blocks in one batched launch per GPU" if w.blocks is not None
+                                      else "one symmetric partition per GPU"),
                        "pairs_per_step_per_gpu": pairs_step, "rows_per_step_per_gpu": n_rows,
                        "l2": "flushed (512 MiB write) between timed steps", "parallelism": f"partition-per-gpu x{world}",
                        "collective": backend if world > 1 else None},

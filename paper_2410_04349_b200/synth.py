@@ -50,6 +50,16 @@ class Workload:
     rules: object
     path: object
     n: int
+    blocks: object = None  # [(refs int32, split)]: cross blocks / partitions instead of one partition
+
+    def pairs(self, symmetric: bool = True) -> int:
+        if self.blocks is None:
+            return self.n * (self.n - 1) // 2 if symmetric else self.n * (self.n - 1)
+        total = 0
+        for refs, split in self.blocks:
+            k = len(refs)
+            total += split * (k - split) if split >= 0 else (k * (k - 1) // 2 if symmetric else k * (k - 1))
+        return total
 
 
 def _distinct_rows(rng, n: int, width: int, domain: int) -> np.ndarray:
@@ -264,4 +274,76 @@ def edit_heavy(n: int = 1_000_000, seed: int = 11, plan_sample: int = 200_000) -
     return Workload("edit_heavy", enc, rules, path, n)
 
 
-WORKLOADS = {"citation3": citation3, "edit_heavy": edit_heavy}
+SYL = ["ka", "ri", "mo", "ta", "le", "sa", "no", "vi", "de", "ru", "mi", "ko", "na", "el", "an", "to", "be", "ga",
+       "lu", "si", "ha", "jo", "pe", "ze", "ul", "or", "in", "ma", "ne", "bo", "ch", "st", "fr", "gr", "th", "ph",
+       "wi", "ya", "qu", "ex", "ol", "ar", "en", "is", "um", "ad", "ed", "ik", "ov", "ey"]
+
+LINKAGE_RULES = [
+    {"id": "name", "when": [
+        {"t_attr": "block", "op": "eq", "s_attr": "block"},
+        {"t_attr": "name", "op": "sim", "s_attr": "name", "measure": "edit", "threshold": 0.85}]},
+    {"id": "addr", "when": [
+        {"t_attr": "block", "op": "eq", "s_attr": "block"},
+        {"t_attr": "addr", "op": "sim", "s_attr": "addr", "measure": "jaccard", "threshold": 0.6}]},
+]
+
+
+def linkage(n: int = 1_000_000, seed: int = 5, zipf_s: float = 1.3, n_blocks: int = 200_000,
+            plan_sample: int = 100_000) -> Workload:
+    """BASELINE config 5: two-table record linkage.  One relation holds both
+    sources (n/2 tuples each, a ``src`` split); a Zipf(1.3) block key makes a
+    few blocks very large and most tiny.  Every block is one cross run
+    (left = source A of the block, right = source B), i.e. run_cross per
+    block.  30% of B tuples are perturbed copies of
+    an A tuple of the same block."""
+    rng = np.random.default_rng(seed)
+    half = n // 2
+    p = 1.0 / np.arange(1, n_blocks + 1) ** zipf_s
+    p /= p.sum()
+    block = rng.choice(n_blocks, size=n, p=p).astype(np.int32)
+    # person names from syllables: ~2.5k first x ~125k last names
+    first = rng.integers(0, len(SYL) ** 2, size=n)
+    last = rng.integers(0, len(SYL) ** 3, size=n)
+    n_tok = rng.integers(8, 15, size=n)
+    addr = _distinct_rows(rng, n, 14, 5000)
+    # duplicates: B tuple j copies A tuple dup_of[j] (same block), lightly perturbed
+    dup = np.nonzero(rng.random(n - half) < 0.3)[0] + half
+    src = rng.integers(0, half, size=len(dup))
+    block[dup] = block[src]
+    first[dup], last[dup] = first[src], last[src]
+    addr[dup] = addr[src]
+    n_tok[dup] = n_tok[src]
+    drop = rng.random(len(dup)) < 0.3
+    n_tok[dup[drop]] = np.maximum(8, n_tok[dup[drop]] - 1)
+    import random as _random
+
+    prng = _random.Random(seed)
+    S = len(SYL)
+    names = [(SYL[a // S] + SYL[a % S] + " " + SYL[b // (S * S)] + SYL[(b // S) % S] + SYL[b % S]).encode()
+             for a, b in zip(first.tolist(), last.tolist())]
+    for j in dup[rng.random(len(dup)) < 0.5]:
+        names[j] = _perturb(prng, names[j], 1)
+    t_off, t_ids = _csr_from_padded(addr, n_tok, sort_rows=True)
+    enc = Encoded(n)
+    enc.add(("codes", "block"), Column(COL_CODES, block))
+    enc.add(("chars", "name"), _chars_column(names))
+    enc.add(("tokens", "addr"), Column(COL_TOKENS, t_ids.astype(np.int32), t_off, np.zeros(n, np.uint8)))
+    # blocks: group tuple ids by block key and source
+    order = np.lexsort((np.arange(n) >= half, block))
+    bk = block[order]
+    starts = np.flatnonzero(np.r_[True, bk[1:] != bk[:-1]])
+    ends = np.r_[starts[1:], n]
+    blocks = []
+    for a, b in zip(starts, ends):
+        ids = order[a:b].astype(np.int32)
+        nl = int((ids < half).sum())  # lexsort put the A side first: left = ids[:nl]
+        if nl and nl < len(ids):
+            blocks.append((ids, nl))
+    import json
+
+    rules = parse_ruleset(json.dumps(LINKAGE_RULES))
+    path = data_aware_plan(enc, rules, sample=plan_sample, seed=seed)
+    return Workload("linkage", enc, rules, path, n, blocks=blocks)
+
+
+WORKLOADS = {"citation3": citation3, "edit_heavy": edit_heavy, "linkage": linkage}
