@@ -18,6 +18,7 @@ from .errors import ConfigError, RuleBlockError
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "librbgpu.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "rbgpu.h")
+HEADERS = [HEADER, os.path.join(os.path.dirname(HERE), "include", "rbencode.h")]
 
 RB_OK = 0
 RB_ERR_INVALID, RB_ERR_CUDA, RB_ERR_OOM, RB_ERR_LIMIT, RB_ERR_INTERNAL = -1, -2, -3, -4, -5
@@ -79,13 +80,19 @@ _SIGNATURES = {
     "rb_result_copy": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "rb_result_stats": (ctypes.c_int, [c_vp, ctypes.POINTER(RbStats)]),
     "rb_result_destroy": (ctypes.c_int, [c_vp]),
+    # include/rbencode.h
+    "rb_encode_eq_codes": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int64, c_vp]),
+    "rb_encode_tokens": (ctypes.c_int64, [c_vp, c_vp, c_vp, ctypes.c_int64, c_vp, c_vp, c_i32p]),
+    "rb_encode_chars": (ctypes.c_int64, [c_vp, c_vp, c_vp, ctypes.c_int64, c_vp, c_vp]),
 }
 
 
 def header_symbols() -> list[str]:
-    """Every function the public header declares."""
-    text = open(HEADER).read()
-    return re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(rb_\w+)\s*\(", text, flags=re.M)
+    """Every function the public headers declare."""
+    out = []
+    for h in HEADERS:
+        out += re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(rb_\w+)\s*\(", open(h).read(), flags=re.M)
+    return out
 
 
 _lib = None

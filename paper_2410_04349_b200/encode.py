@@ -220,6 +220,40 @@ def _const_key(const):
     return ("num", float(const)) if isinstance(const, (int, float)) and not isinstance(const, bool) else ("str", const)
 
 
+def _ascii_column(cols: list):
+    """(bytes, offsets int64, missing uint8) of the concatenated str columns
+    when every present value is an ASCII ``str``; None otherwise (the
+    Python encoder then keeps CPython's full Unicode semantics)."""
+    import os
+
+    if os.environ.get("RB_NATIVE_ENCODE", "1") == "0":
+        return None
+    vals, miss = [], []
+    for col in cols:
+        for v in col:
+            if is_missing(v):
+                vals.append("")
+                miss.append(1)
+            elif type(v) is str:
+                vals.append(v)
+                miss.append(0)
+            else:
+                return None
+    text = "".join(vals)
+    if not text.isascii():
+        return None
+    lens = np.fromiter(map(len, vals), dtype=np.int64, count=len(vals))
+    offsets = np.zeros(len(vals) + 1, dtype=np.int64)
+    np.cumsum(lens, out=offsets[1:])
+    return text.encode("ascii"), offsets, np.array(miss, dtype=np.uint8)
+
+
+def _native():
+    from . import _lib
+
+    return _lib.lib(), _lib
+
+
 class RelationEncoding(Encoded):
     """Lazily encodes the columns a path touches, from a ``Relation``
     (ours or the reference's)."""
@@ -246,6 +280,14 @@ class RelationEncoding(Encoded):
 
     def _build(self, key):
         tag = key[0]
+        if tag == "codes" and not self._numeric(key[1]):
+            nat = _ascii_column([self._column(key[1])])
+            if nat is not None:  # rb_encode_eq_codes: strip + first-appearance dictionary
+                buf, offs, miss = nat
+                L, lb = _native()
+                out = np.empty(self.n, dtype=np.int32)
+                L.rb_encode_eq_codes(buf, lb.ptr(offs), lb.ptr(miss), self.n, lb.ptr(out))
+                return Column(COL_CODES, out)
         if tag == "codes":
             numeric = self._numeric(key[1])
             mapping: dict = {}
@@ -272,6 +314,14 @@ class RelationEncoding(Encoded):
             a, b = self._tokens([self._column(key[1]), self._column(key[2])], vocab)
             return a, b
         if tag == "chars":
+            nat = _ascii_column([self._column(key[1])])
+            if nat is not None:  # rb_encode_chars: strip + casefold, uint8 (all ASCII)
+                buf, offs, miss = nat
+                L, lb = _native()
+                out_off = np.empty(self.n + 1, dtype=np.int64)
+                out = np.empty(max(1, len(buf)), dtype=np.uint8)
+                m = L.rb_encode_chars(buf, lb.ptr(offs), lb.ptr(miss), self.n, lb.ptr(out_off), lb.ptr(out))
+                return Column(COL_CHARS, out[:m].copy(), out_off, miss)
             col = self._column(key[1])
             missing = np.fromiter((is_missing(v) for v in col), dtype=np.uint8, count=self.n)
             texts = ["" if is_missing(v) else fold_text(value_text(v)) for v in col]
@@ -285,6 +335,23 @@ class RelationEncoding(Encoded):
         return None
 
     def _tokens(self, cols: list, vocab: dict) -> list:
+        nat = _ascii_column(cols)
+        if nat is not None:  # rb_encode_tokens over the columns back to back (one shared vocabulary)
+            buf, offs, miss = nat
+            L, lb = _native()
+            total = len(offs) - 1
+            out_off = np.empty(total + 1, dtype=np.int64)
+            ids = np.empty(max(1, len(buf)), dtype=np.int32)
+            vs = lb.ctypes.c_int32(0)
+            nnz = L.rb_encode_tokens(buf, lb.ptr(offs), lb.ptr(miss), total, lb.ptr(out_off), lb.ptr(ids),
+                                     lb.ctypes.byref(vs))
+            ids = ids[:nnz]
+            res = []
+            for k in range(len(cols)):
+                a, b = k * self.n, (k + 1) * self.n
+                o = out_off[a:b + 1] - out_off[a]
+                res.append(Column(COL_TOKENS, ids[out_off[a]:out_off[b]].copy(), o, miss[a:b].copy()))
+            return res
         out = []
         for col in cols:
             rows = []
