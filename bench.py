@@ -285,7 +285,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="citation3")
-    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--tuples", dest="n", type=int, default=1_000_000, help="tuples per GPU")
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--cpu-pairs", type=int, default=120_000_000, help="oracle sample size (pairs)")
     ap.add_argument("--e2e-steps", type=int, default=None)
