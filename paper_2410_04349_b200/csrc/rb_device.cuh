@@ -407,6 +407,21 @@ struct __align__(16) Tile {
 #define RB_STR_ALWAYS(f) ((f) == 0 ? SPEC_STR0_ALWAYS : SPEC_STR1_ALWAYS)
 #define RB_FULLTAB SPEC_FULLTAB
 #define RB_TOK2D SPEC_TOK2D
+// rule masks are compile-time constants too: a failed test becomes one
+// predicated LOP3 on the live-rule mask
+#define RB_PICK6(f, P) ((f) == 0 ? P##0 : (f) == 1 ? P##1 : (f) == 2 ? P##2 : (f) == 3 ? P##3 : (f) == 4 ? P##4 : P##5)
+#define RB_PICK8(f, P) ((f) < 6 ? RB_PICK6(f, P) : (f) == 6 ? P##6 : P##7)
+#define RB_PICK2(f, P) ((f) == 0 ? P##0 : P##1)
+#define RB_PICK4(z, P) ((z) == 0 ? P##0 : (z) == 1 ? P##1 : (z) == 2 ? P##2 : P##3)
+#define RB_ALL_RULES SPEC_ALL_RULES
+#define RB_EQ_KILL(f) RB_PICK6(f, SPEC_EQ_KILL_)
+#define RB_CONST_KILL(k) RB_PICK8(k, SPEC_CONST_KILL_)
+#define RB_TOK_ROWKILL(f) RB_PICK2(f, SPEC_TOK_ROWKILL_)
+#define RB_STR_ROWKILL(f) RB_PICK2(f, SPEC_STR_ROWKILL_)
+#define RB_TOK_RULES(f) RB_PICK2(f, SPEC_TOK_RULES_)
+#define RB_STR_RULES(f) RB_PICK2(f, SPEC_STR_RULES_)
+#define RB_TOK_KILL(f, z) ((f) == 0 ? RB_PICK4(z, SPEC_TOK0_KILL_) : RB_PICK4(z, SPEC_TOK1_KILL_))
+#define RB_STR_KILL(f, z) ((f) == 0 ? RB_PICK4(z, SPEC_STR0_KILL_) : RB_PICK4(z, SPEC_STR1_KILL_))
 #else
 #define RB_NEQ F.n_eq
 #define RB_NCONST F.n_const
@@ -420,6 +435,15 @@ struct __align__(16) Tile {
 #define RB_STR_ALWAYS(f) F.str_always[f]
 #define RB_FULLTAB F.full_tab
 #define RB_TOK2D F.tok2d
+#define RB_ALL_RULES F.all_rules
+#define RB_EQ_KILL(f) F.eq_kill[f]
+#define RB_CONST_KILL(k) F.const_kill[k]
+#define RB_TOK_ROWKILL(f) F.tok_kill[f]
+#define RB_STR_ROWKILL(f) F.str_kill[f]
+#define RB_TOK_RULES(f) F.tok_rules[f]
+#define RB_STR_RULES(f) F.str_rules[f]
+#define RB_TOK_KILL(f, z) F.tok_slot[f][z].kill
+#define RB_STR_KILL(f, z) F.str_slot[f][z].kill
 #endif
 
 // Shared tables start at TAB_BASE so that the (discarded) lookups of pairs
@@ -463,7 +487,7 @@ struct Outer {
         alive0 = 0;
         if (ok) {
             ti = R.refs ? R.refs[i] : (int32_t)i;
-            alive0 = (Mask)F.all_rules;
+            alive0 = (Mask)RB_ALL_RULES;
             if (mode == MODE_SYM) {
                 const int64_t lo = col0 > i + 1 ? col0 : i + 1;
                 my_pairs += (unsigned long long)(col1 > lo ? col1 - lo : 0);
@@ -481,12 +505,12 @@ struct Outer {
                 if (c >= 0)
                     ocode[f] = c;
                 else
-                    alive0 &= ~(Mask)F.eq_kill[f];
+                    alive0 &= ~(Mask)RB_EQ_KILL(f);
             }
         }
 #pragma unroll
         for (int k = 0; k < MAX_CONST; k++)
-            if (k < RB_NCONST && ok && !__ldg(F.const_mask[k] + ti)) alive0 &= ~(Mask)F.const_kill[k];
+            if (k < RB_NCONST && ok && !__ldg(F.const_mask[k] + ti)) alive0 &= ~(Mask)RB_CONST_KILL(k);
 #pragma unroll
         for (int f = 0; f < MAX_TOK; f++) {
             olen[f] = -1;
@@ -502,7 +526,7 @@ struct Outer {
                 olen[f] = __ldg(F.tok_olen[f] + ti);
                 ohash[f] = __ldg(F.tok_ohash[f] + ti);
                 // jaccard and exact_token are false for a missing or empty t side
-                if (olen[f] <= 0) alive0 &= ~(Mask)F.tok_kill[f];
+                if (olen[f] <= 0) alive0 &= ~(Mask)RB_TOK_ROWKILL(f);
                 if (RB_TOK2D) {
                     const int nn = olen[f] > 0 ? olen[f] : 0;
 #pragma unroll
@@ -534,7 +558,7 @@ struct Outer {
             if (f < RB_NSTR && ok) {
                 oslen[f] = __ldg(F.str_olen[f] + ti);
                 obag[f] = __ldg(F.str_obag[f] + ti);
-                if (oslen[f] < 0) alive0 &= ~(Mask)F.str_kill[f];  // missing t side: edit is false
+                if (oslen[f] < 0) alive0 &= ~(Mask)RB_STR_ROWKILL(f);  // missing t side: edit is false
             }
         }
     }
@@ -572,7 +596,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
             alive[r] = (AllValid || (jj >= o[r].jj_lo && jj != o[r].jj_skip)) ? o[r].alive0 : (Mask)0;
 #pragma unroll
             for (int f = 0; f < MAX_EQ; f++)
-                if (f < RB_NEQ && o[r].ocode[f] != T.eq[f][jj]) alive[r] &= ~(Mask)F.eq_kill[f];
+                if (f < RB_NEQ && o[r].ocode[f] != T.eq[f][jj]) alive[r] &= ~(Mask)RB_EQ_KILL(f);
         }
 
 #pragma unroll
@@ -581,7 +605,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
             Mask need = 0;
 #pragma unroll
             for (int r = 0; r < ROWS; r++) need |= alive[r];
-            if (!RB_TOK_ALWAYS(f) && !__any_sync(FULL, (need & (Mask)F.tok_rules[f]) != 0)) continue;
+            if (!RB_TOK_ALWAYS(f) && !__any_sync(FULL, (need & (Mask)RB_TOK_RULES(f)) != 0)) continue;
             const int m = T.toklen[f][jj];
             const uint32_t m4 = (uint32_t)m << 2;  // byte offset of column m within a need[n][.] row
             const uint4 is = T.toksig[f][jj];
@@ -627,7 +651,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
             Mask need = 0;
 #pragma unroll
             for (int r = 0; r < ROWS; r++) need |= alive[r];
-            if (!RB_STR_ALWAYS(f) && !__any_sync(FULL, (need & (Mask)F.str_rules[f]) != 0)) continue;
+            if (!RB_STR_ALWAYS(f) && !__any_sync(FULL, (need & (Mask)RB_STR_RULES(f)) != 0)) continue;
             const int lb = T.strlen_[f][jj];
             const uint4 ib = T.strbag[f][jj];
 #pragma unroll
@@ -646,7 +670,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                         const int mg = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap0) ? tab[fs.off0 + L] : INT_MAX;
                         const int md = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap1) ? tab[fs.off1 + L] : INT_MAX;
                         const bool ok = present & ((L == 0) | ((gap <= mg) & (lower <= md)));
-                        if (!ok) alive[r] &= ~(Mask)fs.kill;
+                        if (!ok) alive[r] &= ~(Mask)RB_STR_KILL(f, z);
                     }
                 }
             }
