@@ -205,8 +205,10 @@ static __device__ __forceinline__ uint32_t char_at(const DevColumn& c, int64_t k
 }
 
 // Banded Levenshtein with cutoff k (Ukkonen): exact when the distance is
-// <= k, otherwise returns k+1.  Rows run over the shorter string, the
-// single DP row (longer string) lives in this thread's scratch slice.
+// <= k, otherwise returns k+1.  Rows run over the shorter string.  For
+// k <= 31 the band lives in a 64-entry ring in thread-local memory (local
+// memory is lane-interleaved, so a warp's accesses coalesce and stay in L1);
+// wider bands use the thread's slice of the global scratch row.
 static __device__ int lev_bounded(const DevColumn& ca, int64_t a0, int la, const DevColumn& cb, int64_t b0, int lb, int k,
                            int32_t* row) {
     const DevColumn* cs = &ca;
@@ -224,6 +226,34 @@ static __device__ int lev_bounded(const DevColumn& ca, int64_t a0, int la, const
     const int INF = k + 1;
     if (m - n > k) return INF;
     if (n == 0) return m;
+    if (k <= 31) {
+        int ring[64];  // ring[j & 63] = D[i-1][j] over the band of row i-1
+        for (int j = 0; j <= min(k, m); j++) ring[j] = j;
+        for (int i = 1; i <= n; i++) {
+            const uint32_t ai = char_at(*cs, s0 + i - 1);
+            const int jlo = max(0, i - k), jhi = min(m, i + k);
+            int diag = jlo >= 1 ? ring[(jlo - 1) & 63] : 0;
+            int left = INF, rmin = INF;
+            for (int j = jlo; j <= jhi; j++) {
+                const int up = j <= i - 1 + k ? ring[j & 63] : INF;  // D[i-1][j], INF outside its band
+                int v;
+                if (j == 0) {
+                    v = i;
+                } else {
+                    v = diag + (ai == char_at(*cl, l0 + j - 1) ? 0 : 1);
+                    v = min(v, up + 1);
+                    v = min(v, left + 1);
+                }
+                v = min(v, INF);
+                diag = up;
+                ring[j & 63] = v;
+                left = v;
+                rmin = min(rmin, v);
+            }
+            if (rmin > k) return INF;
+        }
+        return ring[m & 63];
+    }
     for (int j = 0; j <= m; j++) row[j] = min(j, INF);
     for (int i = 1; i <= n; i++) {
         const uint32_t ai = char_at(*cs, s0 + i - 1);
