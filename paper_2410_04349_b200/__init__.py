@@ -23,14 +23,17 @@ from .engine import (
     split_rows_by_pairs,
 )
 from .errors import ConfigError, DataParseError, RuleBlockError, RuleParseError, SchemaError, ValidationError
+from .pipeline import BandingConfig, PipelineConfig, PipelineResult, iter_partitions, pipeline_run
 from .plan import Checkpoint, EvalPredicate, ExecutionPath, plan_from_stats
+from .scheduler import MultiDeviceEngine
 from .relation import MISSING, DataPartition, Kind, Relation, Schema, TupleRecord, relation_from_rows
 from .rules import MDRule, Predicate, RuleSet, parse_ruleset, predicate_universe
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BlockStats", "CandidateSet", "Checkpoint", "ConfigError", "DataParseError", "DataPartition", "Encoded",
+    "BandingConfig", "BlockStats", "CandidateSet", "MultiDeviceEngine", "PipelineConfig", "PipelineResult",
+    "iter_partitions", "pipeline_run", "Checkpoint", "ConfigError", "DataParseError", "DataPartition", "Encoded",
     "EngineConfig", "EvalPredicate", "ExecutionPath", "Kind", "MDRule", "MISSING", "PathProgram", "Predicate",
     "Relation", "RelationEncoding", "RuleBlockError", "RuleParseError", "RuleSet", "RunStats", "Schema",
     "SchemaError", "TupleRecord", "ValidationError", "compile_program", "context", "parse_ruleset",

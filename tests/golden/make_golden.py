@@ -267,8 +267,48 @@ def edges():
     write("edge_unicode", rel, path, [case(rel, path, name="sym")])
 
 
+def pipelines(tmp):
+    """Reference pipeline_run (pipeline.py:245-433) on frozen plans:
+    partitioning + every partition + optional sibling pulls + collect."""
+    from ruleblock.partitioning import BandingConfig
+    from ruleblock.pipeline import PipelineConfig, make_devices, pipeline_run
+    from ruleblock.planner.plan import PlanBundle
+
+    def bundle_for(rel, rules):
+        b = generate_plan(rel, rules, FAST_PLANNER)
+        return b
+
+    jobs = []
+    rows, doc, _ = citation_benchmark(n_tuples=1200, n_matches=500)
+    jobs.append(("pipeline_citation", rows_to_relation(rows, CITATION_HEADER, tmp, name="pc.csv"), doc))
+    for seed in (3, 7, 12):
+        rows, doc = random_instance(seed)
+        jobs.append((f"pipeline_random_{seed:03d}", rows_to_relation(rows, ["cat", "num", "stext", "ltext"], tmp,
+                                                                     name=f"pr{seed}.csv"), doc))
+    for name, rel, doc in jobs:
+        rules = parse_ruleset(json.dumps(doc))
+        bundle = bundle_for(rel, rules)
+        cases = []
+        for max_size, pulls, sym in ((32, False, True), (32, True, True), (8, True, True), (16, False, False)):
+            res = pipeline_run(rel, rules, PipelineConfig(async_mode=False, max_partition_size=max_size,
+                                                          enable_pulls=pulls, banding=BandingConfig(rows=4, seed=0)),
+                               EngineConfig(num_blocks=1, symmetric_mode=sym), make_devices(2), plan=bundle)
+            cases.append({"name": f"max{max_size}_pulls{int(pulls)}_sym{int(sym)}", "max_partition_size": max_size,
+                          "enable_pulls": pulls, "symmetric": sym, "n_partitions": res.n_partitions,
+                          "expected": sorted([int(t), int(s), r] for t, s, r in res.candidates.pairs)})
+        doc_out = {"relation": relation_doc(rel), "path": path_to_dict(bundle.path), "cases": cases}
+        with gzip.open(os.path.join(HERE, name + ".json.gz"), "wt") as fh:
+            json.dump(doc_out, fh, separators=(",", ":"))
+        print(f"{name}: {len(rel)} tuples, {[c['n_partitions'] for c in cases]} partitions, "
+              f"{[len(c['expected']) for c in cases]} rows")
+
+
 def main():
     seeds = range(int(os.environ.get("RB_GOLDEN_SEEDS", "60")))
+    if os.environ.get("RB_GOLDEN_ONLY") == "pipelines":
+        with tempfile.TemporaryDirectory() as tmp:
+            pipelines(tmp)
+        return
     with tempfile.TemporaryDirectory() as tmp:
         products(tmp)
         edges()
@@ -276,6 +316,7 @@ def main():
         grouped(tmp)
         if os.environ.get("RB_GOLDEN_SKIP_CITATION") != "1":
             citation(tmp)
+        pipelines(tmp)
 
 
 if __name__ == "__main__":

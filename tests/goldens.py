@@ -18,7 +18,17 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def names() -> list[str]:
-    return sorted(os.path.basename(p)[: -len(".json.gz")] for p in glob.glob(os.path.join(GOLDEN, "*.json.gz")))
+    """Engine-level fixtures (one run per case)."""
+    return sorted(n for n in _all() if not n.startswith("pipeline_"))
+
+
+def pipeline_names() -> list[str]:
+    """Reference pipeline_run fixtures (partitioning + pulls + collect)."""
+    return sorted(n for n in _all() if n.startswith("pipeline_"))
+
+
+def _all() -> list[str]:
+    return [os.path.basename(p)[: -len(".json.gz")] for p in glob.glob(os.path.join(GOLDEN, "*.json.gz"))]
 
 
 def load(name: str):

@@ -1,0 +1,60 @@
+"""Plan-derived partitioning restated in pipeline.py must
+produce the reference's partitions exactly: same pids, refs, branches, key
+groups and sibling groups (reference importable in the build container)."""
+
+import json
+import os
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+from paper_2410_04349_b200.pipeline import BandingConfig, collect, iter_partitions, mix64, sibling_pull_pairs, stable_hash64
+
+REF = "/root/reference/pkg/src"
+HAVE_REF = os.path.isdir(REF)
+
+
+def test_hash_helpers_are_deterministic():
+    assert stable_hash64("abc", 0) == stable_hash64("abc", 0) != stable_hash64("abc", 1)
+    x = np.array([1, 2, 3], dtype=np.uint64)
+    assert np.array_equal(mix64(x, 5), mix64(x, 5))
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="reference not importable here")
+@pytest.mark.parametrize("max_size", [3, 16, 512])
+def test_partitions_equal_reference(max_size):
+    sys.path.insert(0, REF)
+    from ruleblock.bench import FAST_PLANNER
+    from ruleblock.datasets import CITATION_HEADER, citation_benchmark, random_instance, rows_to_relation
+    from ruleblock.partitioning import BandingConfig as RB
+    from ruleblock.partitioning import derive_partitioners
+    from ruleblock.partitioning import iter_partitions as ref_iter
+    from ruleblock.partitioning import sibling_pull_pairs as ref_pulls
+    from ruleblock.planner.plan import generate_plan
+    from ruleblock.rules import parse_ruleset
+
+    with tempfile.TemporaryDirectory() as tmp:
+        cases = []
+        for seed in range(6):
+            rows, doc = random_instance(seed)
+            cases.append((rows_to_relation(rows, ["cat", "num", "stext", "ltext"], tmp, name=f"p{seed}.csv"), doc))
+        rows, doc, _ = citation_benchmark(n_tuples=800, n_matches=300)
+        cases.append((rows_to_relation(rows, CITATION_HEADER, tmp, name="cit.csv"), doc))
+        for rel, doc in cases:
+            bundle = generate_plan(rel, parse_ruleset(json.dumps(doc)), FAST_PLANNER)
+            want = list(ref_iter(rel, derive_partitioners(bundle.tree, RB(rows=4, seed=0)), max_size))
+            got = list(iter_partitions(rel, bundle.path, max_size, BandingConfig(rows=4, seed=0)))
+            assert [(p.pid, p.tuple_refs, p.branch_id, p.key_group, p.sibling_group) for p in got] == \
+                   [(p.pid, p.tuple_refs, p.branch_id, p.key_group, p.sibling_group) for p in want]
+            assert sibling_pull_pairs(got) == ref_pulls(want)
+
+
+def test_collect_keeps_earliest_rule_per_pair():
+    from paper_2410_04349_b200.engine import CandidateSet
+
+    a = CandidateSet(arrays=(np.array([1, 1, 2]), np.array([5, 5, 3]), np.array([2, 0, 1])), rule_ids=["a", "b", "c"])
+    b = CandidateSet(arrays=(np.array([1, 4]), np.array([5, 7]), np.array([1, 2])), rule_ids=["a", "b", "c"])
+    cs = collect([a, b], ["a", "b", "c"])
+    assert sorted(cs.pairs) == [(1, 5, "a"), (2, 3, "b"), (4, 7, "c")]
