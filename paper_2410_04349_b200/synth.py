@@ -346,4 +346,87 @@ def linkage(n: int = 1_000_000, seed: int = 5, zipf_s: float = 1.3, n_blocks: in
     return Workload("linkage", enc, rules, path, n, blocks=blocks)
 
 
-WORKLOADS = {"citation3": citation3, "edit_heavy": edit_heavy, "linkage": linkage}
+PERSON5_RULES = [
+    {"id": "R1", "when": [
+        {"t_attr": "last", "op": "eq", "s_attr": "last"},
+        {"t_attr": "dob", "op": "eq", "s_attr": "dob"},
+        {"t_attr": "first", "op": "sim", "s_attr": "first", "measure": "edit", "threshold": 0.8}]},
+    {"id": "R2", "when": [
+        {"t_attr": "zip", "op": "eq", "s_attr": "zip"},
+        {"t_attr": "address", "op": "sim", "s_attr": "address", "measure": "jaccard", "threshold": 0.7}]},
+    {"id": "R3", "when": [
+        {"t_attr": "phone", "op": "eq", "s_attr": "phone"}]},
+    {"id": "R4", "when": [
+        {"t_attr": "first", "op": "eq", "s_attr": "first"},
+        {"t_attr": "zip", "op": "eq", "s_attr": "zip"},
+        {"t_attr": "last", "op": "sim", "s_attr": "last", "measure": "edit", "threshold": 0.85}]},
+    {"id": "R5", "when": [
+        {"t_attr": "dob", "op": "eq", "s_attr": "dob"},
+        {"t_attr": "address", "op": "sim", "s_attr": "address", "measure": "jaccard", "threshold": 0.6},
+        {"t_attr": "first", "op": "sim", "s_attr": "first", "measure": "edit", "threshold": 0.7}]},
+]
+
+
+def person5(n: int = 10_000_000, seed: int = 4, plan_sample: int = 100_000) -> Workload:
+    """BASELINE config 4: a person-style relation -- zip (100k, Zipf), last
+    name (50k, Zipf), first name (5k), date of birth, phone (90% unique),
+    address (8-14 tokens) -- with five rules mixing equality roots with edit
+    and Jaccard tails, planned data-aware from sampled selectivities
+    (SURVEY §8d config 4).  20% of tuples are perturbed duplicates."""
+    rng = np.random.default_rng(seed)
+
+    def zipf(k, size, a=1.1):
+        p = 1.0 / np.arange(1, k + 1) ** a
+        return rng.choice(k, size=size, p=p / p.sum()).astype(np.int32)
+
+    zipc = zipf(100_000, n)
+    last_id = zipf(50_000, n)
+    first_id = rng.integers(0, 5_000, size=n)
+    dob = rng.integers(0, 30_000, size=n).astype(np.int32)
+    phone = rng.integers(0, 1 << 30, size=n).astype(np.int32)
+    shared = rng.random(n) < 0.1  # 10% of phones come from a small shared pool
+    phone[shared] = rng.integers(0, 1000, size=int(shared.sum()), dtype=np.int32)
+    n_tok = rng.integers(8, 15, size=n)
+    addr = _distinct_rows(rng, n, 14, 200_000)
+    dup = np.flatnonzero(rng.random(n) < 0.2)
+    src = rng.integers(0, n, size=len(dup))
+    for arr in (zipc, last_id, first_id, dob, phone, n_tok):
+        arr[dup] = arr[src]
+    addr[dup] = addr[src]
+    import random as _random
+
+    prng = _random.Random(seed)
+    S = len(SYL)
+
+    def name_of(k, parts):
+        out = []
+        for _ in range(parts):
+            out.append(SYL[k % S])
+            k //= S
+        return "".join(out).encode()
+
+    firsts = [name_of(int(k), 3) for k in first_id]
+    lasts = [name_of(int(k) * 7919 + 13, 4) for k in last_id]
+    for j in dup[rng.random(len(dup)) < 0.5]:
+        firsts[j] = _perturb(prng, firsts[j], 1)
+    # equality codes of the same attribute values the edit predicates read
+    first_codes = np.unique(np.array(firsts, dtype=object), return_inverse=True)[1].astype(np.int32)
+    last_codes = np.unique(np.array(lasts, dtype=object), return_inverse=True)[1].astype(np.int32)
+    t_off, t_ids = _csr_from_padded(addr, n_tok, sort_rows=True)
+    enc = Encoded(n)
+    enc.add(("codes", "zip"), Column(COL_CODES, zipc))
+    enc.add(("codes", "last"), Column(COL_CODES, last_codes))
+    enc.add(("codes", "first"), Column(COL_CODES, first_codes))
+    enc.add(("codes", "dob"), Column(COL_CODES, dob))
+    enc.add(("codes", "phone"), Column(COL_CODES, phone))
+    enc.add(("chars", "first"), _chars_column(firsts))
+    enc.add(("chars", "last"), _chars_column(lasts))
+    enc.add(("tokens", "address"), Column(COL_TOKENS, t_ids.astype(np.int32), t_off, np.zeros(n, np.uint8)))
+    import json
+
+    rules = parse_ruleset(json.dumps(PERSON5_RULES))
+    path = data_aware_plan(enc, rules, sample=plan_sample, seed=seed)
+    return Workload("person5", enc, rules, path, n)
+
+
+WORKLOADS = {"citation3": citation3, "edit_heavy": edit_heavy, "linkage": linkage, "person5": person5}
