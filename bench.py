@@ -384,13 +384,22 @@ def main():
     h2d += prog.program.tables.nbytes + prog.program.slots.nbytes + 4 * 4 * len(prog.program.ins_op)
     barrier()
     t0 = time.perf_counter()
+    phase = {"upload": 0.0, "program": 0.0, "run": 0.0, "free": 0.0}
     for _ in range(e2e_steps):
+        q0 = time.perf_counter()
         drel = DeviceRelation(ctx, w.enc)  # H2D of every encoded column
+        q1 = time.perf_counter()
         p2 = PathProgram(w.path, w.enc, compiled=prog.program, drel=drel)  # H2D of the program
+        q2 = time.perf_counter()
         rows2, st2 = step(p2)  # evaluate + D2H of the rows
+        q3 = time.perf_counter()
         assert len(rows2[0]) == n_rows
         p2.close()
         drel.close()
+        q4 = time.perf_counter()
+        for k, v in zip(phase, (q1 - q0, q2 - q1, q3 - q2, q4 - q3)):
+            phase[k] += v / e2e_steps
+    print("e2e phases (s): " + ", ".join(f"{k} {v:.4f}" for k, v in phase.items()), file=sys.stderr)
     torch.cuda.synchronize()
     e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=red_dev)
     if world > 1:

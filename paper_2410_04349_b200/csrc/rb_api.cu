@@ -44,21 +44,32 @@ int fail(int code, const char* fmt, ...) {
                         #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
     } while (0)
 
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync
+// with an unbounded release threshold): relations, programs and results are
+// created and dropped per call on the e2e path, and plain cudaFree there
+// costs tens to hundreds of milliseconds.
+inline cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st) {
+    return cudaMallocAsync(p, std::max(bytes, (size_t)16), st);
+}
+inline void dev_free(void* p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
-    cudaError_t grow(size_t need) {
+    cudaError_t grow(size_t need, cudaStream_t st) {
         if (need <= bytes) return cudaSuccess;
-        if (p) cudaFree(p);
+        dev_free(p, st);
         p = nullptr;
         bytes = 0;
         size_t want = std::max(need, (size_t)256);
-        cudaError_t e = cudaMalloc(&p, want);
+        cudaError_t e = dev_alloc(&p, want, st);
         if (e == cudaSuccess) bytes = want;
         return e;
     }
-    void release() {
-        if (p) cudaFree(p);
+    void release(cudaStream_t st) {
+        dev_free(p, st);
         p = nullptr;
         bytes = 0;
     }
@@ -143,6 +154,12 @@ int rb_ctx_create(int device, rb_ctx** out) {
     }
     c->own_stream = true;
     c->blocks_per_sm = pair_kernel_blocks_per_sm();
+    cudaMemPool_t mp;
+    if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
     if (cudaMallocHost(&c->host_ctr, sizeof(unsigned long long) * (4 + RB_MAX_SLOTS)) != cudaSuccess) {
         cudaGetLastError();
         c->host_ctr = nullptr;
@@ -164,14 +181,14 @@ int rb_ctx_destroy(rb_ctx* c) {
     if (!c) return RB_OK;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    c->items.release();
-    c->refs.release();
-    c->counters.release();
-    c->scratch.release();
+    c->items.release(c->stream);
+    c->refs.release(c->stream);
+    c->counters.release(c->stream);
+    c->scratch.release(c->stream);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
-    for (int k = 0; k < 3; k++)
-        if (c->pool[k]) cudaFree(c->pool[k]);
+    for (int k = 0; k < 3; k++) dev_free(c->pool[k], c->stream);
+    if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->host_ctr) cudaFreeHost(c->host_ctr);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -195,7 +212,7 @@ int rb_relation_create(rb_ctx* c, int64_t n, rb_rel** out) {
 static cudaError_t upload(rb_rel* r, const void* src, size_t bytes, void** dst) {
     *dst = nullptr;
     if (bytes == 0) bytes = 16;  // never hand out null for an empty array
-    cudaError_t e = cudaMalloc(dst, bytes);
+    cudaError_t e = dev_alloc(dst, bytes, r->ctx->stream);
     if (e != cudaSuccess) return e;
     r->allocs.push_back(*dst);
     if (src) return cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, r->ctx->stream);
@@ -305,8 +322,8 @@ int rb_relation_destroy(rb_rel* r) {
     if (!r) return RB_OK;
     cudaSetDevice(r->ctx->device);
     cudaStreamSynchronize(r->ctx->stream);
-    for (void* p : r->allocs) cudaFree(p);
-    if (r->d_cols) cudaFree(r->d_cols);
+    for (void* p : r->allocs) dev_free(p, r->ctx->stream);
+    dev_free(r->d_cols, r->ctx->stream);
     delete r;
     return RB_OK;
 }
@@ -383,13 +400,13 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
     P->n_slots = n_slots;
     auto up = [&](const void* src, size_t bytes, void** dst) -> cudaError_t {
         *dst = nullptr;
-        cudaError_t e = cudaMalloc(dst, std::max(bytes, (size_t)16));
+        cudaError_t e = dev_alloc(dst, bytes, c->stream);
         if (e != cudaSuccess) return e;
         P->allocs.push_back(*dst);
         return cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
     };
     auto bail = [&](cudaError_t e) {
-        for (void* p : P->allocs) cudaFree(p);
+        for (void* p : P->allocs) dev_free(p, c->stream);
         delete P;
         return fail(e == cudaErrorMemoryAllocation ? RB_ERR_OOM : RB_ERR_CUDA, "program upload: %s",
                     cudaGetErrorString(e));
@@ -634,7 +651,7 @@ int rb_program_destroy(rb_prog* P) {
     if (!P) return RB_OK;
     cudaSetDevice(P->ctx->device);
     cudaStreamSynchronize(P->ctx->stream);
-    for (void* p : P->allocs) cudaFree(p);
+    for (void* p : P->allocs) dev_free(p, P->ctx->stream);
     delete P;
     return RB_OK;
 }
@@ -665,10 +682,10 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     if (!res) return fail(RB_ERR_OOM, "host allocation failed");
     res->stream = c->stream;
     auto cleanup = [&](int rc) {
-        if (res->d_t) cudaFree(res->d_t);
-        if (res->d_s) cudaFree(res->d_s);
-        if (res->d_r) cudaFree(res->d_r);
-        if (res->d_p) cudaFree(res->d_p);
+        dev_free(res->d_t, c->stream);
+        dev_free(res->d_s, c->stream);
+        dev_free(res->d_r, c->stream);
+        dev_free(res->d_p, c->stream);
         delete res;
         return rc;
     };
@@ -705,12 +722,12 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         return RB_OK;
     }
 
-    if (cudaError_t e = c->items.grow(sizeof(Item) * items.size())) return cleanup(fail(RB_ERR_CUDA, "items: %s", cudaGetErrorString(e)));
+    if (cudaError_t e = c->items.grow(sizeof(Item) * items.size(), c->stream)) return cleanup(fail(RB_ERR_CUDA, "items: %s", cudaGetErrorString(e)));
     if (refs)
-        if (cudaError_t e = c->refs.grow(sizeof(int32_t) * n)) return cleanup(fail(RB_ERR_CUDA, "refs: %s", cudaGetErrorString(e)));
+        if (cudaError_t e = c->refs.grow(sizeof(int32_t) * n, c->stream)) return cleanup(fail(RB_ERR_CUDA, "refs: %s", cudaGetErrorString(e)));
     // counters: [0] item counter (u32, padded), [1] out_count, [2] pairs, [3] survivors, [4..68) slot evals
     const size_t n_counters = 4 + RB_MAX_SLOTS;
-    if (cudaError_t e = c->counters.grow(sizeof(unsigned long long) * n_counters))
+    if (cudaError_t e = c->counters.grow(sizeof(unsigned long long) * n_counters, c->stream))
         return cleanup(fail(RB_ERR_CUDA, "counters: %s", cudaGetErrorString(e)));
 
     const int bps = P->jit.ok ? P->jit.blocks_per_sm : c->blocks_per_sm;
@@ -718,7 +735,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     int64_t stride = 0;
     if (P->lmax_edit >= 0) {
         stride = (P->lmax_edit + 2 + 31) & ~(int64_t)31;
-        if (cudaError_t e = c->scratch.grow(sizeof(int32_t) * stride * (size_t)grid * BLOCK))
+        if (cudaError_t e = c->scratch.grow(sizeof(int32_t) * stride * (size_t)grid * BLOCK, c->stream))
             return cleanup(fail(RB_ERR_OOM, "edit scratch (%lld B): %s",
                                 (long long)(sizeof(int32_t) * stride * (size_t)grid * BLOCK), cudaGetErrorString(e)));
     }
@@ -739,15 +756,15 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             c->pool_cap = 0;
         } else {
             res->d_t = res->d_s = res->d_r = nullptr;
-            cudaError_t e = cudaMalloc(&res->d_t, sizeof(int32_t) * cap);
-            if (!e) e = cudaMalloc(&res->d_s, sizeof(int32_t) * cap);
-            if (!e) e = cudaMalloc(&res->d_r, sizeof(int32_t) * cap);
+            cudaError_t e = dev_alloc((void**)&res->d_t, sizeof(int32_t) * cap, c->stream);
+            if (!e) e = dev_alloc((void**)&res->d_s, sizeof(int32_t) * cap, c->stream);
+            if (!e) e = dev_alloc((void**)&res->d_r, sizeof(int32_t) * cap, c->stream);
             if (e) return cleanup(fail(RB_ERR_OOM, "output buffer of %lld rows: %s", cap, cudaGetErrorString(e)));
         }
         res->cap = cap;
         cudaError_t e = cudaSuccess;
         if (want_parts) {
-            e = cudaMalloc(&res->d_p, sizeof(int32_t) * cap);
+            e = dev_alloc((void**)&res->d_p, sizeof(int32_t) * cap, c->stream);
             if (e) return cleanup(fail(RB_ERR_OOM, "part buffer of %lld rows: %s", cap, cudaGetErrorString(e)));
         }
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * n_counters, c->stream));
@@ -798,10 +815,10 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             for (int s = 0; s < RB_MAX_SLOTS; s++) res->stats.slot_evals[s] = (int64_t)host_ctr[4 + s];
             break;
         }
-        cudaFree(res->d_t);
-        cudaFree(res->d_s);
-        cudaFree(res->d_r);
-        if (res->d_p) cudaFree(res->d_p);
+        dev_free(res->d_t, c->stream);
+        dev_free(res->d_s, c->stream);
+        dev_free(res->d_r, c->stream);
+        dev_free(res->d_p, c->stream);
         res->d_t = res->d_s = res->d_r = res->d_p = nullptr;
         cap = rows;
     }
@@ -883,18 +900,17 @@ int rb_result_destroy(rb_result* r) {
     if (!r) return RB_OK;
     rb_ctx* c = r->ctx;
     if (c && r->d_t && r->cap > c->pool_cap) {  // keep the larger buffers for the next run
-        for (int k = 0; k < 3; k++)
-            if (c->pool[k]) cudaFree(c->pool[k]);
+        for (int k = 0; k < 3; k++) dev_free(c->pool[k], r->stream);
         c->pool[0] = r->d_t;
         c->pool[1] = r->d_s;
         c->pool[2] = r->d_r;
         c->pool_cap = r->cap;
         r->d_t = r->d_s = r->d_r = nullptr;
     }
-    if (r->d_t) cudaFree(r->d_t);
-    if (r->d_s) cudaFree(r->d_s);
-    if (r->d_r) cudaFree(r->d_r);
-    if (r->d_p) cudaFree(r->d_p);
+    dev_free(r->d_t, r->stream);
+    dev_free(r->d_s, r->stream);
+    dev_free(r->d_r, r->stream);
+    dev_free(r->d_p, r->stream);
     delete r;
     return RB_OK;
 }
