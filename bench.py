@@ -434,15 +434,23 @@ def main():
         achieved = bpp * pairs_step / (k_ms / 1e3) / 1e9
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "traffic.json")
+        pipe = None
         if os.path.exists(tfile):
             try:  # ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, same workload and size
                 entry = json.load(open(tfile)).get(w.name, {})
                 if entry.get("n") == w.n:
                     traffic = entry.get("bytes_per_launch")
+                    m = entry.get("metrics", {})
+                    pipe = {k: float(m[k]["value"]) for k in (
+                        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+                        "smsp__issue_active.avg.pct_of_peak_sustained_active") if k in m}
+                    pipe["source"] = entry.get("capture")
             except Exception:
                 traffic = None
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_kind": peak_kind,
+                "true_bound": "integer ALU pipe (inner tuples are reused from shared memory; see DESIGN.md 3.1)",
+                "ncu_pipes": pipe,
                 "model": "SURVEY 8d streaming bytes: sum_s E_s*b_s + 10 B per row; E_s from oracle first-touch counts",
                 "bytes_per_pair": bpp, "kernel_ms": k_ms, "terms": terms}
 
