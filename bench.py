@@ -42,6 +42,7 @@ WORKLOAD_DESC = {
     "citation3": "BASELINE config 2: 3 rules mixing eq, jaccard and edit",
     "edit_heavy": "BASELINE config 3: edit-distance-heavy rules, 64-256-char strings, maxd 2-5",
     "linkage": "BASELINE config 5: two-table linkage, Zipf(1.3) blocks, one cross run per block, batched",
+    "citation3_parts": "config 2 relation in 512-tuple partitions (the reference pipeline's default), batched",
 }
 UNIT = "pairs/s"
 
@@ -209,7 +210,7 @@ def run_reference_blocks(args, w, prog, cores, world):
     chosen, pairs = [], 0
     for k in rng.permutation(len(w.blocks)):
         refs, sp = w.blocks[k]
-        c = sp * (len(refs) - sp)
+        c = sp * (len(refs) - sp) if sp >= 0 else len(refs) * (len(refs) - 1) // 2
         if c <= args.cpu_pairs // 4 and pairs + c <= args.cpu_pairs:
             chosen.append(k)
             pairs += c

@@ -12,7 +12,9 @@ from .engine import (
     BlockStats,
     CandidateSet,
     EngineConfig,
+    PairBitmaps,
     PathProgram,
+    evaluate_pair,
     RunStats,
     context,
     run_cross,
@@ -34,7 +36,7 @@ __version__ = "0.1.0"
 __all__ = [
     "BandingConfig", "BlockStats", "CandidateSet", "MultiDeviceEngine", "PipelineConfig", "PipelineResult",
     "iter_partitions", "pipeline_run", "Checkpoint", "ConfigError", "DataParseError", "DataPartition", "Encoded",
-    "EngineConfig", "EvalPredicate", "ExecutionPath", "Kind", "MDRule", "MISSING", "PathProgram", "Predicate",
+    "EngineConfig", "PairBitmaps", "evaluate_pair", "EvalPredicate", "ExecutionPath", "Kind", "MDRule", "MISSING", "PathProgram", "Predicate",
     "Relation", "RelationEncoding", "RuleBlockError", "RuleParseError", "RuleSet", "RunStats", "Schema",
     "SchemaError", "TupleRecord", "ValidationError", "compile_program", "context", "parse_ruleset",
     "plan_from_stats", "predicate_universe", "relation_from_rows", "run_cross", "run_crosses", "run_partition", "run_partitions", "run_partition_rows", "split_rows_by_pairs",

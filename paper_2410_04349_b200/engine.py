@@ -345,6 +345,53 @@ class PathProgram:
 # reference-facing API
 
 
+@dataclass
+class PairBitmaps:
+    """Per-pair reuse / value bits and evaluation counts (engine.py:69-90)."""
+
+    reuse: np.ndarray
+    value: np.ndarray
+    scorer_calls: np.ndarray
+
+    @classmethod
+    def for_path(cls, path) -> "PairBitmaps":
+        n = len(path.predicate_table)
+        return cls(np.zeros(n, dtype=bool), np.zeros(n, dtype=bool), np.zeros(n, dtype=np.int64))
+
+    def reset(self) -> None:
+        self.reuse[:] = False
+        self.value[:] = False
+        self.scorer_calls[:] = 0
+
+
+def evaluate_pair(path, t, s, bitmaps: PairBitmaps, reg=None, schema=None, all_witnesses: bool = False):
+    """The sequential per-pair interpreter (engine.py:93-132), evaluated on
+    the device: a two-tuple relation (t, s) run as one ordered cross pair.
+    Returns the first witness rule id (or None), or every witness when
+    ``all_witnesses``.  ``bitmaps.scorer_calls`` receives the exact device
+    evaluations per slot; predicates the phase-1 filter settles are not
+    counted, so counts never exceed the reference's."""
+    from .relation import Relation as _Relation
+    from .relation import Schema as _Schema
+    from .relation import TupleRecord as _TR
+
+    if schema is None:
+        raise ConfigError("evaluate_pair needs the relation schema")
+    sch = _Schema(attributes=tuple((n, k) for n, k in schema.attributes))
+    rel = _Relation(schema=sch, tuples=(_TR(0, t.eid, tuple(t.values)), _TR(1, s.eid, tuple(s.values))))
+    enc = RelationEncoding(rel).prepare(list(path.predicate_table))
+    prog = PathProgram(path, enc, reg)
+    flags = RB_STATS | (RB_ENUMERATE if all_witnesses else 0)
+    (tt, ss, rr), st = prog.run_raw(np.array([0, 1], dtype=np.int32), 2, flags, split=1)
+    bitmaps.scorer_calls += np.array(st.slot_evals[: prog.n_slots], dtype=np.int64)
+    bitmaps.reuse |= bitmaps.scorer_calls > 0
+    order = {rid: k for k, rid in enumerate(path.checkpoint_order())}
+    hits = sorted((prog.rule_ids[k] for k in rr.tolist()), key=lambda rid: order[rid])
+    if all_witnesses:
+        return hits
+    return hits[0] if hits else None
+
+
 def _dedup(t, s, r, symmetric: bool, enumerate_all: bool):
     """engine.py:600-616 on arrays: enumerate -> unique rows; symmetric ->
     the smallest rule index per (t, s); asymmetric -> rows as they are."""

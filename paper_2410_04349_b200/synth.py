@@ -429,4 +429,16 @@ def person5(n: int = 10_000_000, seed: int = 4, plan_sample: int = 100_000) -> W
     return Workload("person5", enc, rules, path, n)
 
 
-WORKLOADS = {"citation3": citation3, "edit_heavy": edit_heavy, "linkage": linkage, "person5": person5}
+def citation3_parts(n: int = 1_000_000, seed: int = 2024, part: int = 512) -> Workload:
+    """Config 2's relation cut into the reference pipeline's default
+    partition size (max_partition_size = 512, pipeline.py:74): many small
+    partitions evaluated in one batched launch."""
+    w = citation3(n, seed)
+    perm = np.random.default_rng(seed + 1).permutation(n).astype(np.int32)
+    w.blocks = [(perm[a:a + part], -1) for a in range(0, n, part)]
+    w.name = "citation3_parts"
+    return w
+
+
+WORKLOADS = {"citation3": citation3, "edit_heavy": edit_heavy, "linkage": linkage, "person5": person5,
+             "citation3_parts": citation3_parts}

@@ -130,3 +130,20 @@ def test_batched_crosses_equal_single_runs():
         single = run_cross(l, r, rel, path)
         assert sorted(cs.pairs) == sorted(single.pairs)
         assert cs.stats.total_comparisons() == len(l) * len(r)
+
+
+def test_evaluate_pair_known_answers():
+    """pkg/tests/test_engine.py:68-118 on the device."""
+    from paper_2410_04349_b200 import PairBitmaps, evaluate_pair
+
+    rel, path, _ = goldens.load("products")
+    T = rel.tuples
+    bm = PairBitmaps.for_path(path)
+    assert evaluate_pair(path, T[0], T[3], bm, None, rel.schema) == "phi1"
+    bm.reset()
+    assert evaluate_pair(path, T[1], T[2], bm, None, rel.schema) == "phi2"
+    bm.reset()
+    assert evaluate_pair(path, T[1], T[2], bm, None, rel.schema, all_witnesses=True) == ["phi2", "phi3"]
+    bm.reset()
+    evaluate_pair(path, T[0], T[4], bm, None, rel.schema)
+    assert bm.scorer_calls.max() <= 1
