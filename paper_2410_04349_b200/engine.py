@@ -447,7 +447,10 @@ def _refs_array(partition) -> np.ndarray:
 
 
 def _candidates(prog: PathProgram, rows, st, cfg: EngineConfig, n_outer: int, wall: float) -> CandidateSet:
-    t, s, r = _dedup(*rows, cfg.symmetric_mode, cfg.enumerate_witnesses)
+    # One partition (or one cross run over disjoint sides) evaluates every
+    # pair once and reaches every checkpoint at most once per pair, so the
+    # rows are already what _dedup_witnesses (engine.py:600-616) returns.
+    t, s, r = (a.astype(np.int64) for a in rows)
     block = BlockStats(
         block_id=0,
         intervals_processed=max(1, -(-n_outer // cfg.n_t)),
@@ -550,7 +553,7 @@ def _batch(prog: PathProgram, blocks, cfg: EngineConfig):
             cmp = n * (n - 1) // 2
         else:
             cmp = n * (n - 1)
-        tt, ss, rr = _dedup(t[a:b], s[a:b], r[a:b], cfg.symmetric_mode, cfg.enumerate_witnesses)
+        tt, ss, rr = (x[a:b].astype(np.int64) for x in (t, s, r))  # unique per block by construction
         block = BlockStats(block_id=0, intervals_processed=1, comparisons=int(cmp), emitted=int(b - a),
                            slot_evals=np.zeros(prog.n_slots, dtype=np.int64))
         stats = RunStats(blocks=[block], wall_s=wall, n_intervals=1, kernel_ms=float(st.kernel_ms),

@@ -37,7 +37,6 @@ from .engine import (
     RunStats,
     _batch,
     _candidates,
-    _dedup,
     _encoding_for,
     _refs_array,
     split_rows_by_pairs,
@@ -228,11 +227,10 @@ class MultiDeviceEngine:
 
 def merge_shards(parts: list, cfg: EngineConfig) -> CandidateSet:
     """Union of the outer-row shards of one partition: disjoint pair sets,
-    so rows concatenate; statistics add up."""
+    so rows simply concatenate; statistics add up."""
     t = np.concatenate([p.arrays[0] for p in parts])
     s = np.concatenate([p.arrays[1] for p in parts])
     r = np.concatenate([p.arrays[2] for p in parts])
-    t, s, r = _dedup(t, s, r, cfg.symmetric_mode, cfg.enumerate_witnesses)
     blocks = [b for p in parts for b in p.stats.blocks]
     stats = RunStats(blocks=blocks, wall_s=max(p.stats.wall_s for p in parts),
                      n_intervals=sum(p.stats.n_intervals for p in parts),
