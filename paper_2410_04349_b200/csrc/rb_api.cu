@@ -612,6 +612,34 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                 fs.cap1 = fs.cap0;
                 continue;
             }
+            if (!t.tok) {
+                // edit: one interleaved int2 table {G, M2}[L] with
+                //   G  = min(maxgap[L], maxd[L])  (gap test and gap <= lev)
+                //   M2 = 2 * maxd[L]              (ceil((bag + gap) / 2) <= maxd)
+                // L = 0 always accepts; a guard entry {-1, -1} at L = -1 makes
+                // a pair with both strings missing fail.
+                const int32_t* maxgap = tables + t.src0;
+                const int32_t* maxd = tables + t.src1;
+                const int64_t lim = std::min(t.len0, t.len1);
+                const int64_t c = full ? lim : std::min(lim, std::max<int64_t>(1, per - 2));
+                if (stab.size() & 1) stab.push_back(0);  // 8-byte alignment
+                stab.push_back(-1);
+                stab.push_back(-1);
+                fs.off0 = (int32_t)stab.size();
+                fs.cap0 = (int32_t)c;
+                for (int64_t L = 0; L < c; L++) {
+                    if (L == 0) {
+                        stab.push_back(INF);
+                        stab.push_back(INF);
+                    } else {
+                        stab.push_back(std::min(maxgap[L], maxd[L]));
+                        stab.push_back(maxd[L] < 0 ? -1 : 2 * maxd[L]);
+                    }
+                }
+                fs.off1 = fs.off0;
+                fs.cap1 = fs.cap0;
+                continue;
+            }
             const int64_t c0 = full ? t.len0 : std::min(t.len0, per);
             const int64_t c1 = full ? t.len1 : std::min(t.len1, per);
             fs.off0 = (int32_t)stab.size();

@@ -412,14 +412,25 @@ static __device__ __noinline__ void drain_queue(const VerifyProg& V, const RunPa
 // ---------------------------------------------------------------------------
 // the pair kernel
 
+// One inner tuple's streamed features, stored record-wise so that the pair
+// loop reads every field of tuple jj at a constant offset from one running
+// shared-memory address (eq codes and token length share a 32-byte line).
+// 144-byte stride: the tile fill (thread k writes record k) hits 8 banks
+// instead of 1.
+struct __align__(16) Rec {
+    int32_t eq[MAX_EQ];
+    int32_t toklen[MAX_TOK];
+    uint4 toksig[MAX_TOK];
+    uint2 tokhash[MAX_TOK];
+    int32_t strlen_[MAX_STR];
+    int32_t tid;
+    int32_t pad0;
+    uint4 strbag[MAX_STR];
+    uint4 pad1;
+};
+
 struct __align__(16) Tile {
-    uint4 toksig[MAX_TOK][TJ];
-    uint4 strbag[MAX_STR][TJ];
-    uint2 tokhash[MAX_TOK][TJ];
-    int32_t eq[MAX_EQ][TJ];
-    int32_t toklen[MAX_TOK][TJ];
-    int32_t strlen_[MAX_STR][TJ];
-    int32_t tid[TJ];
+    Rec r[TJ];
 };
 
 // Shape of the filter program: compile-time constants in a specialised
@@ -486,11 +497,79 @@ static __device__ __forceinline__ int lds_s32(uint32_t addr) {
     asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
+static __device__ __forceinline__ int2 lds_s32x2(uint32_t addr) {
+    int2 v;
+    asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+// sum over the four bytes of |a_i - b_i|, plus c (VABSDIFF4 with accumulate)
+static __device__ __forceinline__ uint32_t vsad4_acc(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
 
 template <bool B>
 struct BoolC {
     static constexpr bool value = B;
 };
+
+// The set of rules still possible for a pair.  Integer masks (u32 / u64)
+// take runtime kill masks; RuleBits<N> is the specialised form for short
+// paths: one bool per rule, kill masks are compile-time constants, so every
+// test folds into a predicate AND (ISETP ... .AND) instead of a SEL / LOP3
+// on a mask register, and "any rule alive" is a short predicate OR.
+template <int NR>
+struct RuleBits {
+    bool b[NR];
+};
+
+template <typename M>
+__device__ __forceinline__ void m_init(M& m, uint64_t all) { m = (M)all; }
+template <typename M>
+__device__ __forceinline__ void m_kill(M& m, bool fail, uint64_t kill) {
+    if (fail) m &= ~(M)kill;
+}
+template <typename M>
+__device__ __forceinline__ bool m_any(const M& m) { return m != 0; }
+template <typename M>
+__device__ __forceinline__ bool m_hits(const M& m, uint64_t rules) { return (m & (M)rules) != 0; }
+template <typename M>
+__device__ __forceinline__ M m_gate(bool valid, const M& m) { return valid ? m : (M)0; }
+
+template <int NR>
+__device__ __forceinline__ void m_init(RuleBits<NR>& m, uint64_t all) {
+#pragma unroll
+    for (int k = 0; k < NR; k++) m.b[k] = ((all >> k) & 1ull) != 0;
+}
+template <int NR>
+__device__ __forceinline__ void m_kill(RuleBits<NR>& m, bool fail, uint64_t kill) {
+#pragma unroll
+    for (int k = 0; k < NR; k++)
+        if ((kill >> k) & 1ull) m.b[k] = m.b[k] & !fail;
+}
+template <int NR>
+__device__ __forceinline__ bool m_any(const RuleBits<NR>& m) {
+    bool a = false;
+#pragma unroll
+    for (int k = 0; k < NR; k++) a = a | m.b[k];
+    return a;
+}
+template <int NR>
+__device__ __forceinline__ bool m_hits(const RuleBits<NR>& m, uint64_t rules) {
+    bool a = false;
+#pragma unroll
+    for (int k = 0; k < NR; k++)
+        if ((rules >> k) & 1ull) a = a | m.b[k];
+    return a;
+}
+template <int NR>
+__device__ __forceinline__ RuleBits<NR> m_gate(bool valid, const RuleBits<NR>& m) {
+    RuleBits<NR> o;
+#pragma unroll
+    for (int k = 0; k < NR; k++) o.b[k] = valid & m.b[k];
+    return o;
+}
 
 // One outer tuple held in registers for a whole work item.
 template <typename Mask>
@@ -499,6 +578,7 @@ struct Outer {
     int32_t ti;
     bool ok;
     Mask alive0;  // rules still possible after the t-only tests
+    Mask alive_c; // rules still possible after the t-only constant tests alone
     int32_t jj_lo, jj_skip;
     int32_t ocode[MAX_EQ];
     int32_t olen[MAX_TOK], orem[MAX_TOK];
@@ -514,10 +594,12 @@ struct Outer {
         i = i_;
         ok = i < row_hi;
         ti = 0;
-        alive0 = 0;
+        m_init(alive0, 0);
+        m_init(alive_c, 0);
         if (ok) {
             ti = R.refs ? R.refs[i] : (int32_t)i;
-            alive0 = (Mask)RB_ALL_RULES;
+            m_init(alive0, RB_ALL_RULES);
+            m_init(alive_c, RB_ALL_RULES);
             if (mode == MODE_SYM) {
                 const int64_t lo = col0 > i + 1 ? col0 : i + 1;
                 my_pairs += (unsigned long long)(col1 > lo ? col1 - lo : 0);
@@ -535,12 +617,15 @@ struct Outer {
                 if (c >= 0)
                     ocode[f] = c;
                 else
-                    alive0 &= ~(Mask)RB_EQ_KILL(f);
+                    m_kill(alive0, true, RB_EQ_KILL(f));
             }
         }
 #pragma unroll
         for (int k = 0; k < MAX_CONST; k++)
-            if (k < RB_NCONST && ok && !__ldg(F.const_mask[k] + ti)) alive0 &= ~(Mask)RB_CONST_KILL(k);
+            if (k < RB_NCONST && ok && !__ldg(F.const_mask[k] + ti)) {
+                m_kill(alive0, true, RB_CONST_KILL(k));
+                m_kill(alive_c, true, RB_CONST_KILL(k));
+            }
 #pragma unroll
         for (int f = 0; f < MAX_TOK; f++) {
             olen[f] = -1;
@@ -555,8 +640,12 @@ struct Outer {
             if (f < RB_NTOK && ok) {
                 olen[f] = __ldg(F.tok_olen[f] + ti);
                 ohash[f] = __ldg(F.tok_ohash[f] + ti);
-                // jaccard and exact_token are false for a missing or empty t side
-                if (olen[f] <= 0) alive0 &= ~(Mask)RB_TOK_ROWKILL(f);
+                // jaccard and exact_token are false for a missing or empty t side.
+                // Such rows also fail the in-loop tests on their own (need[0][.]
+                // is INF; the hash below matches no empty / missing inner row),
+                // which the specialised loop relies on instead of alive0.
+                m_kill(alive0, olen[f] <= 0, RB_TOK_ROWKILL(f));
+                if (olen[f] <= 0) ohash[f].x = ~(uint32_t)mix64(0);
                 if (RB_TOK2D) {
                     const int nn = olen[f] > 0 ? olen[f] : 0;
 #pragma unroll
@@ -588,7 +677,8 @@ struct Outer {
             if (f < RB_NSTR && ok) {
                 oslen[f] = __ldg(F.str_olen[f] + ti);
                 obag[f] = __ldg(F.str_obag[f] + ti);
-                if (oslen[f] < 0) alive0 &= ~(Mask)RB_STR_ROWKILL(f);  // missing t side: edit is false
+                m_kill(alive0, oslen[f] < 0, RB_STR_ROWKILL(f));  // missing t side: edit is false
+                if (oslen[f] < 0) obag[f] = make_uint4(0, 0, 0, 0);  // with gap = |s| + 1 the gap test fails on its own
             }
         }
     }
@@ -619,27 +709,41 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                                           unsigned long long& my_surv) {
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << (threadIdx.x & 31)) - 1u;
+    const uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tab);
+#ifdef RB_SPEC
+    // The specialised loop starts every pair from the constant rule set (or
+    // the row's constant-test survivors): a row whose t side is missing or
+    // empty fails the per-pair tests by construction (see Outer::load), and
+    // any pair let through here is still decided by the exact interpreter.
+    Mask all_rules;
+    m_init(all_rules, RB_ALL_RULES);
+#endif
     for (int jj = 0; jj < tn; jj++) {
         Mask alive[ROWS];
 #pragma unroll
         for (int r = 0; r < ROWS; r++) {
-            alive[r] = (AllValid || (jj >= o[r].jj_lo && jj != o[r].jj_skip)) ? o[r].alive0 : (Mask)0;
+#ifdef RB_SPEC
+            const Mask& base = RB_NCONST == 0 ? all_rules : o[r].alive_c;
+#else
+            const Mask& base = o[r].alive0;
+#endif
+            alive[r] = AllValid ? base : m_gate(jj >= o[r].jj_lo && jj != o[r].jj_skip, base);
 #pragma unroll
             for (int f = 0; f < MAX_EQ; f++)
-                if (f < RB_NEQ && o[r].ocode[f] != T.eq[f][jj]) alive[r] &= ~(Mask)RB_EQ_KILL(f);
+                if (f < RB_NEQ) m_kill(alive[r], o[r].ocode[f] != T.r[jj].eq[f], RB_EQ_KILL(f));
         }
 
 #pragma unroll
         for (int f = 0; f < MAX_TOK; f++) {
             if (f >= RB_NTOK) continue;
-            Mask need = 0;
+            bool need = false;
 #pragma unroll
-            for (int r = 0; r < ROWS; r++) need |= alive[r];
-            if (!RB_TOK_ALWAYS(f) && !__any_sync(FULL, (need & (Mask)RB_TOK_RULES(f)) != 0)) continue;
-            const int m = T.toklen[f][jj];
+            for (int r = 0; r < ROWS; r++) need |= m_hits(alive[r], RB_TOK_RULES(f));
+            if (!RB_TOK_ALWAYS(f) && !__any_sync(FULL, need)) continue;
+            const int m = T.r[jj].toklen[f];
             const uint32_t m4 = (uint32_t)m << 2;  // byte offset of column m within a need[n][.] row
-            const uint4 is = T.toksig[f][jj];
-            const uint2 h = T.tokhash[f][jj];
+            const uint4 is = T.r[jj].toksig[f];
+            const uint2 h = T.r[jj].tokhash[f];
 #pragma unroll
             for (int r = 0; r < ROWS; r++) {
                 // u >= |A n B| (see the header); rows with n <= 0 were killed at load
@@ -670,7 +774,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                             // 32 of its bits suffice to drop all but ~2^-32 of the unequal pairs
                             ok = h.x == o[r].ohash[f].x;
                         }
-                        if (!ok) alive[r] &= ~(Mask)fs.kill;
+                        m_kill(alive[r], !ok, RB_TOK_KILL(f, z));
                     }
                 }
             }
@@ -678,29 +782,32 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
 #pragma unroll
         for (int f = 0; f < MAX_STR; f++) {
             if (f >= RB_NSTR) continue;
-            Mask need = 0;
+            bool need = false;
 #pragma unroll
-            for (int r = 0; r < ROWS; r++) need |= alive[r];
-            if (!RB_STR_ALWAYS(f) && !__any_sync(FULL, (need & (Mask)RB_STR_RULES(f)) != 0)) continue;
-            const int lb = T.strlen_[f][jj];
-            const uint4 ib = T.strbag[f][jj];
+            for (int r = 0; r < ROWS; r++) need |= m_hits(alive[r], RB_STR_RULES(f));
+            if (!RB_STR_ALWAYS(f) && !__any_sync(FULL, need)) continue;
+            const int lb = T.r[jj].strlen_[f];
+            const uint4 ib = T.r[jj].strbag[f];
 #pragma unroll
             for (int r = 0; r < ROWS; r++) {
                 const int la = o[r].oslen[f];
                 const int L = max(la, lb);
                 const int gap = abs(la - lb);
-                const int D = (int)(__vsadu4(o[r].obag[f].x, ib.x) + __vsadu4(o[r].obag[f].y, ib.y) +
-                                    __vsadu4(o[r].obag[f].z, ib.z) + __vsadu4(o[r].obag[f].w, ib.w));
-                const int lower = max(gap, (D + gap + 1) >> 1);
-                const bool present = lb >= 0;  // a missing t side was killed at load
+                // bag + gap in four accumulating byte-SAD steps
+                const int t = (int)vsad4_acc(o[r].obag[f].w, ib.w,
+                                             vsad4_acc(o[r].obag[f].z, ib.z,
+                                                       vsad4_acc(o[r].obag[f].y, ib.y,
+                                                                 vsad4_acc(o[r].obag[f].x, ib.x, (uint32_t)gap))));
 #pragma unroll
                 for (int z = 0; z < MAX_FSLOTS; z++) {
                     if (z < RB_STR_NS(f)) {
                         const FSlot& fs = F.str_slot[f][z];
-                        const int mg = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap0) ? tab[fs.off0 + L] : INT_MAX;
-                        const int md = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap1) ? tab[fs.off1 + L] : INT_MAX;
-                        const bool ok = present & ((L == 0) | ((gap <= mg) & (lower <= md)));
-                        if (!ok) alive[r] &= ~(Mask)RB_STR_KILL(f, z);
+                        // {G, M2}[L] (host: rb_program_create); lengths past a partial table are not filtered
+                        const int2 gm = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap0)
+                                            ? lds_s32x2(tab_s + 4u * (uint32_t)fs.off0 + 8u * (uint32_t)L)
+                                            : make_int2(INT_MAX, INT_MAX);
+                        const bool ok = (gap <= gm.x) & (t <= gm.y);
+                        m_kill(alive[r], !ok, RB_STR_KILL(f, z));
                     }
                 }
             }
@@ -709,13 +816,13 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
         // ---- survivors -> the warp's queue (ballot + popc compaction)
         bool any_surv = false;
 #pragma unroll
-        for (int r = 0; r < ROWS; r++) any_surv |= alive[r] != 0;
+        for (int r = 0; r < ROWS; r++) any_surv |= m_any(alive[r]);
         if (__any_sync(FULL, any_surv)) {
 #pragma unroll
             for (int r = 0; r < ROWS; r++) {
-                const bool surv = alive[r] != 0;
+                const bool surv = m_any(alive[r]);
                 const unsigned bal = __ballot_sync(FULL, surv);
-                if (surv) q[qn + __popc(bal & lt_mask)] = make_int2(o[r].ti, T.tid[jj]);
+                if (surv) q[qn + __popc(bal & lt_mask)] = make_int2(o[r].ti, T.r[jj].tid);
                 qn += __popc(bal);
                 my_surv += surv ? 1 : 0;
             }
@@ -772,24 +879,24 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
             for (int k = threadIdx.x; k < tn; k += BLOCK) {
                 const int64_t j = jt + k;
                 const int32_t sj = R.refs ? __ldg(R.refs + j) : (int32_t)j;
-                T.tid[k] = sj;
+                T.r[k].tid = sj;
 #pragma unroll
                 for (int f = 0; f < MAX_EQ; f++)
-                    if (f < RB_NEQ) T.eq[f][k] = __ldg(F.eq_inner[f] + sj);
+                    if (f < RB_NEQ) T.r[k].eq[f] = __ldg(F.eq_inner[f] + sj);
 #pragma unroll
                 for (int f = 0; f < MAX_TOK; f++)
                     if (f < RB_NTOK) {
-                        T.toklen[f][k] = __ldg(F.tok_ilen[f] + sj);
+                        T.r[k].toklen[f] = __ldg(F.tok_ilen[f] + sj);
                         uint4 sg = __ldg(F.tok_isig[f] + sj);
                         if (RB_TOK_SIG64(f)) sg = make_uint4(sg.x | sg.z, sg.y | sg.w, 0u, 0u);
-                        T.toksig[f][k] = sg;
-                        T.tokhash[f][k] = __ldg(F.tok_ihash[f] + sj);
+                        T.r[k].toksig[f] = sg;
+                        T.r[k].tokhash[f] = __ldg(F.tok_ihash[f] + sj);
                     }
 #pragma unroll
                 for (int f = 0; f < MAX_STR; f++)
                     if (f < RB_NSTR) {
-                        T.strlen_[f][k] = __ldg(F.str_ilen[f] + sj);
-                        T.strbag[f][k] = __ldg(F.str_ibag[f] + sj);
+                        T.r[k].strlen_[f] = __ldg(F.str_ilen[f] + sj);
+                        T.r[k].strbag[f] = __ldg(F.str_ibag[f] + sj);
                     }
             }
             __syncthreads();

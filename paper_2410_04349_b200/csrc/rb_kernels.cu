@@ -63,8 +63,12 @@ __global__ void char_features_kernel(const int64_t* __restrict__ offsets, const 
 #pragma unroll
         for (int z = 0; z < 4; z++)
             w[z] = cnt[4 * z] | (cnt[4 * z + 1] << 8) | (cnt[4 * z + 2] << 16) | (cnt[4 * z + 3] << 24);
-        len[r] = (missing && missing[r]) ? -1 : (int32_t)(b - a);
-        bag[r] = make_uint4(w[0], w[1], w[2], w[3]);
+        const bool miss = missing && missing[r];
+        len[r] = miss ? -1 : (int32_t)(b - a);
+        // a missing row gets a saturated bag: against any present string its
+        // length gap already exceeds the gap table (the pair filter needs no
+        // separate presence test)
+        bag[r] = miss ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
