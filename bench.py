@@ -107,6 +107,26 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def pinned_encoding(enc):
+    """A copy of an Encoded whose column arrays live in pinned (page-locked)
+    host memory, so the H2D copies of the e2e leg run at DMA speed."""
+    import torch
+    from paper_2410_04349_b200.encode import Column, Encoded
+
+    def pin(a):
+        if a is None:
+            return None
+        t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+        out = t.numpy().view(a.dtype).reshape(a.shape)
+        out[...] = a
+        return out
+
+    pe = Encoded(enc.n)
+    pe.columns = [Column(c.kind, pin(c.data), pin(c.offsets), pin(c.missing)) for c in enc.columns]
+    pe.index = dict(enc.index)
+    return pe
+
+
 def algorithmic_bytes_per_pair(enc, path, evals_frac, rows_per_pair):
     """A = sum_s E_s * b_s + C * 10 B, per pair.  E_s/pairs comes
     from the oracle's exact first-touch counts on the sample rows."""
@@ -378,8 +398,11 @@ def main():
     ms_step = t_total.item() / args.steps
     value = counts[0].item() / (t_total.item() / 1e3)
 
-    # ---- e2e: host buffers through the C ABI, copies inside the timed region
+    # ---- e2e: host buffers through the C ABI, copies inside the timed region.
+    # The step's inputs (the encoded columns) sit in pinned host memory, as a
+    # loader would leave them; pinning happens once, outside the timed region.
     e2e_steps = args.e2e_steps or max(1, min(args.steps, 3))
+    host_enc = pinned_encoding(w.enc)
     h2d = sum(c.data.nbytes + (0 if c.offsets is None else c.offsets.nbytes)
               + (0 if c.missing is None else c.missing.nbytes) for c in w.enc.columns)
     h2d += prog.program.tables.nbytes + prog.program.slots.nbytes + 4 * 4 * len(prog.program.ins_op)
@@ -388,9 +411,9 @@ def main():
     phase = {"upload": 0.0, "program": 0.0, "run": 0.0, "free": 0.0}
     for _ in range(e2e_steps):
         q0 = time.perf_counter()
-        drel = DeviceRelation(ctx, w.enc)  # H2D of every encoded column
+        drel = DeviceRelation(ctx, host_enc)  # H2D of every encoded column
         q1 = time.perf_counter()
-        p2 = PathProgram(w.path, w.enc, compiled=prog.program, drel=drel)  # H2D of the program
+        p2 = PathProgram(w.path, host_enc, compiled=prog.program, drel=drel)  # H2D of the program
         q2 = time.perf_counter()
         rows2, st2 = step(p2)  # evaluate + D2H of the rows
         q3 = time.perf_counter()
