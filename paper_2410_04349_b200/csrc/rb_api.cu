@@ -209,14 +209,17 @@ int rb_relation_create(rb_ctx* c, int64_t n, rb_rel** out) {
     return RB_OK;
 }
 
-static cudaError_t upload(rb_rel* r, const void* src, size_t bytes, void** dst) {
+// pad: zeroed bytes after the data (word-wise readers may touch them)
+static cudaError_t upload(rb_rel* r, const void* src, size_t bytes, void** dst, size_t pad = 0) {
     *dst = nullptr;
-    if (bytes == 0) bytes = 16;  // never hand out null for an empty array
-    cudaError_t e = dev_alloc(dst, bytes, r->ctx->stream);
+    const size_t alloc = std::max<size_t>(bytes + pad, 16);  // never hand out null for an empty array
+    cudaError_t e = dev_alloc(dst, alloc, r->ctx->stream);
     if (e != cudaSuccess) return e;
     r->allocs.push_back(*dst);
-    if (src) return cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, r->ctx->stream);
-    return cudaMemsetAsync(*dst, 0, bytes, r->ctx->stream);
+    if (!src || bytes == 0) return cudaMemsetAsync(*dst, 0, alloc, r->ctx->stream);
+    e = cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, r->ctx->stream);
+    if (e == cudaSuccess && alloc > bytes) e = cudaMemsetAsync((char*)*dst + bytes, 0, alloc - bytes, r->ctx->stream);
+    return e;
 }
 
 static int add_column(rb_rel* r, const DevColumn& dc, int64_t max_len, int32_t* col, double mean_len = 0) {
@@ -305,7 +308,7 @@ int rb_relation_add_chars(rb_rel* r, const int64_t* offsets, const void* chars, 
     dc.width = width;
     void *d_off, *d_chars, *d_miss = nullptr, *d_len, *d_bag;
     CK(upload(r, offsets, sizeof(int64_t) * (r->n + 1), &d_off));
-    CK(upload(r, chars, (size_t)width * nnz, &d_chars));
+    CK(upload(r, chars, (size_t)width * nnz, &d_chars, 16));  // the edit verifier reads u8 text four bytes at a time
     if (missing) CK(upload(r, missing, r->n, &d_miss));
     CK(upload(r, nullptr, sizeof(int32_t) * r->n, &d_len));
     CK(upload(r, nullptr, sizeof(uint4) * r->n, &d_bag));

@@ -39,6 +39,7 @@ typedef int int32_t;
 typedef unsigned int uint32_t;
 typedef long long int64_t;
 typedef unsigned long long uint64_t;
+typedef unsigned long long uintptr_t;
 #define INT_MIN (-2147483647 - 1)
 #define INT_MAX 2147483647
 #define INT64_MAX 9223372036854775807LL
@@ -204,11 +205,38 @@ static __device__ __forceinline__ uint32_t char_at(const DevColumn& c, int64_t k
     return c.width == 1 ? __ldg((const uint8_t*)c.data + k) : __ldg((const uint32_t*)c.data + k);
 }
 
-// Banded Levenshtein with cutoff k (Ukkonen): exact when the distance is
-// <= k, otherwise returns k+1.  Rows run over the shorter string.  For
-// k <= 31 the band lives in a 64-entry ring in thread-local memory (local
-// memory is lane-interleaved, so a warp's accesses coalesce and stay in L1);
-// wider bands use the thread's slice of the global scratch row.
+// Four bytes of a u8 column starting at any byte offset (two aligned loads).
+static __device__ __forceinline__ uint32_t load4_u8(const DevColumn& c, int64_t k) {
+    const uint8_t* p = (const uint8_t*)c.data + k;
+    const uint32_t* w = (const uint32_t*)((uintptr_t)p & ~(uintptr_t)3);
+    const uint32_t sh = (uint32_t)((uintptr_t)p & 3) * 8;
+    return __funnelshift_r(__ldg(w), __ldg(w + 1), sh);
+}
+
+// Length of the common run s[i..] == l[i+d..] starting at i (returns the
+// first mismatching i, capped by both ends).  u8 columns compare four
+// characters per step.
+static __device__ __forceinline__ int slide(const DevColumn& cs, int64_t s0, int n, const DevColumn& cl, int64_t l0,
+                                            int m, int i, int d) {
+    if (cs.width == 1 && cl.width == 1) {
+        while (i + 4 <= n && i + d + 4 <= m) {
+            const uint32_t x = load4_u8(cs, s0 + i) ^ load4_u8(cl, l0 + i + d);
+            if (x) return i + ((__ffs(x) - 1) >> 3);
+            i += 4;
+        }
+    }
+    while (i < n && i + d < m && char_at(cs, s0 + i) == char_at(cl, l0 + i + d)) i++;
+    return i;
+}
+
+// Bounded Levenshtein: exact when the distance is <= k, otherwise k+1.
+// For k <= 31 (every threshold the configs use) it is Landau-Vishkin /
+// Ukkonen's diagonal algorithm: for e = 0..k edits keep, per diagonal
+// d = j - i, the furthest row reachable with e edits, then slide along
+// matching characters.  Cost O(k^2 + slide length) instead of the band's
+// O(n k) cells; near-duplicate strings slide almost all the way at e = 0.
+// Wider bounds run a banded DP over the thread's slice of the global
+// scratch row.
 static __device__ int lev_bounded(const DevColumn& ca, int64_t a0, int la, const DevColumn& cb, int64_t b0, int lb, int k,
                            int32_t* row) {
     const DevColumn* cs = &ca;
@@ -227,32 +255,34 @@ static __device__ int lev_bounded(const DevColumn& ca, int64_t a0, int la, const
     if (m - n > k) return INF;
     if (n == 0) return m;
     if (k <= 31) {
-        int ring[64];  // ring[j & 63] = D[i-1][j] over the band of row i-1
-        for (int j = 0; j <= min(k, m); j++) ring[j] = j;
-        for (int i = 1; i <= n; i++) {
-            const uint32_t ai = char_at(*cs, s0 + i - 1);
-            const int jlo = max(0, i - k), jhi = min(m, i + k);
-            int diag = jlo >= 1 ? ring[(jlo - 1) & 63] : 0;
-            int left = INF, rmin = INF;
-            for (int j = jlo; j <= jhi; j++) {
-                const int up = j <= i - 1 + k ? ring[j & 63] : INF;  // D[i-1][j], INF outside its band
-                int v;
-                if (j == 0) {
-                    v = i;
-                } else {
-                    v = diag + (ai == char_at(*cl, l0 + j - 1) ? 0 : 1);
-                    v = min(v, up + 1);
-                    v = min(v, left + 1);
+        constexpr int OFF = 32, NEG = -(1 << 30);
+        int fr0[2 * OFF + 1], fr1[2 * OFF + 1];  // furthest row per diagonal, index OFF + d
+        int* prev = fr0;
+        int* cur = fr1;
+        const int dfin = m - n;
+        int i = slide(*cs, s0, n, *cl, l0, m, 0, 0);
+        if (dfin == 0 && i >= n) return 0;
+        prev[OFF] = i;
+        for (int e = 1; e <= k; e++) {
+            for (int d = -e; d <= e; d++) {
+                int best = NEG;
+                if (d >= -(e - 1) && d <= e - 1) best = prev[OFF + d] + 1;                      // substitution
+                if (d + 1 >= -(e - 1) && d + 1 <= e - 1) best = max(best, prev[OFF + d + 1] + 1);  // skip s[i]
+                if (d - 1 >= -(e - 1) && d - 1 <= e - 1) best = max(best, prev[OFF + d - 1]);      // skip l[j]
+                if (d > m || -d > n || best < 0) {
+                    cur[OFF + d] = NEG;
+                    continue;
                 }
-                v = min(v, INF);
-                diag = up;
-                ring[j & 63] = v;
-                left = v;
-                rmin = min(rmin, v);
+                i = min(best, min(n, m - d));
+                i = slide(*cs, s0, n, *cl, l0, m, i, d);
+                cur[OFF + d] = i;
+                if (d == dfin && i >= n) return e;
             }
-            if (rmin > k) return INF;
+            int* t = prev;
+            prev = cur;
+            cur = t;
         }
-        return ring[m & 63];
+        return INF;
     }
     for (int j = 0; j <= m; j++) row[j] = min(j, INF);
     for (int i = 1; i <= n; i++) {
@@ -704,7 +734,7 @@ struct Outer {
 // AllValid: every (outer, jj) pair of the warp is inside the pair space.
 template <typename Mask, int ROWS, bool AllValid>
 __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg& V, const RunParams& R, const Tile& T,
-                                          const int32_t* tab, Outer<Mask> (&o)[ROWS], int tn, int2* q, int& qn,
+                                          const int32_t* tab, Outer<Mask> (&o)[ROWS], int jj0, int tn, int2* q, int& qn,
                                           int part, const int* cp_rule, int32_t* scratch,
                                           unsigned long long& my_surv) {
     const unsigned FULL = 0xffffffffu;
@@ -718,7 +748,10 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
     Mask all_rules;
     m_init(all_rules, RB_ALL_RULES);
 #endif
-    for (int jj = 0; jj < tn; jj++) {
+#if defined(RB_SPEC) && SPEC_UNROLL > 1
+#pragma unroll SPEC_UNROLL
+#endif
+    for (int jj = jj0; jj < tn; jj++) {
         Mask alive[ROWS];
 #pragma unroll
         for (int r = 0; r < ROWS; r++) {
@@ -902,12 +935,20 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
             __syncthreads();
 
             bool all_valid = true;
+            int lo = TJ + 1;
 #pragma unroll
-            for (int r = 0; r < ROWS; r++) all_valid &= o[r].tile(item.mode, jt);
+            for (int r = 0; r < ROWS; r++) {
+                all_valid &= o[r].tile(item.mode, jt);
+                lo = min(lo, o[r].jj_lo);
+            }
+            // the warp's first inner position with a valid pair: the symmetric
+            // triangle's diagonal tiles (and small partitions) skip the dead part
+            const int jj0 = __reduce_min_sync(FULL, lo);
+            if (jj0 >= tn) continue;
             if (__all_sync(FULL, all_valid))
-                tile_loop<Mask, ROWS, true>(F, V, R, T, tab, o, tn, q, qn, part, cp_rule, scratch, my_surv);
+                tile_loop<Mask, ROWS, true>(F, V, R, T, tab, o, 0, tn, q, qn, part, cp_rule, scratch, my_surv);
             else
-                tile_loop<Mask, ROWS, false>(F, V, R, T, tab, o, tn, q, qn, part, cp_rule, scratch, my_surv);
+                tile_loop<Mask, ROWS, false>(F, V, R, T, tab, o, jj0, tn, q, qn, part, cp_rule, scratch, my_surv);
         }
         if (qn) {
             __syncwarp();

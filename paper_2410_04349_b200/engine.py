@@ -285,9 +285,11 @@ class PathProgram:
 
     # -- raw runs ---------------------------------------------------------
 
-    def run_batch(self, refs, offsets, splits, flags: int):
+    def run_batch(self, refs, offsets, splits, flags: int, out=None):
         """One launch over many partitions / cross blocks laid out back to
-        back (rb_run_batch).  Returns ((t, s, rule, part) int32 arrays, rb_stats)."""
+        back (rb_run_batch).  Returns ((t, s, rule, part) int32 arrays, rb_stats).
+        ``out``: optional (t, s, rule, part) int32 host arrays the rows are
+        copied into when they fit (see run_raw)."""
         L = lib()
         res = _lib.c_vp()
         refs_a = i32(refs)
@@ -299,7 +301,10 @@ class PathProgram:
             cnt = _lib.ctypes.c_int64(0)
             check(L.rb_result_count(res, _lib.ctypes.byref(cnt)))
             k = cnt.value
-            t, s, r, p = (np.empty(k, dtype=np.int32) for _ in range(4))
+            if out is not None and all(len(a) >= k and a.dtype == np.int32 and a.flags["C_CONTIGUOUS"] for a in out):
+                t, s, r, p = (a[:k] for a in out)
+            else:
+                t, s, r, p = (np.empty(k, dtype=np.int32) for _ in range(4))
             if k:
                 check(L.rb_result_copy(res, ptr(t), ptr(s), ptr(r)))
                 check(L.rb_result_copy_parts(res, ptr(p)))
@@ -309,8 +314,11 @@ class PathProgram:
             L.rb_result_destroy(res)
         return (t, s, r, p), st
 
-    def run_raw(self, refs, n: int, flags: int, *, split: int = -1, row_lo: int = 0, row_hi: Optional[int] = None):
-        """Evaluate on the device.  Returns ((t, s, rule) int32 arrays, rb_stats)."""
+    def run_raw(self, refs, n: int, flags: int, *, split: int = -1, row_lo: int = 0, row_hi: Optional[int] = None,
+                out=None):
+        """Evaluate on the device.  Returns ((t, s, rule) int32 arrays, rb_stats).
+        ``out``: optional (t, s, rule) int32 host arrays (e.g. pinned) the rows
+        are copied into when they fit; the returned arrays are then views."""
         L = lib()
         res = _lib.c_vp()
         refs_a = None if refs is None else i32(refs)
@@ -329,9 +337,12 @@ class PathProgram:
             cnt = _lib.ctypes.c_int64(0)
             check(L.rb_result_count(res, _lib.ctypes.byref(cnt)))
             k = cnt.value
-            t = np.empty(k, dtype=np.int32)
-            s = np.empty(k, dtype=np.int32)
-            r = np.empty(k, dtype=np.int32)
+            if out is not None and all(len(a) >= k and a.dtype == np.int32 and a.flags["C_CONTIGUOUS"] for a in out):
+                t, s, r = (a[:k] for a in out)
+            else:
+                t = np.empty(k, dtype=np.int32)
+                s = np.empty(k, dtype=np.int32)
+                r = np.empty(k, dtype=np.int32)
             if k:
                 check(L.rb_result_copy(res, ptr(t), ptr(s), ptr(r)))
             st = _lib.RbStats()
