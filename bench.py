@@ -107,6 +107,13 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def pinned_rows(k):
+    """Three reusable pinned int32 host arrays of k rows (t, s, rule)."""
+    import torch
+
+    return tuple(torch.empty(max(1, k), dtype=torch.int32, pin_memory=True).numpy() for _ in range(3))
+
+
 def pinned_encoding(enc):
     """A copy of an Encoded whose column arrays live in pinned (page-locked)
     host memory, so the H2D copies of the e2e leg run at DMA speed."""
@@ -359,13 +366,19 @@ def main():
         b_splits = np.array([sp for _, sp in w.blocks], dtype=np.int64)
 
         def step(p):
-            (t, s, r, _), st_ = p.run_batch(b_refs, b_offs, b_splits, RB_SYMMETRIC)
+            (t, s, r, _), st_ = p.run_batch(b_refs, b_offs, b_splits, RB_SYMMETRIC,
+                                            out=None if host_rows is None else host_rows + (host_part,))
             return (t, s, r), st_
     else:
         def step(p):
-            return p.run_raw(None, w.n, RB_SYMMETRIC)
+            return p.run_raw(None, w.n, RB_SYMMETRIC, out=host_rows)
 
-    for _ in range(args.warmup):
+    # result rows land in reusable pinned host buffers (sized by the first run)
+    host_rows = None
+    rows, st = step(prog)
+    host_rows = pinned_rows(len(rows[0]))
+    host_part = pinned_rows(len(rows[0]))[0]
+    for _ in range(args.warmup - 1):
         rows, st = step(prog)
     n_rows = len(rows[0])
     pairs_step = int(st.comparisons)
@@ -406,6 +419,12 @@ def main():
     h2d = sum(c.data.nbytes + (0 if c.offsets is None else c.offsets.nbytes)
               + (0 if c.missing is None else c.missing.nbytes) for c in w.enc.columns)
     h2d += prog.program.tables.nbytes + prog.program.slots.nbytes + 4 * 4 * len(prog.program.ins_op)
+    # one untimed pass first: the stream-ordered pool grows to the e2e working set once
+    drel = DeviceRelation(ctx, host_enc)
+    p2 = PathProgram(w.path, host_enc, compiled=prog.program, drel=drel)
+    step(p2)
+    p2.close()
+    drel.close()
     barrier()
     t0 = time.perf_counter()
     phase = {"upload": 0.0, "program": 0.0, "run": 0.0, "free": 0.0}

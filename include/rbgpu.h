@@ -156,6 +156,12 @@ int rb_result_count(const rb_result* res, int64_t* rows);
 int rb_result_copy(const rb_result* res, int32_t* t, int32_t* s, int32_t* rule);
 int rb_result_copy_parts(const rb_result* res, int32_t* part);
 int rb_result_stats(const rb_result* res, rb_stats* out);
+/* device pointers of the result rows (count rows each, on the result's
+ * device, ordered on its stream), valid until rb_result_destroy: the rows
+ * can be gathered across GPUs (NCCL) without a host round trip.  part is
+ * NULL unless the result is batched. */
+int rb_result_device(const rb_result* res, const int32_t** t, const int32_t** s, const int32_t** rule,
+                     const int32_t** part);
 int rb_result_destroy(rb_result* res);
 
 #ifdef __cplusplus

@@ -80,6 +80,7 @@ _SIGNATURES = {
     "rb_result_copy": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "rb_result_stats": (ctypes.c_int, [c_vp, ctypes.POINTER(RbStats)]),
     "rb_result_destroy": (ctypes.c_int, [c_vp]),
+    "rb_result_device": (ctypes.c_int, [c_vp, c_vpp, c_vpp, c_vpp, c_vpp]),
     # include/rbencode.h
     "rb_encode_eq_codes": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int64, c_vp]),
     "rb_encode_tokens": (ctypes.c_int64, [c_vp, c_vp, c_vp, ctypes.c_int64, c_vp, c_vp, c_i32p]),

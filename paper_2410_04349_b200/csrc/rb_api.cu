@@ -921,6 +921,16 @@ int rb_result_copy(const rb_result* r, int32_t* t, int32_t* s, int32_t* rule) {
     return RB_OK;
 }
 
+int rb_result_device(const rb_result* r, const int32_t** t, const int32_t** s, const int32_t** rule,
+                     const int32_t** part) {
+    if (!r || !t || !s || !rule) return fail(RB_ERR_INVALID, "rb_result_device: null argument");
+    *t = r->d_t;
+    *s = r->d_s;
+    *rule = r->d_r;
+    if (part) *part = r->d_p;
+    return RB_OK;
+}
+
 int rb_result_stats(const rb_result* r, rb_stats* out) {
     if (!r || !out) return fail(RB_ERR_INVALID, "rb_result_stats: null argument");
     *out = r->stats;
