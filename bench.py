@@ -365,12 +365,27 @@ def main():
         np.cumsum([len(r) for r, _ in w.blocks], out=b_offs[1:])
         b_splits = np.array([sp for _, sp in w.blocks], dtype=np.int64)
 
-        def step(p):
+        def step(p, host=True):
             (t, s, r, _), st_ = p.run_batch(b_refs, b_offs, b_splits, RB_SYMMETRIC,
                                             out=None if host_rows is None else host_rows + (host_part,))
             return (t, s, r), st_
+    elif world > 1 and backend == "nccl":
+        # N GPUs: each rank evaluates its partition, then the final collect is
+        # one NCCL all-gather of the row counts and of the rows themselves,
+        # straight from the device result buffers (distributed.gather_rows)
+        from paper_2410_04349_b200.distributed import gather_rows, run_rows_device
+
+        gathered = [0]
+
+        def step(p, host=False):
+            rows_d, st_ = run_rows_device(p, None, w.n, RB_SYMMETRIC, 0, w.n)
+            allrows = gather_rows(rows_d)
+            gathered[0] = int(allrows.shape[0])
+            if host:  # the e2e leg reads the collected rows back
+                allrows.cpu()
+            return (rows_d[:, 0], rows_d[:, 1], rows_d[:, 2]), st_
     else:
-        def step(p):
+        def step(p, host=True):
             return p.run_raw(None, w.n, RB_SYMMETRIC, out=host_rows)
 
     # result rows land in reusable pinned host buffers (sized by the first run)
@@ -434,7 +449,7 @@ def main():
         q1 = time.perf_counter()
         p2 = PathProgram(w.path, host_enc, compiled=prog.program, drel=drel)  # H2D of the program
         q2 = time.perf_counter()
-        rows2, st2 = step(p2)  # evaluate + D2H of the rows
+        rows2, st2 = step(p2, host=True)  # evaluate + D2H of the rows
         q3 = time.perf_counter()
         assert len(rows2[0]) == n_rows
         p2.close()
@@ -448,7 +463,8 @@ def main():
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = counts[0].item() / args.steps / e2e_s.item()
-    d2h = 12 * n_rows + 8 * 68
+    nccl_collect = world > 1 and backend == "nccl" and w.blocks is None
+    d2h = 12 * (gathered[0] if nccl_collect else n_rows) + 8 * 68
 
     # ---- CPU oracle sample (rank 0, N = 1): baseline + parity on the same rows
     cpu = None
@@ -508,7 +524,9 @@ def main():
                                       else "one symmetric partition per GPU"),
                        "pairs_per_step_per_gpu": pairs_step, "rows_per_step_per_gpu": n_rows,
                        "l2": "flushed (512 MiB write) between timed steps", "parallelism": f"partition-per-gpu x{world}",
-                       "collective": backend if world > 1 else None},
+                       "collective": (f"{backend}: all-gather of row counts and rows (final collect)"
+                                      if world > 1 and backend == "nccl" and w.blocks is None
+                                      else backend if world > 1 else None)},
             "blocking_wall_s": ms_step / 1e3,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "blocking_wall_s": e2e_s.item()},

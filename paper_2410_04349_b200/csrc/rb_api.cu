@@ -83,7 +83,7 @@ struct rb_ctx {
     bool own_stream = false;
     int sm_count = 0;
     int blocks_per_sm = 1;
-    DevBuf items, refs, counters, scratch;
+    DevBuf items, refs, counters, scratch, surv;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // output buffers of the last destroyed result, reused by the next run
     int32_t* pool[3] = {nullptr, nullptr, nullptr};
@@ -112,6 +112,7 @@ struct rb_prog {
     std::vector<void*> allocs;
     JitKernel jit;
     long long last_rows = 0;  // output size of the previous run: sizes the next buffer
+    long long last_surv = 0;  // survivors of the previous run: sizes the deferred-verification buffer
 };
 
 struct rb_result {
@@ -160,7 +161,7 @@ int rb_ctx_create(int device, rb_ctx** out) {
         cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
     }
     cudaGetLastError();
-    if (cudaMallocHost(&c->host_ctr, sizeof(unsigned long long) * (4 + RB_MAX_SLOTS)) != cudaSuccess) {
+    if (cudaMallocHost(&c->host_ctr, sizeof(unsigned long long) * (8 + RB_MAX_SLOTS)) != cudaSuccess) {
         cudaGetLastError();
         c->host_ctr = nullptr;
     }
@@ -185,6 +186,7 @@ int rb_ctx_destroy(rb_ctx* c) {
     c->refs.release(c->stream);
     c->counters.release(c->stream);
     c->scratch.release(c->stream);
+    c->surv.release(c->stream);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     for (int k = 0; k < 3; k++) dev_free(c->pool[k], c->stream);
@@ -586,7 +588,9 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
         int64_t total1d = TAB_BASE, total2d = TAB_BASE;
         for (auto& t : treq) {
             total1d += t.len0 + t.len1;
-            total2d += t.tok ? (t.nmax + 1) * (t.mmax + 2) : t.len0 + t.len1;
+            // 2-D: the jaccard slots of one token feature share one interleaved table
+            const int njp = t.tok ? (F.tok_njac[t.feat] <= 1 ? 1 : F.tok_njac[t.feat] <= 2 ? 2 : 4) : 0;
+            total2d += t.tok ? (t.z == 0 ? (t.nmax + 1) * (t.mmax + 2) * njp + 4 : 0) : t.len0 + t.len1 + 4;
         }
         F.tok2d = total2d <= SMEM_TAB ? 1 : 0;
         const bool full = F.tok2d || total1d <= SMEM_TAB;
@@ -595,11 +599,21 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
         for (auto& t : treq) {
             FSlot& fs = t.tok ? F.tok_slot[t.feat][t.z] : F.str_slot[t.feat][t.z];
             if (t.tok && F.tok2d) {
+                // need[n][m][z] for the feature's jaccard slots z, interleaved so
+                // one vector load per pair fetches every slot's threshold:
+                // entry (n, m, z) at tok_off[f] + ((n * w2) + m + 1) * njp + z
+                const int f = t.feat;
+                const int njp = F.tok_njac[f] <= 1 ? 1 : F.tok_njac[f] <= 2 ? 2 : 4;
+                const int64_t w2 = t.mmax + 2;
+                if (t.z == 0) {
+                    while (stab.size() % 4) stab.push_back(INF);  // 16-byte alignment of vector entries
+                    F.tok_off[f] = (int32_t)stab.size();
+                    F.tok_w2[f] = (int32_t)w2;
+                    F.tok_njp[f] = njp;
+                    stab.resize(stab.size() + (size_t)((t.nmax + 1) * w2 * njp), INF);
+                }
                 const int32_t* minsmall = tables + t.src0;
                 const int32_t* mink = tables + t.src1;
-                fs.w2 = (int32_t)(t.mmax + 2);
-                fs.off0 = (int32_t)stab.size();
-                fs.cap0 = (int32_t)((t.nmax + 1) * fs.w2);
                 for (int64_t nn = 0; nn <= t.nmax; nn++)
                     for (int64_t mm = -1; mm <= t.mmax; mm++) {
                         int32_t v = INF;
@@ -609,10 +623,11 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                             const int32_t mk = nn + mm < t.len1 ? mink[nn + mm] : INF;
                             if (small >= ms && mk <= small) v = mk;
                         }
-                        stab.push_back(v);
+                        stab[(size_t)(F.tok_off[f] + (nn * w2 + mm + 1) * njp + t.z)] = v;
                     }
-                fs.off1 = fs.off0;
-                fs.cap1 = fs.cap0;
+                fs.w2 = (int32_t)w2;
+                fs.off0 = fs.off1 = F.tok_off[f];
+                fs.cap0 = fs.cap1 = (int32_t)((t.nmax + 1) * w2 * njp);
                 continue;
             }
             if (!t.tok) {
@@ -722,31 +737,34 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     };
 
     // ---- work items: BLOCK * rows outer rows x CHUNK inner columns, per part
-    const int64_t rows_per_item = (int64_t)BLOCK * (P->jit.ok ? P->jit.rows : 1);
-    std::vector<Item> items;
-    for (size_t pi = 0; pi < parts.size(); pi++) {
-        const Part& pt = parts[pi];
-        const bool cross = pt.split >= 0;
-        const int32_t mode = cross ? MODE_CROSS : ((flags & RB_SYMMETRIC) ? MODE_SYM : MODE_ASYM);
-        const int64_t end = pt.base + pt.n;
-        const int64_t rlo = pt.base + std::max<int64_t>(0, row_lo);
-        const int64_t rhi = pt.base + std::min<int64_t>(row_hi, cross ? pt.split : pt.n);
-        for (int64_t r0 = rlo; r0 < rhi; r0 += rows_per_item) {
-            const int64_t rend = std::min<int64_t>(r0 + rows_per_item, rhi);
-            int64_t c0 = cross ? pt.base + pt.split : (mode == MODE_SYM ? r0 + 1 : pt.base);
-            for (; c0 < end; c0 += CHUNK) {
-                Item it{};
-                it.row0 = (int32_t)r0;
-                it.col0 = (int32_t)c0;
-                it.col1 = (int32_t)std::min<int64_t>(c0 + CHUNK, end);
-                it.row_hi = (int32_t)rend;
-                it.mode = mode;
-                it.part = (int32_t)pi;
-                items.push_back(it);
+    auto build_items = [&](int64_t rows_per_item) {
+        std::vector<Item> items;
+        for (size_t pi = 0; pi < parts.size(); pi++) {
+            const Part& pt = parts[pi];
+            const bool cross = pt.split >= 0;
+            const int32_t mode = cross ? MODE_CROSS : ((flags & RB_SYMMETRIC) ? MODE_SYM : MODE_ASYM);
+            const int64_t end = pt.base + pt.n;
+            const int64_t rlo = pt.base + std::max<int64_t>(0, row_lo);
+            const int64_t rhi = pt.base + std::min<int64_t>(row_hi, cross ? pt.split : pt.n);
+            for (int64_t r0 = rlo; r0 < rhi; r0 += rows_per_item) {
+                const int64_t rend = std::min<int64_t>(r0 + rows_per_item, rhi);
+                int64_t c0 = cross ? pt.base + pt.split : (mode == MODE_SYM ? r0 + 1 : pt.base);
+                for (; c0 < end; c0 += CHUNK) {
+                    Item it{};
+                    it.row0 = (int32_t)r0;
+                    it.col0 = (int32_t)c0;
+                    it.col1 = (int32_t)std::min<int64_t>(c0 + CHUNK, end);
+                    it.row_hi = (int32_t)rend;
+                    it.mode = mode;
+                    it.part = (int32_t)pi;
+                    items.push_back(it);
+                }
             }
         }
-    }
-    const int n_items = (int)items.size();
+        return items;
+    };
+    std::vector<Item> items = build_items((int64_t)BLOCK * (P->jit.ok ? P->jit.rows : 1));
+    int n_items = (int)items.size();
     const int64_t n = total;
     if (n_items == 0) {
         *out = res;
@@ -756,19 +774,34 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     if (cudaError_t e = c->items.grow(sizeof(Item) * items.size(), c->stream)) return cleanup(fail(RB_ERR_CUDA, "items: %s", cudaGetErrorString(e)));
     if (refs)
         if (cudaError_t e = c->refs.grow(sizeof(int32_t) * n, c->stream)) return cleanup(fail(RB_ERR_CUDA, "refs: %s", cudaGetErrorString(e)));
-    // counters: [0] item counter (u32, padded), [1] out_count, [2] pairs, [3] survivors, [4..68) slot evals
-    const size_t n_counters = 4 + RB_MAX_SLOTS;
+    // counters: [0] item counter (u32, padded), [1] out_count, [2] pairs, [3] survivors, [4..68) slot evals,
+    // [68] entries appended to the deferred survivor buffer
+    const size_t n_counters = 5 + RB_MAX_SLOTS;
+    const size_t SURV = 4 + RB_MAX_SLOTS;
+    // deferred verification: buffered survivors up to this many entries (16 B each); a
+    // run that needs more falls back to the generic kernel, which decides them in place
+    const long long SURV_LIMIT = 1ll << 28;
+    bool defer = P->jit.ok && P->jit.defer;
+    bool generic = !P->jit.ok;
+    // capacity: the program's last survivor count, or whatever the context's
+    // (pooled) buffer already holds, at least 16M entries (256 MB)
+    long long scap = defer ? std::min(SURV_LIMIT, std::max<long long>({1ll << 24, P->last_surv + P->last_surv / 4,
+                                                                      (long long)(c->surv.bytes / sizeof(int4))}))
+                           : 0;
     if (cudaError_t e = c->counters.grow(sizeof(unsigned long long) * n_counters, c->stream))
         return cleanup(fail(RB_ERR_CUDA, "counters: %s", cudaGetErrorString(e)));
 
     const int bps = P->jit.ok ? P->jit.blocks_per_sm : c->blocks_per_sm;
     const int grid = std::max(1, std::min(n_items, c->sm_count * bps));
+    const int gridg = c->sm_count * c->blocks_per_sm;  // generic kernel (fallback)
+    const int grid_v = c->sm_count * (P->jit.ok ? P->jit.verify_blocks_per_sm : 1);  // deferred verification
     int64_t stride = 0;
     if (P->lmax_edit >= 0) {
         stride = (P->lmax_edit + 2 + 31) & ~(int64_t)31;
-        if (cudaError_t e = c->scratch.grow(sizeof(int32_t) * stride * (size_t)grid * BLOCK, c->stream))
+        const size_t slices = (size_t)std::max(grid, std::max(gridg, grid_v)) * BLOCK;
+        if (cudaError_t e = c->scratch.grow(sizeof(int32_t) * stride * slices, c->stream))
             return cleanup(fail(RB_ERR_OOM, "edit scratch (%lld B): %s",
-                                (long long)(sizeof(int32_t) * stride * (size_t)grid * BLOCK), cudaGetErrorString(e)));
+                                (long long)(sizeof(int32_t) * stride * slices), cudaGetErrorString(e)));
     }
 
     CK(cudaMemcpyAsync(c->items.p, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice, c->stream));
@@ -818,10 +851,24 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         R.slot_evals = &ctr[4];
         R.scratch = (int32_t*)c->scratch.p;
         R.scratch_stride = stride;
+        if (defer) {
+            if (cudaError_t e2 = c->surv.grow(sizeof(int4) * (size_t)scap, c->stream))
+                return cleanup(fail(RB_ERR_OOM, "survivor buffer of %lld entries: %s", scap, cudaGetErrorString(e2)));
+            R.surv = (int4*)c->surv.p;
+            R.surv_cap = scap;
+            R.surv_count = &ctr[SURV];
+        }
 
         CK(cudaEventRecord(c->ev0, c->stream));
-        e = P->jit.ok ? launch_jit_kernel(P->jit, P->F, P->V, R, grid, c->stream)
-                      : launch_pair_kernel(P->F, P->V, R, grid, c->stream);
+        if (defer) {
+            e = launch_jit_kernel(P->jit, P->F, P->V, R, grid, c->stream);
+            // phase 2 right behind it, sized on the device from the survivor count
+            if (!e) e = launch_jit_verify(P->jit, P->V, R, grid_v, c->stream);
+        } else if (P->jit.ok && !generic) {
+            e = launch_jit_kernel(P->jit, P->F, P->V, R, grid, c->stream);
+        } else {
+            e = launch_pair_kernel(P->F, P->V, R, std::max(1, std::min(n_items, gridg)), c->stream);
+        }
         if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel launch: %s", cudaGetErrorString(e)));
         CK(cudaEventRecord(c->ev1, c->stream));
         unsigned long long stack_ctr[n_counters];
@@ -832,15 +879,47 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         float ms = 0;
         cudaEventElapsedTime(&ms, c->ev0, c->ev1);
         res->stats.kernel_ms += ms;
-        res->stats.launches += 1;
+        res->stats.launches += defer ? 2 : 1;
         const long long rows = (long long)host_ctr[1];
+        if (defer && (long long)host_ctr[SURV] > scap) {  // the survivor buffer was short: redo with room
+            if ((long long)host_ctr[SURV] <= SURV_LIMIT) {
+                scap = (long long)host_ctr[SURV];
+            } else {
+                // too many to buffer: decide them inside the generic pair kernel
+                // (one outer row per thread, so the items are rebuilt for it)
+                defer = false;
+                generic = true;
+                items = build_items(BLOCK);
+                n_items = (int)items.size();
+                if (cudaError_t e2 = c->items.grow(sizeof(Item) * items.size(), c->stream))
+                    return cleanup(fail(RB_ERR_CUDA, "items: %s", cudaGetErrorString(e2)));
+                CK(cudaMemcpyAsync(c->items.p, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice,
+                                   c->stream));
+            }
+            P->last_surv = (long long)host_ctr[SURV];
+            dev_free(res->d_p, c->stream);
+            res->d_p = nullptr;
+            if (c->pool[0] == nullptr) {  // keep the output buffers for the retry
+                c->pool[0] = res->d_t;
+                c->pool[1] = res->d_s;
+                c->pool[2] = res->d_r;
+                c->pool_cap = cap;
+            } else {
+                dev_free(res->d_t, c->stream);
+                dev_free(res->d_s, c->stream);
+                dev_free(res->d_r, c->stream);
+            }
+            res->d_t = res->d_s = res->d_r = nullptr;
+            continue;
+        }
         if (rows <= cap) {
+            if (defer) P->last_surv = (long long)host_ctr[SURV];
             res->count = rows;
             res->stats.comparisons = (int64_t)host_ctr[2];
             res->stats.survivors = (int64_t)host_ctr[3];
             res->stats.emitted = rows;
             res->stats.retries = attempt;
-            res->stats.specialized = P->jit.ok ? 1 : 0;
+            res->stats.specialized = generic ? 0 : 1;
             res->stats.jit_compile_ms = P->jit.compile_ms;
             P->last_rows = rows;
             for (int s = 0; s < RB_MAX_SLOTS; s++) res->stats.slot_evals[s] = (int64_t)host_ctr[4 + s];

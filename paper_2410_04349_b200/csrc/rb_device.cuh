@@ -138,6 +138,9 @@ struct FilterPlan {
     uint64_t tok_rules[MAX_TOK];
     uint64_t tok_kill[MAX_TOK];  // OR of the feature's slot kills: an outer row without tokens fails them all
     FSlot tok_slot[MAX_TOK][MAX_FSLOTS];
+    int32_t tok_off[MAX_TOK];  // 2-D mode: interleaved need[n][m][z] table (see rb_program_create)
+    int32_t tok_w2[MAX_TOK];
+    int32_t tok_njp[MAX_TOK];  // jaccard slots per entry, padded to 1, 2 or 4
     const int32_t* str_olen[MAX_STR];
     const uint4* str_obag[MAX_STR];
     const int32_t* str_ilen[MAX_STR];
@@ -186,6 +189,11 @@ struct RunParams {
     unsigned long long* slot_evals;
     int32_t* scratch;
     int64_t scratch_stride;
+    // deferred verification (specialised kernel): phase 1 appends its
+    // survivors {t, s, part} here; rb_verify_kernel_spec decides them
+    int4* surv;
+    long long surv_cap;
+    unsigned long long* surv_count;
 };
 
 // device-side helpers shared by kernels
@@ -393,49 +401,87 @@ static __device__ uint64_t interpret(const VerifyProg& V, int32_t ti, int32_t si
     return hit;
 }
 
-static __device__ __noinline__ void drain_queue(const VerifyProg& V, const RunParams& R, const int2* q, int qn, int part, const int* cp_rule,
-                            int32_t* scratch) {
+// Warp-collective: every lane decides one pair (valid lanes only) with the
+// exact interpreter and the warp appends the reached checkpoints' rows with
+// one atomicAdd.  engine.py:531-559 + CandidateSink.reserve (214-246).
+static __device__ __forceinline__ void verify_emit(const VerifyProg& V, const RunParams& R, bool valid, int32_t ti,
+                                                   int32_t si, int part, const int* cp_rule, int32_t* scratch) {
     const int lane = threadIdx.x & 31;
     const bool enumerate = (R.flags & RB_ENUMERATE) != 0;
     const bool sym = (R.flags & RB_SYMMETRIC) != 0;
+    uint64_t hit = 0;
+    if (valid) hit = interpret(V, ti, si, enumerate, scratch, (R.flags & RB_STATS) ? R.slot_evals : nullptr);
+    const int cnt = __popcll(hit);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return;
+    unsigned long long at = 0;
+    if (lane == 31) at = atomicAdd(R.out_count, (unsigned long long)total);
+    at = __shfl_sync(0xffffffffu, at, 31) + (unsigned long long)(incl - cnt);
+    int32_t a = ti, b = si;
+    if (sym && a > b) {
+        a = si;
+        b = ti;
+    }
+    while (hit) {
+        const int ord = __ffsll((long long)hit) - 1;
+        hit &= hit - 1;
+        if (at < (unsigned long long)R.cap) {
+            R.out_t[at] = a;
+            R.out_s[at] = b;
+            R.out_r[at] = cp_rule[ord];
+            if (R.out_p) R.out_p[at] = part;
+        }
+        at++;
+    }
+}
+
+static __device__ __noinline__ void drain_queue(const VerifyProg& V, const RunParams& R, const int2* q, int qn, int part, const int* cp_rule,
+                            int32_t* scratch) {
+    const int lane = threadIdx.x & 31;
     for (int base = 0; base < qn; base += 32) {
         const int k = base + lane;
-        uint64_t hit = 0;
-        int32_t ti = 0, si = 0;
-        if (k < qn) {
+        const int2 e = k < qn ? q[k] : make_int2(0, 0);
+        verify_emit(V, R, k < qn, e.x, e.y, part, cp_rule, scratch);
+    }
+}
+
+// Deferred form: the warp appends its queue to the global survivor buffer
+// (one atomicAdd, coalesced 16-byte stores).  Entries past the capacity are
+// counted but not stored; the host then re-runs with room for all of them.
+static __device__ __forceinline__ void flush_survivors(const RunParams& R, const int2* q, int qn, int part) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long at = 0;
+    if (lane == 0) at = atomicAdd(R.surv_count, (unsigned long long)qn);
+    at = __shfl_sync(0xffffffffu, at, 0);
+    for (int k = lane; k < qn; k += 32)
+        if (at + k < (unsigned long long)R.surv_cap) {
             const int2 e = q[k];
-            ti = e.x;
-            si = e.y;
-            hit = interpret(V, ti, si, enumerate, scratch, (R.flags & RB_STATS) ? R.slot_evals : nullptr);
+            R.surv[at + k] = make_int4(e.x, e.y, part, 0);
         }
-        const int cnt = __popcll(hit);
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        if (total == 0) continue;
-        unsigned long long at = 0;
-        if (lane == 31) at = atomicAdd(R.out_count, (unsigned long long)total);
-        at = __shfl_sync(0xffffffffu, at, 31) + (unsigned long long)(incl - cnt);
-        int32_t a = ti, b = si;
-        if (sym && a > b) {
-            a = si;
-            b = ti;
-        }
-        while (hit) {
-            const int ord = __ffsll((long long)hit) - 1;
-            hit &= hit - 1;
-            if (at < (unsigned long long)R.cap) {
-                R.out_t[at] = a;
-                R.out_s[at] = b;
-                R.out_r[at] = cp_rule[ord];
-                if (R.out_p) R.out_p[at] = part;
-            }
-            at++;
-        }
+}
+
+// Phase 2 as its own kernel: every thread decides one buffered survivor.
+// Runs at full occupancy with its own register budget, so the pair kernel
+// keeps no interpreter state.
+__device__ __forceinline__ void verify_body(const VerifyProg& V, const RunParams& R) {
+    __shared__ int cp_rule[RB_MAX_CHECKPOINTS];
+    for (int k = threadIdx.x; k < RB_MAX_CHECKPOINTS; k += blockDim.x) cp_rule[k] = V.cp_rule[k];
+    __syncthreads();
+    const unsigned long long cnt = *R.surv_count;
+    const long long n = (long long)(cnt < (unsigned long long)R.surv_cap ? cnt : (unsigned long long)R.surv_cap);
+    int32_t* scratch = R.scratch + (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) * R.scratch_stride;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    // whole warps iterate together (verify_emit is warp-collective)
+    for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
+        const long long k = base + (threadIdx.x & 31);
+        const int4 e = k < n ? R.surv[k] : make_int4(0, 0, 0, 0);
+        verify_emit(V, R, k < n, e.x, e.y, e.z, cp_rule, scratch);
     }
 }
 
@@ -474,6 +520,7 @@ struct __align__(16) Tile {
 #define RB_TOK_NJ(f) ((f) == 0 ? SPEC_TOK0_NJ : SPEC_TOK1_NJ)
 #define RB_TOK_ALWAYS(f) ((f) == 0 ? SPEC_TOK0_ALWAYS : SPEC_TOK1_ALWAYS)
 #define RB_TOK_SIG64(f) ((f) == 0 ? SPEC_TOK0_SIG64 : SPEC_TOK1_SIG64)
+#define RB_TOK_NJP(f) (RB_TOK_NJ(f) <= 1 ? 1 : RB_TOK_NJ(f) <= 2 ? 2 : 4)
 #define RB_STR_NS(f) ((f) == 0 ? SPEC_STR0_NS : SPEC_STR1_NS)
 #define RB_STR_ALWAYS(f) ((f) == 0 ? SPEC_STR0_ALWAYS : SPEC_STR1_ALWAYS)
 #define RB_FULLTAB SPEC_FULLTAB
@@ -502,6 +549,7 @@ struct __align__(16) Tile {
 #define RB_TOK_NJ(f) F.tok_njac[f]
 #define RB_TOK_ALWAYS(f) F.tok_always[f]
 #define RB_TOK_SIG64(f) F.tok_sig64[f]
+#define RB_TOK_NJP(f) F.tok_njp[f]
 #define RB_STR_NS(f) F.str_nslots[f]
 #define RB_STR_ALWAYS(f) F.str_always[f]
 #define RB_FULLTAB F.full_tab
@@ -525,6 +573,11 @@ constexpr int TAB_BASE = 2;
 static __device__ __forceinline__ int lds_s32(uint32_t addr) {
     int v;
     asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+static __device__ __forceinline__ int4 lds_s32x4(uint32_t addr) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
     return v;
 }
 static __device__ __forceinline__ int2 lds_s32x2(uint32_t addr) {
@@ -612,7 +665,7 @@ struct Outer {
     int32_t jj_lo, jj_skip;
     int32_t ocode[MAX_EQ];
     int32_t olen[MAX_TOK], orem[MAX_TOK];
-    uint32_t orow[MAX_TOK][MAX_FSLOTS];  // 2-D jaccard: shared-memory byte address of need[n][-1]
+    uint32_t orow[MAX_TOK];  // 2-D jaccard: shared-memory byte address of need[n][0][0]
     uint32_t lev[MAX_TOK][4];
     uint2 ohash[MAX_TOK];
     int32_t oslen[MAX_STR];
@@ -665,8 +718,9 @@ struct Outer {
             for (int w = 0; w < 4; w++) lev[f][w] = 0;
             // inactive rows still run the (discarded) lookups: point them at the guard entries
             const uint32_t guard = (uint32_t)__cvta_generic_to_shared(tab + TAB_BASE);
-#pragma unroll
-            for (int z = 0; z < MAX_FSLOTS; z++) orow[f][z] = guard;
+            orow[f] = guard;
+            if (RB_TOK2D && f < RB_NTOK)  // keep vector loads aligned: inactive rows read row n = 0
+                orow[f] = (uint32_t)__cvta_generic_to_shared(tab + F.tok_off[f] + RB_TOK_NJP(f));
             if (f < RB_NTOK && ok) {
                 olen[f] = __ldg(F.tok_olen[f] + ti);
                 ohash[f] = __ldg(F.tok_ohash[f] + ti);
@@ -678,11 +732,8 @@ struct Outer {
                 if (olen[f] <= 0) ohash[f].x = ~(uint32_t)mix64(0);
                 if (RB_TOK2D) {
                     const int nn = olen[f] > 0 ? olen[f] : 0;
-#pragma unroll
-                    for (int z = 0; z < MAX_FSLOTS; z++)
-                        if (z < RB_TOK_NJ(f))
-                            orow[f][z] = (uint32_t)__cvta_generic_to_shared(
-                                tab + F.tok_slot[f][z].off0 + nn * F.tok_slot[f][z].w2 + 1);
+                    orow[f] = (uint32_t)__cvta_generic_to_shared(
+                        tab + F.tok_off[f] + (nn * F.tok_w2[f] + 1) * RB_TOK_NJP(f));
                 }
                 const int64_t a = __ldg(F.tok_ooff[f] + ti), b = __ldg(F.tok_ooff[f] + ti + 1);
                 const uint32_t fold = RB_TOK_SIG64(f) ? 1u : 3u;  // 64-bit mode: bit b and b+64 coincide
@@ -732,7 +783,7 @@ struct Outer {
 
 // The per-pair filter over one shared tile for ROWS outer tuples per thread.
 // AllValid: every (outer, jj) pair of the warp is inside the pair space.
-template <typename Mask, int ROWS, bool AllValid>
+template <typename Mask, int ROWS, bool AllValid, bool DEFER>
 __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg& V, const RunParams& R, const Tile& T,
                                           const int32_t* tab, Outer<Mask> (&o)[ROWS], int jj0, int tn, int2* q, int& qn,
                                           int part, const int* cp_rule, int32_t* scratch,
@@ -774,7 +825,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
             for (int r = 0; r < ROWS; r++) need |= m_hits(alive[r], RB_TOK_RULES(f));
             if (!RB_TOK_ALWAYS(f) && !__any_sync(FULL, need)) continue;
             const int m = T.r[jj].toklen[f];
-            const uint32_t m4 = (uint32_t)m << 2;  // byte offset of column m within a need[n][.] row
+            const uint32_t mo = (uint32_t)(m * RB_TOK_NJP(f)) << 2;  // byte offset of column m within a need[n] row
             const uint4 is = T.r[jj].toksig[f];
             const uint2 h = T.r[jj].tokhash[f];
 #pragma unroll
@@ -785,6 +836,23 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                                   : __popc(o[r].lev[f][0] & is.x) + __popc(o[r].lev[f][1] & is.y) +
                                         __popc(o[r].lev[f][2] & is.z) + __popc(o[r].lev[f][3] & is.w) + o[r].orem[f];
                 const int n = o[r].olen[f];
+                int need2d[4] = {0, 0, 0, 0};
+                if (RB_TOK2D && RB_TOK_NJ(f) > 0) {  // one vector load: every jaccard slot's need[n][m]
+                    const uint32_t a = o[r].orow[f] + mo;
+                    if (RB_TOK_NJP(f) == 1) {
+                        need2d[0] = lds_s32(a);
+                    } else if (RB_TOK_NJP(f) == 2) {
+                        const int2 v = lds_s32x2(a);
+                        need2d[0] = v.x;
+                        need2d[1] = v.y;
+                    } else {
+                        const int4 v = lds_s32x4(a);
+                        need2d[0] = v.x;
+                        need2d[1] = v.y;
+                        need2d[2] = v.z;
+                        need2d[3] = v.w;
+                    }
+                }
 #pragma unroll
                 for (int z = 0; z < MAX_FSLOTS; z++) {
                     if (z < RB_TOK_NS(f)) {
@@ -793,7 +861,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                         if (z < RB_TOK_NJ(f)) {  // jaccard: exact integer tables
                             if (RB_TOK2D) {
                                 // need[n][m]: INF unless the length tests pass, else mink[n+m]
-                                ok = u >= lds_s32(o[r].orow[f][z] + m4);
+                                ok = u >= need2d[z];
                             } else {
                                 const bool live = m >= 0;
                                 const int small = min(n, m), big = max(n, m);
@@ -861,7 +929,10 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
             }
             if (qn > QCAP - 32 * ROWS) {
                 __syncwarp();
-                drain_queue(V, R, q, qn, part, cp_rule, scratch);
+                if (DEFER)
+                    flush_survivors(R, q, qn, part);
+                else
+                    drain_queue(V, R, q, qn, part, cp_rule, scratch);
                 __syncwarp();
                 qn = 0;
             }
@@ -871,11 +942,11 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
 
 // Mask = uint32_t when the path has <= 32 checkpoints, else uint64_t.
 // ROWS outer tuples per thread: a work item covers BLOCK * ROWS outer rows.
-template <typename Mask, int ROWS>
+template <typename Mask, int ROWS, bool DEFER = false>
 __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg& V, const RunParams& R) {
     __shared__ Tile T;
     __shared__ int2 queue[NWARPS][QCAP];
-    __shared__ int32_t tab[SMEM_TAB];
+    __shared__ __align__(16) int32_t tab[SMEM_TAB];
     __shared__ int cp_rule[MAX_RULES];
     __shared__ int s_item;
 
@@ -903,7 +974,10 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
         Outer<Mask> o[ROWS];
 #pragma unroll
         for (int r = 0; r < ROWS; r++)
-            o[r].load(F, R, tab, item.mode, (int64_t)item.row0 + r * BLOCK + threadIdx.x, (int64_t)item.row_hi, col0, col1,
+            // a warp owns 32 * ROWS consecutive outer rows, so its rows meet the
+            // symmetric diagonal together (tight jj0 skip, more all-valid tiles)
+            o[r].load(F, R, tab, item.mode, (int64_t)item.row0 + (warp * ROWS + r) * 32 + lane, (int64_t)item.row_hi,
+                      col0, col1,
                       my_pairs);
 
         for (int64_t jt = col0; jt < col1; jt += TJ) {
@@ -946,13 +1020,17 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
             const int jj0 = __reduce_min_sync(FULL, lo);
             if (jj0 >= tn) continue;
             if (__all_sync(FULL, all_valid))
-                tile_loop<Mask, ROWS, true>(F, V, R, T, tab, o, 0, tn, q, qn, part, cp_rule, scratch, my_surv);
+                tile_loop<Mask, ROWS, true, DEFER>(F, V, R, T, tab, o, 0, tn, q, qn, part, cp_rule, scratch, my_surv);
             else
-                tile_loop<Mask, ROWS, false>(F, V, R, T, tab, o, jj0, tn, q, qn, part, cp_rule, scratch, my_surv);
+                tile_loop<Mask, ROWS, false, DEFER>(F, V, R, T, tab, o, jj0, tn, q, qn, part, cp_rule, scratch,
+                                                    my_surv);
         }
         if (qn) {
             __syncwarp();
-            drain_queue(V, R, q, qn, part, cp_rule, scratch);
+            if (DEFER)
+                flush_survivors(R, q, qn, part);
+            else
+                drain_queue(V, R, q, qn, part, cp_rule, scratch);
             __syncwarp();
             qn = 0;
         }
@@ -976,6 +1054,11 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
 extern "C" __global__ void __launch_bounds__(rb::BLOCK, SPEC_MINBLOCKS)
     rb_pair_kernel_spec(const __grid_constant__ rb::FilterPlan F, const __grid_constant__ rb::VerifyProg V,
                         const __grid_constant__ rb::RunParams R) {
-    rb::pair_body<SPEC_MASK, SPEC_ROWS>(F, V, R);
+    rb::pair_body<SPEC_MASK, SPEC_ROWS, SPEC_DEFER != 0>(F, V, R);
+}
+
+extern "C" __global__ void __launch_bounds__(rb::BLOCK) rb_verify_kernel_spec(const __grid_constant__ rb::VerifyProg V,
+                                                                           const __grid_constant__ rb::RunParams R) {
+    rb::verify_body(V, R);
 }
 #endif

@@ -29,6 +29,9 @@ struct JitKernel {
     cudaKernel_t kernel = nullptr;
     int blocks_per_sm = 1;
     int rows = 1;  // outer rows per thread
+    bool defer = false;  // survivors go to a buffer decided by `verify` (see RunParams::surv)
+    cudaKernel_t verify = nullptr;
+    int verify_blocks_per_sm = 1;
     double compile_ms = 0;
     std::string key;
     std::string log;
@@ -36,5 +39,6 @@ struct JitKernel {
 JitKernel jit_pair_kernel(const FilterPlan& F, int device);
 cudaError_t launch_jit_kernel(const JitKernel& k, const FilterPlan& F, const VerifyProg& V, const RunParams& R,
                               int grid, cudaStream_t st);
+cudaError_t launch_jit_verify(const JitKernel& k, const VerifyProg& V, const RunParams& R, int grid, cudaStream_t st);
 
 }  // namespace rb

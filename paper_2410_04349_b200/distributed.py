@@ -32,7 +32,7 @@ class _DevRows:
     """__cuda_array_interface__ view of one int32 device array."""
 
     def __init__(self, ptr: int, n: int):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, True), "version": 3,
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, False), "version": 3,
                                          "strides": None}
 
 
@@ -73,8 +73,6 @@ def gather_rows(rows, group=None):
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    if world == 1:
-        return rows
     cnt = torch.tensor([rows.shape[0]], dtype=torch.int64, device=rows.device)
     counts = torch.empty(world, dtype=torch.int64, device=rows.device)
     dist.all_gather_into_tensor(counts, cnt, group=group)

@@ -89,3 +89,28 @@ def test_shards_gathered_equal_whole(name, symmetric):
         got = sorted((t, s, path.rule_ids[k]) for t, s, k in rows)
         assert got == want
     assert sum(c for _, _, c in out) == cmp
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["citation", "products"])
+def test_distributed_single_rank_nccl(name):
+    """The device path of run_partition_distributed on one GPU: rows from
+    rb_result_device, NCCL all-gathers (world size 1 on a 1-GPU box)."""
+    from paper_2410_04349_b200 import DataPartition, EngineConfig
+    from paper_2410_04349_b200.distributed import run_partition_distributed
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rel, path, cases = goldens.load(name)
+        for case in cases:
+            if case["left"] is not None or case["enumerate"]:
+                continue
+            refs = tuple(range(len(rel))) if case["refs"] is None else tuple(case["refs"])
+            cfg = EngineConfig(symmetric_mode=case["symmetric"])
+            cs = run_partition_distributed(DataPartition(0, refs), rel, path, cfg)
+            assert sorted(cs.pairs) == goldens.expected_rows(case)
+            assert cs.stats.total_comparisons() == case["comparisons"]
+    finally:
+        dist.destroy_process_group()

@@ -44,7 +44,7 @@ def main():
     os.unlink(fh.name)
     out = outs[0] if outs else "/tmp/spec.sass"
     open(out, "w").write(sass)
-    print(res.strip().splitlines()[-1] if res.strip() else "")
+    print("\n".join(l for l in res.strip().splitlines() if "REG" in l or "Function" in l))
     print("wrote", out, len(sass.splitlines()), "lines")
 
 
