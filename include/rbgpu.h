@@ -90,6 +90,8 @@ typedef struct rb_stats {
     int32_t specialized;   /* 1: the NVRTC-specialised kernel ran, 0: the generic one */
     int32_t reserved;
     double jit_compile_ms; /* one-off specialisation cost of this program's kernel */
+    double pair_ms;        /* device time of the pair (phase-1) kernel alone; kernel_ms adds
+                              the deferred verification kernel                          */
 } rb_stats;
 
 typedef struct rb_ctx rb_ctx;

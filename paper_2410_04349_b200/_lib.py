@@ -43,6 +43,7 @@ class RbStats(ctypes.Structure):
         ("specialized", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
         ("jit_compile_ms", ctypes.c_double),
+        ("pair_ms", ctypes.c_double),
     ]
 
 

@@ -84,7 +84,7 @@ struct rb_ctx {
     int sm_count = 0;
     int blocks_per_sm = 1;
     DevBuf items, refs, counters, scratch, surv;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr;
     // output buffers of the last destroyed result, reused by the next run
     int32_t* pool[3] = {nullptr, nullptr, nullptr};
     long long pool_cap = 0;
@@ -149,6 +149,7 @@ int rb_ctx_create(int device, rb_ctx** out) {
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev_mid);
     if (e != cudaSuccess) {
         delete c;
         return fail(RB_ERR_CUDA, "context setup: %s", cudaGetErrorString(e));
@@ -189,6 +190,7 @@ int rb_ctx_destroy(rb_ctx* c) {
     c->surv.release(c->stream);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->ev_mid) cudaEventDestroy(c->ev_mid);
     for (int k = 0; k < 3; k++) dev_free(c->pool[k], c->stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->host_ctr) cudaFreeHost(c->host_ctr);
@@ -862,6 +864,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         CK(cudaEventRecord(c->ev0, c->stream));
         if (defer) {
             e = launch_jit_kernel(P->jit, P->F, P->V, R, grid, c->stream);
+            if (!e) e = cudaEventRecord(c->ev_mid, c->stream);
             // phase 2 right behind it, sized on the device from the survivor count
             if (!e) e = launch_jit_verify(P->jit, P->V, R, grid_v, c->stream);
         } else if (P->jit.ok && !generic) {
@@ -879,6 +882,9 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         float ms = 0;
         cudaEventElapsedTime(&ms, c->ev0, c->ev1);
         res->stats.kernel_ms += ms;
+        float pms = ms;
+        if (defer) cudaEventElapsedTime(&pms, c->ev0, c->ev_mid);
+        res->stats.pair_ms += pms;
         res->stats.launches += defer ? 2 : 1;
         const long long rows = (long long)host_ctr[1];
         if (defer && (long long)host_ctr[SURV] > scap) {  // the survivor buffer was short: redo with room

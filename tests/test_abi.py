@@ -40,7 +40,7 @@ def test_struct_layouts_match_the_header():
 
     assert oracle.lib().orc_slot_size() == SLOT_DTYPE.itemsize == 48
     # rb_stats: 3 x i64, f64, 2 x i32, 64 x i64, 2 x i32, f64
-    assert ctypes.sizeof(_lib.RbStats) == 8 * 3 + 8 + 4 * 2 + 8 * 64 + 4 * 2 + 8
+    assert ctypes.sizeof(_lib.RbStats) == 8 * 3 + 8 + 4 * 2 + 8 * 64 + 4 * 2 + 8 + 8
 
 
 @pytest.mark.skipif(os.path.exists("/dev/nvidia0"), reason="checks the no-GPU failure path")

@@ -1,4 +1,5 @@
 set -x
-python bench.py --steps 3 --no-cpu > gpurun_out/cap/c3_bench.json 2> gpurun_out/cap/c3_bench.err
-bash profiles/capture.sh r1s3c citation3 1000000 2024
-bash profiles/capture.sh r1s3e edit_heavy 1000000 11
+timeout 1500 python -m pytest tests/ -q -m gpu -x 2>&1 | tail -25 > gpurun_out/gpu_tests.log; tail -2 gpurun_out/gpu_tests.log
+bash tools/gpu_perf.sh s4
+bash profiles/capture.sh r1s4c citation3 1000000 2024
+bash profiles/capture.sh r1s4e edit_heavy 1000000 11
