@@ -782,13 +782,18 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     const size_t SURV = 4 + RB_MAX_SLOTS;
     // deferred verification: buffered survivors up to this many entries (16 B each); a
     // run that needs more falls back to the generic kernel, which decides them in place
-    const long long SURV_LIMIT = 1ll << 28;
+    // RB_SURV_LIMIT / RB_SURV_MIN override both bounds (tests drive the retry and fallback paths with them)
+    const char* env_lim = std::getenv("RB_SURV_LIMIT");
+    const char* env_min = std::getenv("RB_SURV_MIN");
+    const long long SURV_LIMIT = env_lim ? std::max(1ll, std::atoll(env_lim)) : 1ll << 28;
+    const long long SURV_MIN = env_min ? std::max(1ll, std::atoll(env_min)) : 1ll << 24;
     bool defer = P->jit.ok && P->jit.defer;
     bool generic = !P->jit.ok;
     // capacity: the program's last survivor count, or whatever the context's
-    // (pooled) buffer already holds, at least 16M entries (256 MB)
-    long long scap = defer ? std::min(SURV_LIMIT, std::max<long long>({1ll << 24, P->last_surv + P->last_surv / 4,
-                                                                      (long long)(c->surv.bytes / sizeof(int4))}))
+    // (pooled) buffer already holds, at least SURV_MIN entries (256 MB)
+    long long scap = defer ? std::min(SURV_LIMIT, std::max<long long>({SURV_MIN, P->last_surv + P->last_surv / 4,
+                                                                      env_min ? 0ll
+                                                                              : (long long)(c->surv.bytes / sizeof(int4))}))
                            : 0;
     if (cudaError_t e = c->counters.grow(sizeof(unsigned long long) * n_counters, c->stream))
         return cleanup(fail(RB_ERR_CUDA, "counters: %s", cudaGetErrorString(e)));

@@ -1,0 +1,54 @@
+"""Deferred verification (phase-1 survivors buffered, decided by a second
+kernel): the survivor buffer overflowing must re-run with room for every
+survivor, and a run needing more than the buffer limit must fall back to
+the generic kernel, which decides survivors in place.  Both paths are forced
+with RB_SURV_MIN / RB_SURV_LIMIT and compared with the reference goldens."""
+
+import pytest
+
+import goldens
+from paper_2410_04349_b200 import DataPartition, EngineConfig, run_cross, run_partition
+
+CASES = ["citation", "products", "grouped", "edit_low", "skewed", "random_007", "random_031"]
+
+
+def _replay(name):
+    rel, path, cases = goldens.load(name)
+    out = []
+    for case in cases:
+        cfg = EngineConfig(symmetric_mode=case["symmetric"], enumerate_witnesses=case["enumerate"])
+        if case["left"] is not None:
+            cs = run_cross(DataPartition(0, tuple(case["left"])), DataPartition(1, tuple(case["right"])), rel, path,
+                           cfg)
+        else:
+            refs = tuple(range(len(rel))) if case["refs"] is None else tuple(case["refs"])
+            cs = run_partition(DataPartition(0, refs), rel, path, cfg)
+        assert sorted(cs.pairs) == goldens.expected_rows(case), (name, case["name"])
+        assert cs.stats.total_comparisons() == case["comparisons"]
+        out.append(cs)
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", [c for c in CASES if c in goldens.names()])
+def test_survivor_buffer_overflow_reruns(name, monkeypatch):
+    monkeypatch.delenv("RB_JIT", raising=False)
+    monkeypatch.setenv("RB_SURV_MIN", "7")
+    runs = _replay(name)
+    surv = [cs.stats.blocks[0].survivors for cs in runs]
+    assert any(s > 7 for s in surv)
+    for cs, s in zip(runs, surv):
+        if s > 7:  # the first attempt overflowed: pair + verify twice
+            assert cs.stats.launches == 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", [c for c in CASES if c in goldens.names()])
+def test_survivor_limit_falls_back_to_generic(name, monkeypatch):
+    monkeypatch.delenv("RB_JIT", raising=False)
+    monkeypatch.setenv("RB_SURV_MIN", "3")
+    monkeypatch.setenv("RB_SURV_LIMIT", "5")
+    runs = _replay(name)
+    for cs in runs:
+        if cs.stats.blocks[0].survivors > 5:
+            assert not cs.stats.specialized and cs.stats.launches == 3
