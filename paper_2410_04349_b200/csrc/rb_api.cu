@@ -462,9 +462,78 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
     // filter class of each slot, in evaluation order: 0 eq/const, 1+f token
     // feature f, 1+MAX_TOK+f string feature f; -1 not filtered
     std::vector<int> cls(n_slots, -1);
+
+    // ---- rule-level composite keys: the equality-type tests one rule needs
+    // (eq codes, exact_token) become one key column, tested with one compare
+    // (composite_key_kernel).  covered[s]: rules whose key contains slot s.
+    std::vector<uint64_t> covered(n_slots, 0);
+    {
+        const char* env_ck = std::getenv("RB_COMPOSITE");
+        const bool enable = !(env_ck && env_ck[0] == '0');
+        constexpr int MAXC = MAX_EQ + MAX_TOK * MAX_FSLOTS;
+        std::map<uint64_t, uint64_t> groups;  // component slots -> rules
+        for (size_t r = 0; r < need.size() && enable; r++) {
+            uint64_t m = 0;
+            int cnt = 0;
+            for (int s = 0; s < n_slots && cnt < MAXC; s++)
+                if (((need[r] >> s) & 1) && (slots[s].kind == RB_SLOT_EQ_CODE || slots[s].kind == RB_SLOT_EXACT)) {
+                    m |= 1ull << s;
+                    cnt++;
+                }
+            if (cnt >= 2) groups[m] |= 1ull << r;
+        }
+        for (auto& g : groups) {
+            if (F.n_eq >= MAX_EQ) break;
+            CompositeSpec so{}, si{};
+            bool same = true;
+            for (int s = 0; s < n_slots; s++) {
+                if (!((g.first >> s) & 1)) continue;
+                const rb_slot& sl = slots[s];
+                const DevColumn& L = rel->cols[sl.lhs];
+                const DevColumn& R = rel->cols[sl.rhs];
+                same &= sl.lhs == sl.rhs;
+                if (sl.kind == RB_SLOT_EQ_CODE) {
+                    so.codes[so.n] = L.codes;
+                    si.codes[si.n] = R.codes;
+                } else {
+                    so.len[so.n] = L.len;
+                    so.hash[so.n] = L.hash;
+                    si.len[si.n] = R.len;
+                    si.hash[si.n] = R.hash;
+                }
+                so.n++;
+                si.n++;
+            }
+            void* d_o = nullptr;
+            void* d_i = nullptr;
+            if ((e = dev_alloc(&d_o, sizeof(int32_t) * std::max<int64_t>(rel->n, 1), c->stream))) return bail(e);
+            P->allocs.push_back(d_o);
+            if ((e = launch_composite_key(rel->n, so, (int32_t*)d_o, c->stream))) return bail(e);
+            d_i = d_o;
+            if (!same) {
+                if ((e = dev_alloc(&d_i, sizeof(int32_t) * std::max<int64_t>(rel->n, 1), c->stream))) return bail(e);
+                P->allocs.push_back(d_i);
+                if ((e = launch_composite_key(rel->n, si, (int32_t*)d_i, c->stream))) return bail(e);
+            }
+            const int f = F.n_eq++;
+            F.eq_outer[f] = (const int32_t*)d_o;
+            F.eq_inner[f] = (const int32_t*)d_i;
+            F.eq_kill[f] = g.second;
+            for (int s = 0; s < n_slots; s++)
+                if ((g.first >> s) & 1) covered[s] |= g.second;
+        }
+    }
+
     for (int s = 0; s < n_slots; s++) {
         const rb_slot& sl = slots[s];
-        const uint64_t kill = kill_of(s);
+        uint64_t kill = kill_of(s);
+        if (sl.kind == RB_SLOT_EQ_CODE || sl.kind == RB_SLOT_EXACT) {
+            kill &= ~covered[s];  // those rules test it through their composite key
+            if (!kill) {
+                if (covered[s]) cls[s] = 0;
+                continue;
+            }
+        }
         const DevColumn& L = rel->cols[sl.lhs];
         const DevColumn& R = rel->cols[sl.rhs];
         const auto key = std::make_pair(sl.lhs, sl.rhs);
@@ -787,8 +856,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     const char* env_min = std::getenv("RB_SURV_MIN");
     const long long SURV_LIMIT = env_lim ? std::max(1ll, std::atoll(env_lim)) : 1ll << 28;
     const long long SURV_MIN = env_min ? std::max(1ll, std::atoll(env_min)) : 1ll << 24;
-    bool defer = P->jit.ok && P->jit.defer;
-    bool generic = !P->jit.ok;
+    const bool defer = P->jit.ok && P->jit.defer;
     // capacity: the program's last survivor count, or whatever the context's
     // (pooled) buffer already holds, at least SURV_MIN entries (256 MB)
     long long scap = defer ? std::min(SURV_LIMIT, std::max<long long>({SURV_MIN, P->last_surv + P->last_surv / 4,
@@ -817,6 +885,152 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     long long cap = std::max<long long>(1 << 20, P->last_rows + P->last_rows / 4);
     unsigned long long* ctr = (unsigned long long*)c->counters.p;
     res->ctx = c;
+    unsigned long long stack_ctr[n_counters];
+    unsigned long long* host_ctr = c->host_ctr ? c->host_ctr : stack_ctr;
+
+    if (defer) {
+        // ---- deferred verification, streamed over item ranges.  Each range:
+        // pair kernel -> (survivor count) -> verify kernel.  A range whose
+        // survivors overflow the buffer is rolled back and re-run with a
+        // larger buffer (up to SURV_LIMIT) or split in half, so any survivor
+        // volume streams through a bounded buffer; the output buffer grows
+        // (keeping its rows) before a verify that could overflow it.
+        if (c->pool[0] && c->pool_cap >= cap) {
+            res->d_t = c->pool[0];
+            res->d_s = c->pool[1];
+            res->d_r = c->pool[2];
+            cap = c->pool_cap;
+            c->pool[0] = c->pool[1] = c->pool[2] = nullptr;
+            c->pool_cap = 0;
+        } else {
+            cudaError_t e = dev_alloc((void**)&res->d_t, sizeof(int32_t) * cap, c->stream);
+            if (!e) e = dev_alloc((void**)&res->d_s, sizeof(int32_t) * cap, c->stream);
+            if (!e) e = dev_alloc((void**)&res->d_r, sizeof(int32_t) * cap, c->stream);
+            if (e) return cleanup(fail(RB_ERR_OOM, "output buffer of %lld rows: %s", cap, cudaGetErrorString(e)));
+        }
+        if (want_parts)
+            if (cudaError_t e = dev_alloc((void**)&res->d_p, sizeof(int32_t) * cap, c->stream))
+                return cleanup(fail(RB_ERR_OOM, "part buffer of %lld rows: %s", cap, cudaGetErrorString(e)));
+        res->cap = cap;
+        if (cudaError_t e = c->surv.grow(sizeof(int4) * (size_t)scap, c->stream))
+            return cleanup(fail(RB_ERR_OOM, "survivor buffer of %lld entries: %s", scap, cudaGetErrorString(e)));
+        std::vector<unsigned long long> base(n_counters, 0);  // counters after the last completed range
+        CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * n_counters, c->stream));
+        RunParams R{};
+        R.refs = refs ? (const int32_t*)c->refs.p : nullptr;
+        R.n = n;
+        R.flags = flags;
+        R.item_counter = (unsigned int*)&ctr[0];
+        R.out_count = &ctr[1];
+        R.stat_pairs = &ctr[2];
+        R.stat_surv = &ctr[3];
+        R.slot_evals = &ctr[4];
+        R.scratch = (int32_t*)c->scratch.p;
+        R.scratch_stride = stride;
+        R.surv_count = &ctr[SURV];
+        const long long per_row = (flags & RB_ENUMERATE) ? std::max(1, P->F.n_rules) : 1;
+        std::vector<std::pair<int, int>> ranges{{0, n_items}};
+        int retries = 0;
+        while (!ranges.empty()) {
+            const int lo = ranges.back().first, hi = ranges.back().second;
+            ranges.pop_back();
+            CK(cudaMemsetAsync(&ctr[0], 0, sizeof(unsigned long long), c->stream));
+            CK(cudaMemsetAsync(&ctr[SURV], 0, sizeof(unsigned long long), c->stream));
+            R.items = (const Item*)c->items.p + lo;
+            R.n_items = hi - lo;
+            R.surv = (int4*)c->surv.p;
+            R.surv_cap = scap;
+            R.out_t = res->d_t;
+            R.out_s = res->d_s;
+            R.out_r = res->d_r;
+            R.out_p = res->d_p;
+            R.cap = cap;
+            CK(cudaEventRecord(c->ev0, c->stream));
+            cudaError_t e = launch_jit_kernel(P->jit, P->F, P->V, R, std::max(1, std::min(hi - lo, grid)), c->stream);
+            if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel launch: %s", cudaGetErrorString(e)));
+            CK(cudaEventRecord(c->ev_mid, c->stream));
+            CK(cudaMemcpyAsync(host_ctr, ctr, sizeof(unsigned long long) * n_counters, cudaMemcpyDeviceToHost,
+                               c->stream));
+            if ((e = cudaStreamSynchronize(c->stream))) return cleanup(fail(RB_ERR_CUDA, "pair kernel: %s", cudaGetErrorString(e)));
+            float pms = 0;
+            cudaEventElapsedTime(&pms, c->ev0, c->ev_mid);
+            res->stats.pair_ms += pms;
+            res->stats.kernel_ms += pms;
+            res->stats.launches += 1;
+            const long long surv = (long long)host_ctr[SURV];
+            if (surv > scap) {  // roll this range back, then retry it with room or in halves
+                retries++;
+                CK(cudaMemcpyAsync(ctr, base.data(), sizeof(unsigned long long) * n_counters, cudaMemcpyHostToDevice,
+                                   c->stream));
+                if (surv <= SURV_LIMIT || hi - lo == 1) {
+                    scap = surv;
+                    if ((e = c->surv.grow(sizeof(int4) * (size_t)scap, c->stream)))
+                        return cleanup(fail(RB_ERR_OOM, "survivor buffer of %lld entries: %s", scap,
+                                            cudaGetErrorString(e)));
+                    ranges.push_back({lo, hi});
+                } else {
+                    const int mid = lo + (hi - lo) / 2;
+                    ranges.push_back({mid, hi});
+                    ranges.push_back({lo, mid});
+                }
+                continue;
+            }
+            const long long need_rows = (long long)host_ctr[1] + surv * per_row;
+            if (need_rows > cap) {  // grow the output, keeping the rows already written
+                const long long ncap = std::max(need_rows, cap + cap / 2);
+                const long long keep = (long long)host_ctr[1];
+                int32_t* nb[4] = {nullptr, nullptr, nullptr, nullptr};
+                int32_t* ob[4] = {res->d_t, res->d_s, res->d_r, res->d_p};
+                for (int k = 0; k < 4; k++) {
+                    if (!ob[k]) continue;
+                    if ((e = dev_alloc((void**)&nb[k], sizeof(int32_t) * ncap, c->stream)))
+                        return cleanup(fail(RB_ERR_OOM, "output buffer of %lld rows: %s", ncap, cudaGetErrorString(e)));
+                    if (keep) CK(cudaMemcpyAsync(nb[k], ob[k], sizeof(int32_t) * keep, cudaMemcpyDeviceToDevice, c->stream));
+                    dev_free(ob[k], c->stream);
+                }
+                res->d_t = nb[0];
+                res->d_s = nb[1];
+                res->d_r = nb[2];
+                res->d_p = nb[3];
+                cap = ncap;
+                res->cap = cap;
+                R.out_t = res->d_t;
+                R.out_s = res->d_s;
+                R.out_r = res->d_r;
+                R.out_p = res->d_p;
+                R.cap = cap;
+            }
+            CK(cudaEventRecord(c->ev0, c->stream));
+            if ((e = launch_jit_verify(P->jit, P->V, R, grid_v, c->stream)))
+                return cleanup(fail(RB_ERR_CUDA, "verify kernel launch: %s", cudaGetErrorString(e)));
+            CK(cudaEventRecord(c->ev1, c->stream));
+            CK(cudaMemcpyAsync(host_ctr, ctr, sizeof(unsigned long long) * n_counters, cudaMemcpyDeviceToHost,
+                               c->stream));
+            if ((e = cudaStreamSynchronize(c->stream))) return cleanup(fail(RB_ERR_CUDA, "verify kernel: %s", cudaGetErrorString(e)));
+            float vms = 0;
+            cudaEventElapsedTime(&vms, c->ev0, c->ev1);
+            res->stats.kernel_ms += vms;
+            res->stats.launches += 1;
+            std::copy(host_ctr, host_ctr + n_counters, base.begin());
+            P->last_surv = std::max(P->last_surv, surv);
+        }
+        const long long rows = (long long)base[1];
+        res->count = rows;
+        res->stats.comparisons = (int64_t)base[2];
+        res->stats.survivors = (int64_t)base[3];
+        res->stats.emitted = rows;
+        res->stats.retries = retries;
+        res->stats.specialized = 1;
+        res->stats.jit_compile_ms = P->jit.compile_ms;
+        P->last_rows = rows;
+        for (int s = 0; s < RB_MAX_SLOTS; s++) res->stats.slot_evals[s] = (int64_t)base[4 + s];
+        *out = res;
+        return RB_OK;
+    }
+
+    // ---- the generic kernel (no NVRTC specialisation): survivors are
+    // decided inside the pair kernel; an output overflow re-runs once with
+    // the exact size
     for (int attempt = 0;; attempt++) {
         if (c->pool[0] && c->pool_cap >= cap) {  // reuse the pooled buffers
             res->d_t = c->pool[0];
@@ -858,79 +1072,28 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         R.slot_evals = &ctr[4];
         R.scratch = (int32_t*)c->scratch.p;
         R.scratch_stride = stride;
-        if (defer) {
-            if (cudaError_t e2 = c->surv.grow(sizeof(int4) * (size_t)scap, c->stream))
-                return cleanup(fail(RB_ERR_OOM, "survivor buffer of %lld entries: %s", scap, cudaGetErrorString(e2)));
-            R.surv = (int4*)c->surv.p;
-            R.surv_cap = scap;
-            R.surv_count = &ctr[SURV];
-        }
 
         CK(cudaEventRecord(c->ev0, c->stream));
-        if (defer) {
-            e = launch_jit_kernel(P->jit, P->F, P->V, R, grid, c->stream);
-            if (!e) e = cudaEventRecord(c->ev_mid, c->stream);
-            // phase 2 right behind it, sized on the device from the survivor count
-            if (!e) e = launch_jit_verify(P->jit, P->V, R, grid_v, c->stream);
-        } else if (P->jit.ok && !generic) {
-            e = launch_jit_kernel(P->jit, P->F, P->V, R, grid, c->stream);
-        } else {
-            e = launch_pair_kernel(P->F, P->V, R, std::max(1, std::min(n_items, gridg)), c->stream);
-        }
+        e = P->jit.ok ? launch_jit_kernel(P->jit, P->F, P->V, R, grid, c->stream)
+                      : launch_pair_kernel(P->F, P->V, R, std::max(1, std::min(n_items, gridg)), c->stream);
         if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel launch: %s", cudaGetErrorString(e)));
         CK(cudaEventRecord(c->ev1, c->stream));
-        unsigned long long stack_ctr[n_counters];
-        unsigned long long* host_ctr = c->host_ctr ? c->host_ctr : stack_ctr;
         CK(cudaMemcpyAsync(host_ctr, ctr, sizeof(unsigned long long) * n_counters, cudaMemcpyDeviceToHost, c->stream));
         e = cudaStreamSynchronize(c->stream);
         if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel: %s", cudaGetErrorString(e)));
         float ms = 0;
         cudaEventElapsedTime(&ms, c->ev0, c->ev1);
         res->stats.kernel_ms += ms;
-        float pms = ms;
-        if (defer) cudaEventElapsedTime(&pms, c->ev0, c->ev_mid);
-        res->stats.pair_ms += pms;
-        res->stats.launches += defer ? 2 : 1;
+        res->stats.pair_ms += ms;
+        res->stats.launches += 1;
         const long long rows = (long long)host_ctr[1];
-        if (defer && (long long)host_ctr[SURV] > scap) {  // the survivor buffer was short: redo with room
-            if ((long long)host_ctr[SURV] <= SURV_LIMIT) {
-                scap = (long long)host_ctr[SURV];
-            } else {
-                // too many to buffer: decide them inside the generic pair kernel
-                // (one outer row per thread, so the items are rebuilt for it)
-                defer = false;
-                generic = true;
-                items = build_items(BLOCK);
-                n_items = (int)items.size();
-                if (cudaError_t e2 = c->items.grow(sizeof(Item) * items.size(), c->stream))
-                    return cleanup(fail(RB_ERR_CUDA, "items: %s", cudaGetErrorString(e2)));
-                CK(cudaMemcpyAsync(c->items.p, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice,
-                                   c->stream));
-            }
-            P->last_surv = (long long)host_ctr[SURV];
-            dev_free(res->d_p, c->stream);
-            res->d_p = nullptr;
-            if (c->pool[0] == nullptr) {  // keep the output buffers for the retry
-                c->pool[0] = res->d_t;
-                c->pool[1] = res->d_s;
-                c->pool[2] = res->d_r;
-                c->pool_cap = cap;
-            } else {
-                dev_free(res->d_t, c->stream);
-                dev_free(res->d_s, c->stream);
-                dev_free(res->d_r, c->stream);
-            }
-            res->d_t = res->d_s = res->d_r = nullptr;
-            continue;
-        }
         if (rows <= cap) {
-            if (defer) P->last_surv = (long long)host_ctr[SURV];
             res->count = rows;
             res->stats.comparisons = (int64_t)host_ctr[2];
             res->stats.survivors = (int64_t)host_ctr[3];
             res->stats.emitted = rows;
             res->stats.retries = attempt;
-            res->stats.specialized = generic ? 0 : 1;
+            res->stats.specialized = P->jit.ok ? 1 : 0;
             res->stats.jit_compile_ms = P->jit.compile_ms;
             P->last_rows = rows;
             for (int s = 0; s < RB_MAX_SLOTS; s++) res->stats.slot_evals[s] = (int64_t)host_ctr[4 + s];

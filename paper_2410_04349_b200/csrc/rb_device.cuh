@@ -540,6 +540,8 @@ struct __align__(16) Tile {
 #define RB_STR_RULES(f) RB_PICK2(f, SPEC_STR_RULES_)
 #define RB_TOK_KILL(f, z) ((f) == 0 ? RB_PICK4(z, SPEC_TOK0_KILL_) : RB_PICK4(z, SPEC_TOK1_KILL_))
 #define RB_STR_KILL(f, z) ((f) == 0 ? RB_PICK4(z, SPEC_STR0_KILL_) : RB_PICK4(z, SPEC_STR1_KILL_))
+// edit tables' shared-memory offsets as immediates: the lookup is one LEA + LDS [R + imm]
+#define RB_STR_OFF(f, z) ((f) == 0 ? RB_PICK4(z, SPEC_STR0_OFF_) : RB_PICK4(z, SPEC_STR1_OFF_))
 #else
 #define RB_NEQ F.n_eq
 #define RB_NCONST F.n_const
@@ -563,6 +565,7 @@ struct __align__(16) Tile {
 #define RB_STR_RULES(f) F.str_rules[f]
 #define RB_TOK_KILL(f, z) F.tok_slot[f][z].kill
 #define RB_STR_KILL(f, z) F.str_slot[f][z].kill
+#define RB_STR_OFF(f, z) F.str_slot[f][z].off0
 #endif
 
 // Shared tables start at TAB_BASE so that the (discarded) lookups of pairs
@@ -905,7 +908,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                         const FSlot& fs = F.str_slot[f][z];
                         // {G, M2}[L] (host: rb_program_create); lengths past a partial table are not filtered
                         const int2 gm = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap0)
-                                            ? lds_s32x2(tab_s + 4u * (uint32_t)fs.off0 + 8u * (uint32_t)L)
+                                            ? lds_s32x2(tab_s + 4u * (uint32_t)RB_STR_OFF(f, z) + 8u * (uint32_t)L)
                                             : make_int2(INT_MAX, INT_MAX);
                         const bool ok = (gap <= gm.x) & (t <= gm.y);
                         m_kill(alive[r], !ok, RB_STR_KILL(f, z));

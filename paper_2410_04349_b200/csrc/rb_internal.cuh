@@ -17,6 +17,14 @@ cudaError_t launch_token_features(const int64_t* offsets, const int32_t* ids, co
                                   int32_t* len, uint4* sig, uint2* hash, cudaStream_t st);
 cudaError_t launch_char_features(const int64_t* offsets, const void* chars, int32_t width, const uint8_t* missing,
                                  int64_t n, int32_t* len, uint4* bag, cudaStream_t st);
+// components of one composite key, read on one side (t or s) of the pair
+struct CompositeSpec {
+    int n;
+    const int32_t* codes[MAX_EQ + MAX_TOK * MAX_FSLOTS];  // eq code column, or null for a token list
+    const int32_t* len[MAX_EQ + MAX_TOK * MAX_FSLOTS];    // token list length (-1 missing)
+    const uint2* hash[MAX_EQ + MAX_TOK * MAX_FSLOTS];     // token list hash
+};
+cudaError_t launch_composite_key(int64_t n, const CompositeSpec& spec, int32_t* out, cudaStream_t st);
 cudaError_t launch_pair_kernel(const FilterPlan& F, const VerifyProg& V, const RunParams& R, int grid,
                                cudaStream_t st);
 int pair_kernel_blocks_per_sm();

@@ -88,6 +88,39 @@ cudaError_t launch_char_features(const int64_t* offsets, const void* chars, int3
     return cudaGetLastError();
 }
 
+// Rule-level composite keys: one 31-bit hash per tuple over the equality
+// codes and token-list hashes of every equality-type test (eq code,
+// exact_token) one rule requires, so the pair filter tests the whole
+// conjunction with one compare.  Equal components give equal keys; unequal
+// ones collide with probability 2^-31 and are caught by the exact pass.  A
+// missing code or a missing / empty token list (the test is false) gives -1.
+__global__ void composite_key_kernel(int64_t n, CompositeSpec spec, int32_t* __restrict__ out) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t h = 0x243F6A8885A308D3ull;
+        bool ok = true;
+        for (int k = 0; k < spec.n; k++) {
+            uint32_t v;
+            if (spec.codes[k]) {
+                const int32_t c = spec.codes[k][r];
+                ok &= c >= 0;
+                v = (uint32_t)c;
+            } else {
+                ok &= spec.len[k][r] > 0;
+                v = spec.hash[k][r].x;
+            }
+            h = mix64(h ^ ((uint64_t)k << 40) ^ v);
+        }
+        out[r] = ok ? (int32_t)(h & 0x7fffffffu) : -1;
+    }
+}
+
+cudaError_t launch_composite_key(int64_t n, const CompositeSpec& spec, int32_t* out, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    int grid = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+    composite_key_kernel<<<grid, 256, 0, st>>>(n, spec, out);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // the generic pair kernel (shape read from the kernel parameters)
 
