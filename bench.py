@@ -114,19 +114,23 @@ def pinned_rows(k):
     return tuple(torch.empty(max(1, k), dtype=torch.int32, pin_memory=True).numpy() for _ in range(3))
 
 
+def pin_array(a):
+    """A pinned (page-locked) host copy of a numpy array."""
+    import torch
+
+    t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+    out = t.numpy().view(a.dtype).reshape(a.shape)
+    out[...] = a
+    return out
+
+
 def pinned_encoding(enc):
     """A copy of an Encoded whose column arrays live in pinned (page-locked)
     host memory, so the H2D copies of the e2e leg run at DMA speed."""
-    import torch
     from paper_2410_04349_b200.encode import Column, Encoded
 
     def pin(a):
-        if a is None:
-            return None
-        t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
-        out = t.numpy().view(a.dtype).reshape(a.shape)
-        out[...] = a
-        return out
+        return None if a is None else pin_array(a)
 
     pe = Encoded(enc.n)
     pe.columns = [Column(c.kind, pin(c.data), pin(c.offsets), pin(c.missing)) for c in enc.columns]
@@ -360,7 +364,7 @@ def main():
         torch.cuda.synchronize()
 
     if w.blocks is not None:  # many cross blocks / partitions: one batched launch per step
-        b_refs = np.concatenate([r for r, _ in w.blocks]).astype(np.int32)
+        b_refs = pin_array(np.concatenate([r for r, _ in w.blocks]).astype(np.int32))  # the batch's input refs
         b_offs = np.zeros(len(w.blocks) + 1, dtype=np.int64)
         np.cumsum([len(r) for r, _ in w.blocks], out=b_offs[1:])
         b_splits = np.array([sp for _, sp in w.blocks], dtype=np.int64)
