@@ -113,6 +113,7 @@ struct rb_prog {
     JitKernel jit;
     long long last_rows = 0;  // output size of the previous run: sizes the next buffer
     long long last_surv = 0;  // survivors of the previous run: sizes the deferred-verification buffer
+    double surv_rate = -1.0;  // survivors per work item in the previous run (-1: none yet)
 };
 
 struct rb_result {
@@ -785,12 +786,17 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     if (!c || !rel || !P || !out) return fail(RB_ERR_INVALID, "run: null argument");
     if (P->rel != rel || rel->ctx != c) return fail(RB_ERR_INVALID, "run: program/relation/context mismatch");
     if (total < 0 || total > INT32_MAX) return fail(RB_ERR_INVALID, "run: partition size out of range");
-    if (refs) {
+    // tuple refs are range-checked on the device (refs_check_kernel, ahead of
+    // the pair kernel, which then does nothing); the host scans only to name
+    // the bad position (bad_refs below)
+    auto bad_refs = [&]() {
         for (int64_t k = 0; k < total; k++)
             if (refs[k] < 0 || refs[k] >= rel->n)
-                return fail(RB_ERR_INVALID, "tuple ref %d at position %lld outside the relation",
-                            refs[k], (long long)k);
-    } else if (total > rel->n) {
+                return fail(RB_ERR_INVALID, "tuple ref %d at position %lld outside the relation", refs[k],
+                            (long long)k);
+        return fail(RB_ERR_INVALID, "tuple ref outside the relation");
+    };
+    if (!refs && total > rel->n) {
         return fail(RB_ERR_INVALID, "identity partition of %lld tuples exceeds the relation", (long long)total);
     }
     *out = nullptr;
@@ -847,8 +853,9 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         if (cudaError_t e = c->refs.grow(sizeof(int32_t) * n, c->stream)) return cleanup(fail(RB_ERR_CUDA, "refs: %s", cudaGetErrorString(e)));
     // counters: [0] item counter (u32, padded), [1] out_count, [2] pairs, [3] survivors, [4..68) slot evals,
     // [68] entries appended to the deferred survivor buffer
-    const size_t n_counters = 5 + RB_MAX_SLOTS;
+    const size_t n_counters = 6 + RB_MAX_SLOTS;
     const size_t SURV = 4 + RB_MAX_SLOTS;
+    const size_t BAD = 5 + RB_MAX_SLOTS;  // set by refs_check_kernel
     // deferred verification: buffered survivors up to this many entries (16 B each); a
     // run that needs more falls back to the generic kernel, which decides them in place
     // RB_SURV_LIMIT / RB_SURV_MIN override both bounds (tests drive the retry and fallback paths with them)
@@ -916,7 +923,9 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             return cleanup(fail(RB_ERR_OOM, "survivor buffer of %lld entries: %s", scap, cudaGetErrorString(e)));
         std::vector<unsigned long long> base(n_counters, 0);  // counters after the last completed range
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * n_counters, c->stream));
+        if (refs) CK(launch_refs_check((const int32_t*)c->refs.p, n, rel->n, &ctr[BAD], c->stream));
         RunParams R{};
+        R.bad_refs = refs ? &ctr[BAD] : nullptr;
         R.refs = refs ? (const int32_t*)c->refs.p : nullptr;
         R.n = n;
         R.flags = flags;
@@ -929,9 +938,35 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         R.scratch_stride = stride;
         R.surv_count = &ctr[SURV];
         const long long per_row = (flags & RB_ENUMERATE) ? std::max(1, P->F.n_rules) : 1;
-        std::vector<std::pair<int, int>> ranges{{0, n_items}};
-        int retries = 0;
-        while (!ranges.empty()) {
+        // Ranges are sized from the survivors per item seen so far (the
+        // program's previous run, else a probe of 1/64 of the items), so a
+        // range rarely overflows the buffer; one that does is rolled back and
+        // re-run larger or in halves (the `ranges` stack).
+        std::vector<std::pair<int, int>> ranges;
+        int retries = 0, next = 0;
+        long long done_items = 0, done_surv = 0;
+        for (;;) {
+            if (ranges.empty()) {
+                if (next >= n_items) break;
+                const double rate = done_items ? (double)done_surv / (double)done_items : P->surv_rate;
+                long long size;
+                if (rate < 0) {
+                    size = std::max<long long>(grid, n_items / 64);  // probe
+                } else {
+                    const double budget = 0.8 * (double)SURV_LIMIT;
+                    size = rate > 0 ? (long long)(budget / rate) : (long long)n_items;
+                    const long long want = (long long)(rate * (double)std::min<long long>(size, n_items - next) * 1.25) + 4096;
+                    if (want > scap) {  // grow ahead of the launch instead of after an overflow
+                        scap = std::min(SURV_LIMIT, want);
+                        if (cudaError_t e = c->surv.grow(sizeof(int4) * (size_t)scap, c->stream))
+                            return cleanup(fail(RB_ERR_OOM, "survivor buffer of %lld entries: %s", scap,
+                                                cudaGetErrorString(e)));
+                    }
+                }
+                size = std::max<long long>(1, std::min<long long>(size, n_items - next));
+                ranges.push_back({next, next + (int)size});
+                next += (int)size;
+            }
             const int lo = ranges.back().first, hi = ranges.back().second;
             ranges.pop_back();
             CK(cudaMemsetAsync(&ctr[0], 0, sizeof(unsigned long long), c->stream));
@@ -952,6 +987,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             CK(cudaMemcpyAsync(host_ctr, ctr, sizeof(unsigned long long) * n_counters, cudaMemcpyDeviceToHost,
                                c->stream));
             if ((e = cudaStreamSynchronize(c->stream))) return cleanup(fail(RB_ERR_CUDA, "pair kernel: %s", cudaGetErrorString(e)));
+            if (host_ctr[BAD]) return cleanup(bad_refs());
             float pms = 0;
             cudaEventElapsedTime(&pms, c->ev0, c->ev_mid);
             res->stats.pair_ms += pms;
@@ -1013,7 +1049,10 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             res->stats.launches += 1;
             std::copy(host_ctr, host_ctr + n_counters, base.begin());
             P->last_surv = std::max(P->last_surv, surv);
+            done_items += hi - lo;
+            done_surv += surv;
         }
+        P->surv_rate = done_items ? (double)done_surv / (double)done_items : -1.0;
         const long long rows = (long long)base[1];
         res->count = rows;
         res->stats.comparisons = (int64_t)base[2];
@@ -1053,8 +1092,10 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             if (e) return cleanup(fail(RB_ERR_OOM, "part buffer of %lld rows: %s", cap, cudaGetErrorString(e)));
         }
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * n_counters, c->stream));
+        if (refs) CK(launch_refs_check((const int32_t*)c->refs.p, n, rel->n, &ctr[BAD], c->stream));
 
         RunParams R{};
+        R.bad_refs = refs ? &ctr[BAD] : nullptr;
         R.refs = refs ? (const int32_t*)c->refs.p : nullptr;
         R.n = n;
         R.flags = flags;
@@ -1081,6 +1122,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         CK(cudaMemcpyAsync(host_ctr, ctr, sizeof(unsigned long long) * n_counters, cudaMemcpyDeviceToHost, c->stream));
         e = cudaStreamSynchronize(c->stream);
         if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel: %s", cudaGetErrorString(e)));
+        if (host_ctr[BAD]) return cleanup(bad_refs());
         float ms = 0;
         cudaEventElapsedTime(&ms, c->ev0, c->ev1);
         res->stats.kernel_ms += ms;

@@ -194,6 +194,7 @@ struct RunParams {
     int4* surv;
     long long surv_cap;
     unsigned long long* surv_count;
+    const unsigned long long* bad_refs;  // non-zero: a tuple ref is out of range, evaluate nothing
 };
 
 // device-side helpers shared by kernels
@@ -961,6 +962,7 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
     unsigned long long my_pairs = 0, my_surv = 0;
     int32_t* scratch = R.scratch + (int64_t)(blockIdx.x * BLOCK + threadIdx.x) * R.scratch_stride;
 
+    if (R.bad_refs && *R.bad_refs) return;  // the host reports the bad ref
     for (int k = threadIdx.x; k < MAX_RULES; k += BLOCK) cp_rule[k] = V.cp_rule[k];
     for (int k = threadIdx.x; k < F.n_tab; k += BLOCK) tab[k] = F.tab_src[k];
 

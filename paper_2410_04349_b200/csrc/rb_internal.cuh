@@ -24,6 +24,8 @@ struct CompositeSpec {
     const int32_t* len[MAX_EQ + MAX_TOK * MAX_FSLOTS];    // token list length (-1 missing)
     const uint2* hash[MAX_EQ + MAX_TOK * MAX_FSLOTS];     // token list hash
 };
+cudaError_t launch_refs_check(const int32_t* refs, int64_t n, int64_t limit, unsigned long long* bad,
+                              cudaStream_t st);
 cudaError_t launch_composite_key(int64_t n, const CompositeSpec& spec, int32_t* out, cudaStream_t st);
 cudaError_t launch_pair_kernel(const FilterPlan& F, const VerifyProg& V, const RunParams& R, int grid,
                                cudaStream_t st);

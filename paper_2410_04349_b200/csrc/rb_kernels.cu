@@ -121,6 +121,25 @@ cudaError_t launch_composite_key(int64_t n, const CompositeSpec& spec, int32_t* 
     return cudaGetLastError();
 }
 
+// Range check of a run's tuple refs (replaces a host scan of every ref).
+__global__ void refs_check_kernel(const int32_t* __restrict__ refs, int64_t n, int64_t limit,
+                                  unsigned long long* bad) {
+    bool ok = true;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = refs[k];
+        ok &= r >= 0 && (int64_t)r < limit;
+    }
+    if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1ull);
+}
+
+cudaError_t launch_refs_check(const int32_t* refs, int64_t n, int64_t limit, unsigned long long* bad,
+                              cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    int grid = (int)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8);
+    refs_check_kernel<<<grid, 256, 0, st>>>(refs, n, limit, bad);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // the generic pair kernel (shape read from the kernel parameters)
 

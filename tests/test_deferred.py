@@ -53,3 +53,21 @@ def test_survivor_limit_streams_in_ranges(name, monkeypatch):
         assert cs.stats.specialized
         if cs.stats.blocks[0].survivors > 5:
             assert cs.stats.launches > 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("flavour", ["specialized", "generic"])
+def test_out_of_range_ref_fails_loudly(flavour, monkeypatch):
+    """A tuple ref outside the relation is caught on the device before any
+    pair is evaluated, and reported with its position."""
+    from paper_2410_04349_b200.errors import ConfigError
+
+    if flavour == "generic":
+        monkeypatch.setenv("RB_JIT", "0")
+    else:
+        monkeypatch.delenv("RB_JIT", raising=False)
+    rel, path, _ = goldens.load("products")
+    with pytest.raises(ConfigError, match="position 3"):
+        run_partition(DataPartition(0, (0, 1, 2, len(rel) + 7)), rel, path)
+    with pytest.raises(ConfigError, match="outside the relation"):
+        run_cross(DataPartition(0, (0, 1)), DataPartition(1, (len(rel),)), rel, path)
