@@ -509,6 +509,8 @@ def main():
                     pipe = {k: float(m[k]["value"]) for k in (
                         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
                         "smsp__issue_active.avg.pct_of_peak_sustained_active") if k in m}
+                    if "smsp__inst_executed.sum" in m:  # the per-pair instruction cost of the capture
+                        pipe["warp_instructions_per_pair"] = float(m["smsp__inst_executed.sum"]["value"]) / pairs_step
                     pipe["source"] = entry.get("capture")
             except Exception:
                 traffic = None

@@ -1,4 +1,5 @@
 set -x
-bash tools/gpu_perf.sh s8
-bash tools/gpu_variants.sh var8 edit_heavy "RB_JIT_UNROLL=2"
-bash tools/gpu_variants.sh var8 linkage "RB_JIT_UNROLL=2"
+timeout 900 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err; tail -1 gpurun_out/final_bench.json | cut -c1-300
+bash profiles/capture.sh r1s8c citation3 1000000 2024
+bash profiles/capture.sh r1s8e edit_heavy 1000000 11
+bash tools/scale_runs.sh
