@@ -1,5 +1,5 @@
 /*
- * rbencode.h -- native columnar encoding of ASCII text columns (librbgpu.so).
+ * rbencode.h -- native columnar ingest and encoding of text columns (librbgpu.so).
  *
  * Host-side producers of the device columns of include/rbgpu.h.  Each
  * restates, for all-ASCII columns, the reference's Python encoding:
@@ -33,6 +33,33 @@ int64_t rb_encode_tokens(const char* buf, const int64_t* offsets, const uint8_t*
  * returns the number of bytes written */
 int64_t rb_encode_chars(const char* buf, const int64_t* offsets, const uint8_t* missing, int64_t n,
                         int64_t* out_offsets, uint8_t* out);
+
+/* ---- columnar CSV ingest (rb_csv.cpp): load_relation, relation.py:186-257.
+ * rb_csv_parse reads CSV with the semantics of Python's csv.reader default
+ * dialect over a file opened with newline=""; the first record is the
+ * header.  Status: RB_CSV_OK; RB_CSV_FIELD_COUNT (a record's field count
+ * differs from the header's; *err_line = its record number, data records
+ * numbered from 2 as in relation.py); RB_CSV_NEEDS_PYTHON (invalid UTF-8, a
+ * NUL byte, a field over the csv field limit: run csv.reader for its exact
+ * behaviour); RB_CSV_EMPTY (no header row). */
+#define RB_CSV_OK 0
+#define RB_CSV_FIELD_COUNT (-1)
+#define RB_CSV_NEEDS_PYTHON (-2)
+#define RB_CSV_EMPTY (-3)
+#define RB_CSV_INVALID (-4)
+typedef struct rb_csv rb_csv;
+int rb_csv_parse(const char* data, int64_t len, rb_csv** out, int64_t* err_line);
+int rb_csv_shape(const rb_csv* t, int64_t* rows, int32_t* cols);
+int rb_csv_header(const rb_csv* t, int32_t col, const char** bytes, int64_t* nbytes);
+/* the cells of one column: bytes [offsets[r], offsets[r+1]) of *bytes, valid until rb_csv_free */
+int rb_csv_column(const rb_csv* t, int32_t col, const char** bytes, int64_t* nbytes, const int64_t** offsets);
+void rb_csv_free(rb_csv* t);
+
+/* parse_number (relation.py:64-77) per cell: status[i] = 1 number (out[i]),
+ * 0 not a number, 2 the cell is not ASCII (decide it in Python) */
+void rb_parse_numbers(const char* buf, const int64_t* offsets, int64_t n, double* out, uint8_t* status);
+/* len(cell.split()) per cell, -1 when the cell is not ASCII */
+void rb_token_counts(const char* buf, const int64_t* offsets, int64_t n, int32_t* counts);
 
 #ifdef __cplusplus
 }

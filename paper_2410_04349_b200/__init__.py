@@ -24,6 +24,7 @@ from .engine import (
     run_partition_rows,
     split_rows_by_pairs,
 )
+from .ingest import ColumnarRelation, load_relation
 from .errors import ConfigError, DataParseError, RuleBlockError, RuleParseError, SchemaError, ValidationError
 from .pipeline import BandingConfig, PipelineConfig, PipelineResult, iter_partitions, pipeline_run
 from .plan import Checkpoint, EvalPredicate, ExecutionPath, plan_from_stats
@@ -34,7 +35,7 @@ from .rules import MDRule, Predicate, RuleSet, parse_ruleset, predicate_universe
 __version__ = "0.1.0"
 
 __all__ = [
-    "BandingConfig", "BlockStats", "CandidateSet", "MultiDeviceEngine", "PipelineConfig", "PipelineResult",
+    "BandingConfig", "BlockStats", "ColumnarRelation", "load_relation", "CandidateSet", "MultiDeviceEngine", "PipelineConfig", "PipelineResult",
     "iter_partitions", "pipeline_run", "Checkpoint", "ConfigError", "DataParseError", "DataPartition", "Encoded",
     "EngineConfig", "PairBitmaps", "evaluate_pair", "EvalPredicate", "ExecutionPath", "Kind", "MDRule", "MISSING", "PathProgram", "Predicate",
     "Relation", "RelationEncoding", "RuleBlockError", "RuleParseError", "RuleSet", "RunStats", "Schema",

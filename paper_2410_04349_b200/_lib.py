@@ -86,6 +86,13 @@ _SIGNATURES = {
     "rb_encode_eq_codes": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int64, c_vp]),
     "rb_encode_tokens": (ctypes.c_int64, [c_vp, c_vp, c_vp, ctypes.c_int64, c_vp, c_vp, c_i32p]),
     "rb_encode_chars": (ctypes.c_int64, [c_vp, c_vp, c_vp, ctypes.c_int64, c_vp, c_vp]),
+    "rb_csv_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, c_vpp, c_i64p]),
+    "rb_csv_shape": (ctypes.c_int, [c_vp, c_i64p, c_i32p]),
+    "rb_csv_header": (ctypes.c_int, [c_vp, ctypes.c_int32, c_vpp, c_i64p]),
+    "rb_csv_column": (ctypes.c_int, [c_vp, ctypes.c_int32, c_vpp, c_i64p, ctypes.POINTER(ctypes.POINTER(ctypes.c_int64))]),
+    "rb_csv_free": (None, [c_vp]),
+    "rb_parse_numbers": (None, [c_vp, c_vp, ctypes.c_int64, c_vp, c_vp]),
+    "rb_token_counts": (None, [c_vp, c_vp, ctypes.c_int64, c_vp]),
 }
 
 

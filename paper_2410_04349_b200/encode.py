@@ -220,6 +220,10 @@ def _const_key(const):
     return ("num", float(const)) if isinstance(const, (int, float)) and not isinstance(const, bool) else ("str", const)
 
 
+def _is_columnar(relation) -> bool:
+    return hasattr(relation, "text_column") and hasattr(relation, "numeric_column")
+
+
 def _ascii_column(cols: list):
     """(bytes, offsets int64, missing uint8) of the concatenated str columns
     when every present value is an ASCII ``str``; None otherwise (the
@@ -266,9 +270,52 @@ class RelationEncoding(Encoded):
 
     def _column(self, attr: str) -> list:
         if attr not in self._cols:
-            k = self.schema.index_of(attr)
-            self._cols[attr] = [rec.values[k] for rec in self.relation.tuples]
+            if _is_columnar(self.relation):  # one column's values, no row objects
+                self._cols[attr] = self.relation.column(attr)
+            else:
+                k = self.schema.index_of(attr)
+                self._cols[attr] = [rec.values[k] for rec in self.relation.tuples]
         return self._cols[attr]
+
+    def _ascii_raw(self, attrs: list):
+        """(bytes, offsets, missing) of text columns straight from a
+        columnar relation's CSV buffers when all of them are ASCII, else the
+        generic path over the column values."""
+        import os
+
+        rel = self.relation
+        if _is_columnar(rel) and os.environ.get("RB_NATIVE_ENCODE", "1") != "0":
+            cols = [rel.text_column(a) for a in attrs]
+            if all(c is not None and c.all_ascii() for c in cols):
+                if len(cols) == 1:
+                    c = cols[0]
+                    return c.buf.tobytes(), c.offsets, c.missing
+                bufs = [c.buf for c in cols]
+                offs = [cols[0].offsets]
+                base = int(cols[0].offsets[-1])
+                for c in cols[1:]:
+                    offs.append(c.offsets[1:] + base)
+                    base += int(c.offsets[-1])
+                return (np.concatenate(bufs).tobytes(), np.concatenate(offs),
+                        np.concatenate([c.missing for c in cols]))
+        return _ascii_column([self._column(a) for a in attrs])
+
+    def _numeric_codes(self, attr: str):
+        """First-appearance dictionary codes of a columnar numeric column
+        (_canonical_key on floats), vectorised; None if not columnar."""
+        rel = self.relation
+        got = rel.numeric_column(attr) if _is_columnar(rel) else None
+        if got is None:
+            return None
+        vals, miss = got
+        out = np.full(self.n, -1, dtype=np.int32)
+        idx = np.nonzero(miss == 0)[0]
+        if len(idx):
+            u, first, inv = np.unique(vals[idx], return_index=True, return_inverse=True)
+            rank = np.empty(len(u), dtype=np.int32)
+            rank[np.argsort(first, kind="stable")] = np.arange(len(u), dtype=np.int32)
+            out[idx] = rank[inv]
+        return out
 
     def _numeric(self, attr: str) -> bool:
         return is_numeric_kind(self.schema.kind_of(attr))
@@ -280,8 +327,12 @@ class RelationEncoding(Encoded):
 
     def _build(self, key):
         tag = key[0]
+        if tag == "codes" and self._numeric(key[1]):
+            codes = self._numeric_codes(key[1])
+            if codes is not None:
+                return Column(COL_CODES, codes)
         if tag == "codes" and not self._numeric(key[1]):
-            nat = _ascii_column([self._column(key[1])])
+            nat = self._ascii_raw([key[1]])
             if nat is not None:  # rb_encode_eq_codes: strip + first-appearance dictionary
                 buf, offs, miss = nat
                 L, lb = _native()
@@ -308,13 +359,13 @@ class RelationEncoding(Encoded):
             )
             return Column(COL_MASK, m)
         if tag == "tokens":
-            return self._tokens([self._column(key[1])], {})[0]
+            return self._tokens([key[1]], {})[0]
         if tag == "xtokens":
             vocab: dict = {}
-            a, b = self._tokens([self._column(key[1]), self._column(key[2])], vocab)
+            a, b = self._tokens([key[1], key[2]], vocab)
             return a, b
         if tag == "chars":
-            nat = _ascii_column([self._column(key[1])])
+            nat = self._ascii_raw([key[1]])
             if nat is not None:  # rb_encode_chars: strip + casefold, uint8 (all ASCII)
                 buf, offs, miss = nat
                 L, lb = _native()
@@ -334,8 +385,9 @@ class RelationEncoding(Encoded):
             return Column(COL_CHARS, flat, offsets, missing)
         return None
 
-    def _tokens(self, cols: list, vocab: dict) -> list:
-        nat = _ascii_column(cols)
+    def _tokens(self, attrs: list, vocab: dict) -> list:
+        nat = self._ascii_raw(attrs)
+        cols = [self._column(a) for a in attrs] if nat is None else attrs
         if nat is not None:  # rb_encode_tokens over the columns back to back (one shared vocabulary)
             buf, offs, miss = nat
             L, lb = _native()

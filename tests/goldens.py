@@ -19,7 +19,7 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 def names() -> list[str]:
     """Engine-level fixtures (one run per case)."""
-    return sorted(n for n in _all() if not n.startswith("pipeline_"))
+    return sorted(n for n in _all() if not n.startswith(("pipeline_", "ingest")))
 
 
 def pipeline_names() -> list[str]:
