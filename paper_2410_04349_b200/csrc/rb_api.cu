@@ -923,7 +923,10 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             return cleanup(fail(RB_ERR_OOM, "survivor buffer of %lld entries: %s", scap, cudaGetErrorString(e)));
         std::vector<unsigned long long> base(n_counters, 0);  // counters after the last completed range
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * n_counters, c->stream));
-        if (refs) CK(launch_refs_check((const int32_t*)c->refs.p, n, rel->n, &ctr[BAD], c->stream));
+        if (refs) {
+            CK(launch_refs_check((const int32_t*)c->refs.p, n, rel->n, &ctr[BAD], c->stream));
+            res->stats.launches += 1;
+        }
         RunParams R{};
         R.bad_refs = refs ? &ctr[BAD] : nullptr;
         R.refs = refs ? (const int32_t*)c->refs.p : nullptr;
@@ -1092,7 +1095,10 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             if (e) return cleanup(fail(RB_ERR_OOM, "part buffer of %lld rows: %s", cap, cudaGetErrorString(e)));
         }
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * n_counters, c->stream));
-        if (refs) CK(launch_refs_check((const int32_t*)c->refs.p, n, rel->n, &ctr[BAD], c->stream));
+        if (refs) {
+            CK(launch_refs_check((const int32_t*)c->refs.p, n, rel->n, &ctr[BAD], c->stream));
+            res->stats.launches += 1;
+        }
 
         RunParams R{};
         R.bad_refs = refs ? &ctr[BAD] : nullptr;

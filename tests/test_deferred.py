@@ -38,8 +38,8 @@ def test_survivor_buffer_overflow_reruns(name, monkeypatch):
     surv = [cs.stats.blocks[0].survivors for cs in runs]
     assert any(s > 7 for s in surv)
     for cs, s in zip(runs, surv):
-        if s > 7:  # the first pair launch overflowed and was rolled back: pair, pair + verify
-            assert cs.stats.launches == 3
+        if s > 7:  # ref check, then the first pair launch overflowed and was rolled back: pair, pair + verify
+            assert cs.stats.launches == 4
 
 
 @pytest.mark.gpu
@@ -52,7 +52,7 @@ def test_survivor_limit_streams_in_ranges(name, monkeypatch):
     for cs in runs:
         assert cs.stats.specialized
         if cs.stats.blocks[0].survivors > 5:
-            assert cs.stats.launches > 2
+            assert cs.stats.launches > 3
 
 
 @pytest.mark.gpu

@@ -1,5 +1,4 @@
 set -x
-timeout 900 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err; tail -1 gpurun_out/final_bench.json | cut -c1-300
-bash profiles/capture.sh r1s8c citation3 1000000 2024
-bash profiles/capture.sh r1s8e edit_heavy 1000000 11
-bash tools/scale_runs.sh
+bash tools/gpu_variants.sh var9 citation3 "RB_JIT_ROWS=3" "RB_JIT_ROWS=2"
+bash tools/gpu_variants.sh var9 person5 "RB_JIT_BITS=8 RB_JIT_ROWS=1 RB_JIT_MINBLOCKS=4" "RB_JIT_BITS=8 RB_JIT_ROWS=1 RB_JIT_MINBLOCKS=3" "RB_JIT_ROWS=1 RB_JIT_MINBLOCKS=4" "RB_JIT_ROWS=2"
+bash tools/gpu_variants.sh var9 edit_heavy "RB_JIT_ROWS=3"
