@@ -1,4 +1,5 @@
 set -x
-bash tools/gpu_variants.sh var9 citation3 "RB_JIT_ROWS=3" "RB_JIT_ROWS=2"
-bash tools/gpu_variants.sh var9 person5 "RB_JIT_BITS=8 RB_JIT_ROWS=1 RB_JIT_MINBLOCKS=4" "RB_JIT_BITS=8 RB_JIT_ROWS=1 RB_JIT_MINBLOCKS=3" "RB_JIT_ROWS=1 RB_JIT_MINBLOCKS=4" "RB_JIT_ROWS=2"
-bash tools/gpu_variants.sh var9 edit_heavy "RB_JIT_ROWS=3"
+timeout 1500 python -m pytest tests/ -q -m gpu -x 2>&1 | tail -25 > gpurun_out/gpu_tests.log; tail -2 gpurun_out/gpu_tests.log
+bash tools/gpu_perf.sh s11
+bash tools/gpu_variants.sh var11 citation3 "RB_JIT_MIRROR=0"
+bash tools/gpu_variants.sh var11 citation3_parts "RB_JIT_MIRROR=0"
