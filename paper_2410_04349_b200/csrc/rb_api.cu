@@ -889,7 +889,11 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     CK(cudaMemcpyAsync(c->items.p, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice, c->stream));
     if (refs) CK(cudaMemcpyAsync(c->refs.p, refs, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
 
-    long long cap = std::max<long long>(1 << 20, P->last_rows + P->last_rows / 4);
+    // output rows: the previous run's count + 25%, at least RB_OUT_MIN (1M; tests lower it
+    // to drive the grow-in-place path)
+    const char* env_out = std::getenv("RB_OUT_MIN");
+    long long cap = std::max<long long>(env_out ? std::max(1ll, std::atoll(env_out)) : 1 << 20,
+                                        P->last_rows + P->last_rows / 4);
     unsigned long long* ctr = (unsigned long long*)c->counters.p;
     res->ctx = c;
     unsigned long long stack_ctr[n_counters];
@@ -902,7 +906,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         // larger buffer (up to SURV_LIMIT) or split in half, so any survivor
         // volume streams through a bounded buffer; the output buffer grows
         // (keeping its rows) before a verify that could overflow it.
-        if (c->pool[0] && c->pool_cap >= cap) {
+        if (c->pool[0] && c->pool_cap >= cap && !env_out) {
             res->d_t = c->pool[0];
             res->d_s = c->pool[1];
             res->d_r = c->pool[2];

@@ -71,3 +71,32 @@ def test_out_of_range_ref_fails_loudly(flavour, monkeypatch):
         run_partition(DataPartition(0, (0, 1, 2, len(rel) + 7)), rel, path)
     with pytest.raises(ConfigError, match="outside the relation"):
         run_cross(DataPartition(0, (0, 1)), DataPartition(1, (len(rel),)), rel, path)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", [c for c in CASES if c in goldens.names()])
+def test_output_grows_in_place_across_ranges(name, monkeypatch):
+    """Tiny survivor budget (many ranges) and a 2-row initial output buffer:
+    rows already written must survive every in-place growth."""
+    monkeypatch.delenv("RB_JIT", raising=False)
+    monkeypatch.setenv("RB_SURV_MIN", "2")
+    monkeypatch.setenv("RB_SURV_LIMIT", "16")
+    monkeypatch.setenv("RB_OUT_MIN", "2")
+    _replay(name)
+
+
+@pytest.mark.gpu
+def test_batched_output_growth_keeps_parts(monkeypatch):
+    """The same with a batched run: the partition index of every kept row
+    must move with it."""
+    from paper_2410_04349_b200 import run_partitions
+
+    monkeypatch.delenv("RB_JIT", raising=False)
+    rel, path, cases = goldens.load("citation")
+    parts = [DataPartition(k, tuple(range(k * 400, min(len(rel), k * 400 + 700)))) for k in range(10)]
+    want = [run_partition(p, rel, path).sorted_pairs() for p in parts]
+    monkeypatch.setenv("RB_SURV_MIN", "2")
+    monkeypatch.setenv("RB_SURV_LIMIT", "64")
+    monkeypatch.setenv("RB_OUT_MIN", "2")
+    got = [cs.sorted_pairs() for cs in run_partitions(parts, rel, path)]
+    assert got == want and sum(map(len, want)) > 10

@@ -21,7 +21,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2410_04349_b200 import DataPartition, EngineConfig, ingest, run_partition  # noqa: E402
 from paper_2410_04349_b200.encode import RelationEncoding  # noqa: E402
 from paper_2410_04349_b200.engine import PathProgram  # noqa: E402
-from paper_2410_04349_b200.rules import parse_ruleset  # noqa: E402
+from paper_2410_04349_b200.rules import parse_ruleset, predicate_universe  # noqa: E402
 from paper_2410_04349_b200.synth import CITATION3_RULES, data_aware_plan  # noqa: E402
 
 
@@ -49,12 +49,11 @@ def main():
     rel = ingest.load_relation(path)
     t["ingest_s"] = time.perf_counter() - t0
     t0 = time.perf_counter()
-    enc = RelationEncoding(rel)
+    enc = RelationEncoding(rel).prepare(sorted(predicate_universe(rules), key=str))
+    t["encode_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
     path_ = data_aware_plan(enc, rules, sample=200_000, seed=0)  # planning (not part of blocking time)
     t["plan_s"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    enc.prepare(path_.predicate_table)
-    t["encode_s"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     prog = PathProgram(path_, enc)
     t["upload_and_compile_s"] = time.perf_counter() - t0
