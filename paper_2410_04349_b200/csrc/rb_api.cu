@@ -520,6 +520,7 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             F.eq_outer[f] = (const int32_t*)d_o;
             F.eq_inner[f] = (const int32_t*)d_i;
             F.eq_kill[f] = g.second;
+            F.eq_slots[f] = g.first;
             for (int s = 0; s < n_slots; s++)
                 if ((g.first >> s) & 1) covered[s] |= g.second;
         }
@@ -550,6 +551,7 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                 F.eq_inner[f] = R.codes;
             }
             F.eq_kill[f] |= kill;
+            F.eq_slots[f] |= 1ull << s;
             cls[s] = 0;
         } else if (sl.kind == RB_SLOT_EQ_CONST) {
             auto it = constf.find(sl.lhs);
@@ -592,6 +594,8 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             fs = FSlot{};
             fs.kill = kill;
             fs.kind = sl.kind;
+            fs.slot = s;
+            fs.delta = sl.delta;
             if (sl.kind == RB_SLOT_JACCARD)
                 treq.push_back({true, f, at, sl.tab0, sl.len0, sl.tab1, sl.len1, rel->max_len[sl.lhs],
                                 rel->max_len[sl.rhs]});
@@ -623,6 +627,8 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             FSlot& fs = F.str_slot[f][at];
             fs.kill = kill;
             fs.kind = sl.kind;
+            fs.slot = s;
+            fs.delta = sl.delta;
             treq.push_back({false, f, at, sl.tab0, sl.len0, sl.tab1, sl.len1, 0, 0});
             F.str_rules[f] |= kill;
             F.str_kill[f] |= kill;
@@ -652,6 +658,90 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             }
             if (uses && !earlier) F.str_always[f] = 1;
         }
+    }
+    // ---- implied kills: a failed test also rules out every rule that needs
+    // a test implying it.  The threshold tables are monotone in delta, so a
+    // Jaccard (edit) slot failing implies every slot on the same feature
+    // with a higher delta fails; an equality key failing implies every key
+    // over a superset of its slots fails (a component of a composite key);
+    // an exact_token slot failing implies the composite keys containing it.
+    {
+        uint64_t tk[MAX_TOK][MAX_FSLOTS], sk[MAX_STR][MAX_FSLOTS], ek[MAX_EQ];
+        for (int f = 0; f < F.n_tok; f++)
+            for (int z = 0; z < F.tok_nslots[f]; z++) tk[f][z] = F.tok_slot[f][z].kill;
+        for (int f = 0; f < F.n_str; f++)
+            for (int z = 0; z < F.str_nslots[f]; z++) sk[f][z] = F.str_slot[f][z].kill;
+        for (int f = 0; f < F.n_eq; f++) ek[f] = F.eq_kill[f];
+        for (int f = 0; f < F.n_tok; f++)
+            for (int z = 0; z < F.tok_njac[f]; z++)
+                for (int y = 0; y < F.tok_njac[f]; y++)
+                    if (y != z && F.tok_slot[f][y].delta >= F.tok_slot[f][z].delta) F.tok_slot[f][z].kill |= tk[f][y];
+        for (int f = 0; f < F.n_str; f++)
+            for (int z = 0; z < F.str_nslots[f]; z++)
+                for (int y = 0; y < F.str_nslots[f]; y++)
+                    if (y != z && F.str_slot[f][y].delta >= F.str_slot[f][z].delta) F.str_slot[f][z].kill |= sk[f][y];
+        for (int a = 0; a < F.n_eq; a++)
+            for (int b = 0; b < F.n_eq; b++)
+                if (a != b && F.eq_slots[a] && (F.eq_slots[a] & ~F.eq_slots[b]) == 0) F.eq_kill[a] |= ek[b];
+        for (int f = 0; f < F.n_tok; f++)
+            for (int z = F.tok_njac[f]; z < F.tok_nslots[f]; z++)
+                for (int b = 0; b < F.n_eq; b++)
+                    if ((F.eq_slots[b] >> F.tok_slot[f][z].slot) & 1) F.tok_slot[f][z].kill |= ek[b];
+    }
+    // ---- stage-1 gate (specialised kernel): for each rule, in checkpoint
+    // order, not yet ruled out by a chosen test, choose the equality key or
+    // always-evaluated token slot holding its earliest path slot.  If every
+    // rule is covered, the other equality / token tests run only for warps
+    // with a live pair after stage 1.
+    {
+        const char* env_gate = std::getenv("RB_GATE");
+        bool covered_all = !(env_gate && env_gate[0] == '0');
+        uint64_t covered = 0;
+        std::vector<int> first_pos(n_slots, INT32_MAX);  // earliest instruction of each slot
+        for (int k = 0; k < n_ins; k++)
+            if (op[k] == 0 && first_pos[slot[k]] == INT32_MAX) first_pos[slot[k]] = k;
+        std::vector<char> eq_chosen(F.n_eq, 0);
+        std::vector<std::vector<char>> tok_chosen(F.n_tok, std::vector<char>(MAX_FSLOTS, 0));
+        for (size_t r = 0; r < need.size() && covered_all; r++) {
+            if ((covered >> r) & 1) continue;
+            int best_pos = INT32_MAX, bf = -1, bz = -1;  // bz < 0: equality key bf
+            for (int f = 0; f < F.n_eq; f++) {
+                if (!((F.eq_kill[f] >> r) & 1) || !(F.eq_slots[f] & need[r])) continue;
+                for (int sl2 = 0; sl2 < n_slots; sl2++)
+                    if (((F.eq_slots[f] & need[r]) >> sl2) & 1 && first_pos[sl2] < best_pos) {
+                        best_pos = first_pos[sl2];
+                        bf = f;
+                        bz = -1;
+                    }
+            }
+            for (int f = 0; f < F.n_tok; f++) {
+                if (!F.tok_always[f]) continue;
+                for (int z = 0; z < F.tok_nslots[f]; z++) {
+                    const FSlot& fs = F.tok_slot[f][z];
+                    if (((fs.kill >> r) & 1) && ((need[r] >> fs.slot) & 1) && first_pos[fs.slot] < best_pos) {
+                        best_pos = first_pos[fs.slot];
+                        bf = f;
+                        bz = z;
+                    }
+                }
+            }
+            if (bf < 0) {
+                covered_all = false;
+                break;
+            }
+            if (bz < 0) {
+                eq_chosen[bf] = 1;
+                covered |= F.eq_kill[bf];
+            } else {
+                tok_chosen[bf][bz] = 1;
+                covered |= F.tok_slot[bf][bz].kill;
+            }
+        }
+        F.gate = covered_all && F.n_rules > 0 ? 1 : 0;
+        for (int f = 0; f < F.n_eq; f++) F.eq_stage2[f] = F.gate && !eq_chosen[f];
+        for (int f = 0; f < F.n_tok; f++)
+            for (int z = 0; z < F.tok_nslots[f]; z++)
+                F.tok_slot[f][z].stage2 = F.gate && F.tok_always[f] && !tok_chosen[f][z];
     }
     std::vector<int32_t> stab(TAB_BASE, 0);  // guard entries: lookups of missing (-1) lengths land here
     {

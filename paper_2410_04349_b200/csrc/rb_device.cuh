@@ -101,11 +101,14 @@ struct DevSlot {
 // staged in shared memory at [off0, off0+cap0) and [off1, off1+cap1); a
 // length beyond a cap is simply not filtered (left to the exact pass).
 struct FSlot {
-    uint64_t kill;  // rules whose precondition contains this slot
+    uint64_t kill;  // rules whose precondition contains this slot (+ rules it rules out by implication)
     int32_t kind;
     int32_t off0, cap0;
     int32_t off1, cap1;
-    int32_t w2;  // jaccard in 2-D mode: need[n][m] at off0 + n*w2 + (m+1)
+    int32_t w2;      // jaccard in 2-D mode: need[n][m] at off0 + n*w2 + (m+1)
+    int32_t slot;    // the path slot it filters
+    int32_t stage2;  // evaluated after the stage-1 gate (see FilterPlan::gate)
+    double delta;    // threshold (implied kills between slots of one feature)
 };
 
 // Phase-1 filter program.  Per pair the kernel keeps the set of rules that
@@ -122,6 +125,11 @@ struct FilterPlan {
     const int32_t* eq_outer[MAX_EQ];
     const int32_t* eq_inner[MAX_EQ];
     uint64_t eq_kill[MAX_EQ];
+    uint64_t eq_slots[MAX_EQ];   // path slots the feature tests (a composite key: several)
+    int32_t eq_stage2[MAX_EQ];   // evaluated after the stage-1 gate
+    // Stage-1 gate: a few selective tests whose (implied) kills cover every
+    // rule run first; a warp with no live pair left skips all other tests.
+    int32_t gate;
     const uint8_t* const_mask[MAX_CONST];
     uint64_t const_kill[MAX_CONST];
     const int64_t* tok_ooff[MAX_TOK];
@@ -541,6 +549,9 @@ struct __align__(16) Tile {
 #define RB_STR_RULES(f) RB_PICK2(f, SPEC_STR_RULES_)
 #define RB_TOK_KILL(f, z) ((f) == 0 ? RB_PICK4(z, SPEC_TOK0_KILL_) : RB_PICK4(z, SPEC_TOK1_KILL_))
 #define RB_STR_KILL(f, z) ((f) == 0 ? RB_PICK4(z, SPEC_STR0_KILL_) : RB_PICK4(z, SPEC_STR1_KILL_))
+#define RB_GATE SPEC_GATE
+#define RB_EQ_STAGE2(f) RB_PICK6(f, SPEC_EQ_STAGE2_)
+#define RB_TOK_STAGE2(f, z) ((f) == 0 ? RB_PICK4(z, SPEC_TOK0_STAGE2_) : RB_PICK4(z, SPEC_TOK1_STAGE2_))
 // edit tables' shared-memory offsets as immediates: the lookup is one LEA + LDS [R + imm]
 #define RB_STR_OFF(f, z) ((f) == 0 ? RB_PICK4(z, SPEC_STR0_OFF_) : RB_PICK4(z, SPEC_STR1_OFF_))
 #else
@@ -567,6 +578,10 @@ struct __align__(16) Tile {
 #define RB_TOK_KILL(f, z) F.tok_slot[f][z].kill
 #define RB_STR_KILL(f, z) F.str_slot[f][z].kill
 #define RB_STR_OFF(f, z) F.str_slot[f][z].off0
+// the generic kernel evaluates every test in one stage
+#define RB_GATE 0
+#define RB_EQ_STAGE2(f) 0
+#define RB_TOK_STAGE2(f, z) 0
 #endif
 
 // Shared tables start at TAB_BASE so that the (discarded) lookups of pairs
@@ -818,8 +833,12 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
             alive[r] = AllValid ? base : m_gate(jj >= o[r].jj_lo && jj != o[r].jj_skip, base);
 #pragma unroll
             for (int f = 0; f < MAX_EQ; f++)
-                if (f < RB_NEQ) m_kill(alive[r], o[r].ocode[f] != T.r[jj].eq[f], RB_EQ_KILL(f));
+                if (f < RB_NEQ && !RB_EQ_STAGE2(f)) m_kill(alive[r], o[r].ocode[f] != T.r[jj].eq[f], RB_EQ_KILL(f));
         }
+        // token tests kept for stage 2 (always-evaluated features only)
+        int u_keep[ROWS][MAX_TOK];
+        int need_keep[ROWS][MAX_TOK][4];
+        uint32_t hash_keep[MAX_TOK];
 
 #pragma unroll
         for (int f = 0; f < MAX_TOK; f++) {
@@ -841,6 +860,8 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                                         __popc(o[r].lev[f][2] & is.z) + __popc(o[r].lev[f][3] & is.w) + o[r].orem[f];
                 const int n = o[r].olen[f];
                 int need2d[4] = {0, 0, 0, 0};
+                u_keep[r][f] = u;
+                hash_keep[f] = h.x;
                 if (RB_TOK2D && RB_TOK_NJ(f) > 0) {  // one vector load: every jaccard slot's need[n][m]
                     const uint32_t a = o[r].orow[f] + mo;
                     if (RB_TOK_NJP(f) == 1) {
@@ -858,8 +879,10 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                     }
                 }
 #pragma unroll
+                for (int z = 0; z < 4; z++) need_keep[r][f][z] = need2d[z];
+#pragma unroll
                 for (int z = 0; z < MAX_FSLOTS; z++) {
-                    if (z < RB_TOK_NS(f)) {
+                    if (z < RB_TOK_NS(f) && !RB_TOK_STAGE2(f, z)) {
                         const FSlot& fs = F.tok_slot[f][z];
                         bool ok;
                         if (z < RB_TOK_NJ(f)) {  // jaccard: exact integer tables
@@ -884,6 +907,34 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                 }
             }
         }
+#if RB_GATE
+        {
+            // stage-1 tests cover every rule: a warp with no live pair skips the rest
+            bool any = false;
+#pragma unroll
+            for (int r = 0; r < ROWS; r++) any |= m_any(alive[r]);
+            if (!__any_sync(FULL, any)) continue;
+#pragma unroll
+            for (int r = 0; r < ROWS; r++) {
+#pragma unroll
+                for (int f = 0; f < MAX_EQ; f++)
+                    if (f < RB_NEQ && RB_EQ_STAGE2(f))
+                        m_kill(alive[r], o[r].ocode[f] != T.r[jj].eq[f], RB_EQ_KILL(f));
+#pragma unroll
+                for (int f = 0; f < MAX_TOK; f++) {
+#pragma unroll
+                    for (int z = 0; z < MAX_FSLOTS; z++) {
+                        if (f < RB_NTOK && z < RB_TOK_NS(f) && RB_TOK_STAGE2(f, z)) {
+                            // 2-D Jaccard tables or the exact_token hash (stage 2 needs TOK2D)
+                            const bool ok = z < RB_TOK_NJ(f) ? u_keep[r][f] >= need_keep[r][f][z]
+                                                             : hash_keep[f] == o[r].ohash[f].x;
+                            m_kill(alive[r], !ok, RB_TOK_KILL(f, z));
+                        }
+                    }
+                }
+            }
+        }
+#endif
 #pragma unroll
         for (int f = 0; f < MAX_STR; f++) {
             if (f >= RB_NSTR) continue;

@@ -1,4 +1,4 @@
 set -x
-timeout 900 python tools/ingest_e2e.py 1000000 > gpurun_out/ingest_e2e.json 2> gpurun_out/ingest_e2e.err; tail -1 gpurun_out/ingest_e2e.json
-bash profiles/capture.sh r1s11l linkage 1000000 5
-bash profiles/capture.sh r1s11p person5 1000000 4
+timeout 1500 python -m pytest tests/ -q -m gpu -x 2>&1 | tail -25 > gpurun_out/gpu_tests.log; tail -2 gpurun_out/gpu_tests.log
+bash tools/gpu_perf.sh s12
+bash tools/gpu_variants.sh var12b citation3 "RB_GATE=0"
