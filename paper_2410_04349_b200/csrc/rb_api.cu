@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <utility>
@@ -111,6 +112,8 @@ struct rb_prog {
     int64_t lmax_edit = -1;  // longest string any edit slot reads (-1: no edit slot)
     std::vector<void*> allocs;
     JitKernel jit;
+    JitKernel jit_small;  // 2-row variant for batches of small partitions (compiled on first use)
+    bool jit_small_tried = false;
     long long last_rows = 0;  // output size of the previous run: sizes the next buffer
     long long last_surv = 0;  // survivors of the previous run: sizes the deferred-verification buffer
     double surv_rate = -1.0;  // survivors per work item in the previous run (-1: none yet)
@@ -930,7 +933,20 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         }
         return items;
     };
-    std::vector<Item> items = build_items((int64_t)BLOCK * (P->jit.ok ? P->jit.rows : 1));
+    // a 3-row kernel's 768-row items would leave threads idle on small
+    // partitions: batches whose average part is shorter use a 2-row variant
+    const JitKernel* jp = &P->jit;
+    if (P->jit.ok && P->jit.rows > 2 && !parts.empty() && total / (int64_t)parts.size() < (int64_t)BLOCK * P->jit.rows) {
+        static std::mutex small_mu;  // programs may be shared by host threads
+        std::lock_guard<std::mutex> lock(small_mu);
+        if (!P->jit_small_tried) {
+            P->jit_small = jit_pair_kernel(P->F, c->device, 2);
+            P->jit_small_tried = true;
+        }
+        if (P->jit_small.ok) jp = &P->jit_small;
+    }
+    const JitKernel& J = *jp;
+    std::vector<Item> items = build_items((int64_t)BLOCK * (J.ok ? J.rows : 1));
     int n_items = (int)items.size();
     const int64_t n = total;
     if (n_items == 0) {
@@ -953,7 +969,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     const char* env_min = std::getenv("RB_SURV_MIN");
     const long long SURV_LIMIT = env_lim ? std::max(1ll, std::atoll(env_lim)) : 1ll << 28;
     const long long SURV_MIN = env_min ? std::max(1ll, std::atoll(env_min)) : 1ll << 24;
-    const bool defer = P->jit.ok && P->jit.defer;
+    const bool defer = J.ok && J.defer;
     // capacity: the program's last survivor count, or whatever the context's
     // (pooled) buffer already holds, at least SURV_MIN entries (256 MB)
     long long scap = defer ? std::min(SURV_LIMIT, std::max<long long>({SURV_MIN, P->last_surv + P->last_surv / 4,
@@ -963,10 +979,10 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     if (cudaError_t e = c->counters.grow(sizeof(unsigned long long) * n_counters, c->stream))
         return cleanup(fail(RB_ERR_CUDA, "counters: %s", cudaGetErrorString(e)));
 
-    const int bps = P->jit.ok ? P->jit.blocks_per_sm : c->blocks_per_sm;
+    const int bps = J.ok ? J.blocks_per_sm : c->blocks_per_sm;
     const int grid = std::max(1, std::min(n_items, c->sm_count * bps));
     const int gridg = c->sm_count * c->blocks_per_sm;  // generic kernel (fallback)
-    const int grid_v = c->sm_count * (P->jit.ok ? P->jit.verify_blocks_per_sm : 1);  // deferred verification
+    const int grid_v = c->sm_count * (J.ok ? J.verify_blocks_per_sm : 1);  // deferred verification
     int64_t stride = 0;
     if (P->lmax_edit >= 0) {
         stride = (P->lmax_edit + 2 + 31) & ~(int64_t)31;
@@ -1078,7 +1094,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             R.out_p = res->d_p;
             R.cap = cap;
             CK(cudaEventRecord(c->ev0, c->stream));
-            cudaError_t e = launch_jit_kernel(P->jit, P->F, P->V, R, std::max(1, std::min(hi - lo, grid)), c->stream);
+            cudaError_t e = launch_jit_kernel(J, P->F, P->V, R, std::max(1, std::min(hi - lo, grid)), c->stream);
             if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel launch: %s", cudaGetErrorString(e)));
             CK(cudaEventRecord(c->ev_mid, c->stream));
             CK(cudaMemcpyAsync(host_ctr, ctr, sizeof(unsigned long long) * n_counters, cudaMemcpyDeviceToHost,
@@ -1134,7 +1150,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
                 R.cap = cap;
             }
             CK(cudaEventRecord(c->ev0, c->stream));
-            if ((e = launch_jit_verify(P->jit, P->V, R, grid_v, c->stream)))
+            if ((e = launch_jit_verify(J, P->V, R, grid_v, c->stream)))
                 return cleanup(fail(RB_ERR_CUDA, "verify kernel launch: %s", cudaGetErrorString(e)));
             CK(cudaEventRecord(c->ev1, c->stream));
             CK(cudaMemcpyAsync(host_ctr, ctr, sizeof(unsigned long long) * n_counters, cudaMemcpyDeviceToHost,
@@ -1157,7 +1173,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         res->stats.emitted = rows;
         res->stats.retries = retries;
         res->stats.specialized = 1;
-        res->stats.jit_compile_ms = P->jit.compile_ms;
+        res->stats.jit_compile_ms = J.compile_ms;
         P->last_rows = rows;
         for (int s = 0; s < RB_MAX_SLOTS; s++) res->stats.slot_evals[s] = (int64_t)base[4 + s];
         *out = res;
@@ -1215,7 +1231,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         R.scratch_stride = stride;
 
         CK(cudaEventRecord(c->ev0, c->stream));
-        e = P->jit.ok ? launch_jit_kernel(P->jit, P->F, P->V, R, grid, c->stream)
+        e = J.ok ? launch_jit_kernel(J, P->F, P->V, R, grid, c->stream)
                       : launch_pair_kernel(P->F, P->V, R, std::max(1, std::min(n_items, gridg)), c->stream);
         if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel launch: %s", cudaGetErrorString(e)));
         CK(cudaEventRecord(c->ev1, c->stream));
@@ -1235,8 +1251,8 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             res->stats.survivors = (int64_t)host_ctr[3];
             res->stats.emitted = rows;
             res->stats.retries = attempt;
-            res->stats.specialized = P->jit.ok ? 1 : 0;
-            res->stats.jit_compile_ms = P->jit.compile_ms;
+            res->stats.specialized = J.ok ? 1 : 0;
+            res->stats.jit_compile_ms = J.compile_ms;
             P->last_rows = rows;
             for (int s = 0; s < RB_MAX_SLOTS; s++) res->stats.slot_evals[s] = (int64_t)host_ctr[4 + s];
             break;

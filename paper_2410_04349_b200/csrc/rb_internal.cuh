@@ -46,7 +46,8 @@ struct JitKernel {
     std::string key;
     std::string log;
 };
-JitKernel jit_pair_kernel(const FilterPlan& F, int device);
+// force_rows > 0 compiles that many outer rows per thread (the small-partition variant)
+JitKernel jit_pair_kernel(const FilterPlan& F, int device, int force_rows = 0);
 cudaError_t launch_jit_kernel(const JitKernel& k, const FilterPlan& F, const VerifyProg& V, const RunParams& R,
                               int grid, cudaStream_t st);
 cudaError_t launch_jit_verify(const JitKernel& k, const VerifyProg& V, const RunParams& R, int grid, cudaStream_t st);
