@@ -797,10 +797,12 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             }
             if (!t.tok) {
                 // edit: one interleaved int2 table {G, M2}[L] with
-                //   G  = min(maxgap[L], maxd[L])  (gap test and gap <= lev)
+                //   G  = min(maxgap[L], maxd[L])  (gap test; not read by the current filter)
                 //   M2 = 2 * maxd[L]              (ceil((bag + gap) / 2) <= maxd)
-                // L = 0 always accepts; a guard entry {-1, -1} at L = -1 makes
-                // a pair with both strings missing fail.
+                // The pair filter tests bag + gap <= max(M2[la], M2[lb]) with
+                // both values looked up once per tuple (str_m2); M2[0] = 0
+                // lets two empty strings through.  A guard entry {-1, -1}
+                // precedes the table.
                 const int32_t* maxgap = tables + t.src0;
                 const int32_t* maxd = tables + t.src1;
                 const int64_t lim = std::min(t.len0, t.len1);
@@ -811,9 +813,9 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                 fs.off0 = (int32_t)stab.size();
                 fs.cap0 = (int32_t)c;
                 for (int64_t L = 0; L < c; L++) {
-                    if (L == 0) {
+                    if (L == 0) {  // two empty strings match: t = 0 passes; M2 stays monotone in L
                         stab.push_back(INF);
-                        stab.push_back(INF);
+                        stab.push_back(0);
                     } else {
                         stab.push_back(std::min(maxgap[L], maxd[L]));
                         stab.push_back(maxd[L] < 0 ? -1 : 2 * maxd[L]);

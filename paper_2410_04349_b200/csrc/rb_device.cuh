@@ -500,7 +500,7 @@ __device__ __forceinline__ void verify_body(const VerifyProg& V, const RunParams
 // One inner tuple's streamed features, stored record-wise so that the pair
 // loop reads every field of tuple jj at a constant offset from one running
 // shared-memory address (eq codes and token length share a 32-byte line).
-// 144-byte stride: the tile fill (thread k writes record k) hits 8 banks
+// 160-byte stride: the tile fill (thread k writes record k) hits 8 banks
 // instead of 1.
 struct __align__(16) Rec {
     int32_t eq[MAX_EQ];
@@ -511,7 +511,7 @@ struct __align__(16) Rec {
     int32_t tid;
     int32_t pad0;
     uint4 strbag[MAX_STR];
-    uint4 pad1;
+    int32_t strm2[MAX_STR][MAX_FSLOTS];  // 2*maxd[|s|] per edit slot (see the string filter)
 };
 
 struct __align__(16) Tile {
@@ -604,6 +604,14 @@ static __device__ __forceinline__ int2 lds_s32x2(uint32_t addr) {
     asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
     return v;
 }
+// 2*maxd[len] of an edit slot from its {G, M2} table (rb_program_create);
+// lengths past a partial table are not filtered; a missing string gets -1
+static __device__ __forceinline__ int str_m2(const int32_t* tab, const FSlot& fs, int off, int len) {
+    if (len < 0) return -1;
+    if ((unsigned)len >= (unsigned)fs.cap0) return INT_MAX;
+    return tab[off + 2 * len + 1];
+}
+
 // sum over the four bytes of |a_i - b_i|, plus c (VABSDIFF4 with accumulate)
 static __device__ __forceinline__ uint32_t vsad4_acc(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
@@ -689,6 +697,7 @@ struct Outer {
     uint2 ohash[MAX_TOK];
     int32_t oslen[MAX_STR];
     uint4 obag[MAX_STR];
+    int32_t om2[MAX_STR][MAX_FSLOTS];  // 2*maxd[|t|] per edit slot
 
     __device__ __forceinline__ void load(const FilterPlan& F, const RunParams& R, const int32_t* tab, int mode,
                                          int64_t i_, int64_t row_hi, int64_t col0, int64_t col1,
@@ -774,11 +783,16 @@ struct Outer {
         for (int f = 0; f < MAX_STR; f++) {
             oslen[f] = -1;
             obag[f] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int z = 0; z < MAX_FSLOTS; z++) om2[f][z] = -1;
             if (f < RB_NSTR && ok) {
                 oslen[f] = __ldg(F.str_olen[f] + ti);
                 obag[f] = __ldg(F.str_obag[f] + ti);
                 m_kill(alive0, oslen[f] < 0, RB_STR_ROWKILL(f));  // missing t side: edit is false
-                if (oslen[f] < 0) obag[f] = make_uint4(0, 0, 0, 0);  // with gap = |s| + 1 the gap test fails on its own
+                if (oslen[f] < 0) obag[f] = make_uint4(0, 0, 0, 0);  // with gap = |s| + 1 the bag bound fails on its own
+#pragma unroll
+                for (int z = 0; z < MAX_FSLOTS; z++)
+                    if (z < RB_STR_NS(f)) om2[f][z] = str_m2(tab, F.str_slot[f][z], RB_STR_OFF(f, z), oslen[f]);
             }
         }
     }
@@ -947,22 +961,18 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
 #pragma unroll
             for (int r = 0; r < ROWS; r++) {
                 const int la = o[r].oslen[f];
-                const int L = max(la, lb);
-                const int gap = abs(la - lb);
-                // bag + gap in four accumulating byte-SAD steps
+                // t = bag distance + |la - lb| in five accumulating SAD steps;
+                // lev <= maxd[L] implies t <= 2*maxd[L] <= max(2*maxd[la], 2*maxd[lb])
+                // (L is one of la, lb), so no max, no table lookup per pair
                 const int t = (int)vsad4_acc(o[r].obag[f].w, ib.w,
                                              vsad4_acc(o[r].obag[f].z, ib.z,
                                                        vsad4_acc(o[r].obag[f].y, ib.y,
-                                                                 vsad4_acc(o[r].obag[f].x, ib.x, (uint32_t)gap))));
+                                                                 vsad4_acc(o[r].obag[f].x, ib.x,
+                                                                           __sad(la, lb, 0u)))));
 #pragma unroll
                 for (int z = 0; z < MAX_FSLOTS; z++) {
                     if (z < RB_STR_NS(f)) {
-                        const FSlot& fs = F.str_slot[f][z];
-                        // {G, M2}[L] (host: rb_program_create); lengths past a partial table are not filtered
-                        const int2 gm = (RB_FULLTAB || (unsigned)L < (unsigned)fs.cap0)
-                                            ? lds_s32x2(tab_s + 4u * (uint32_t)RB_STR_OFF(f, z) + 8u * (uint32_t)L)
-                                            : make_int2(INT_MAX, INT_MAX);
-                        const bool ok = (gap <= gm.x) & (t <= gm.y);
+                        const bool ok = t <= max(o[r].om2[f][z], T.r[jj].strm2[f][z]);
                         m_kill(alive[r], !ok, RB_STR_KILL(f, z));
                     }
                 }
@@ -1058,8 +1068,12 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
 #pragma unroll
                 for (int f = 0; f < MAX_STR; f++)
                     if (f < RB_NSTR) {
-                        T.r[k].strlen_[f] = __ldg(F.str_ilen[f] + sj);
+                        const int lb = __ldg(F.str_ilen[f] + sj);
+                        T.r[k].strlen_[f] = lb;
                         T.r[k].strbag[f] = __ldg(F.str_ibag[f] + sj);
+#pragma unroll
+                        for (int z = 0; z < MAX_FSLOTS; z++)
+                            if (z < RB_STR_NS(f)) T.r[k].strm2[f][z] = str_m2(tab, F.str_slot[f][z], RB_STR_OFF(f, z), lb);
                     }
             }
             __syncthreads();
