@@ -755,7 +755,7 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             total1d += t.len0 + t.len1;
             // 2-D: the jaccard slots of one token feature share one interleaved table
             const int njp = t.tok ? (F.tok_njac[t.feat] <= 1 ? 1 : F.tok_njac[t.feat] <= 2 ? 2 : 4) : 0;
-            total2d += t.tok ? (t.z == 0 ? (t.nmax + 1) * (t.mmax + 2) * njp + 4 : 0) : t.len0 + t.len1 + 4;
+            total2d += t.tok ? (t.z == 0 ? (t.nmax + 1) * ((t.mmax + 2) | 1) * njp + 4 : 0) : t.len0 + t.len1 + 4;
         }
         F.tok2d = total2d <= SMEM_TAB ? 1 : 0;
         const bool full = F.tok2d || total1d <= SMEM_TAB;
@@ -769,7 +769,10 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                 // entry (n, m, z) at tok_off[f] + ((n * w2) + m + 1) * njp + z
                 const int f = t.feat;
                 const int njp = F.tok_njac[f] <= 1 ? 1 : F.tok_njac[f] <= 2 ? 2 : 4;
-                const int64_t w2 = t.mmax + 2;
+                // row stride (in entries) padded to an odd count: lanes of a warp
+                // read rows n of different outer tuples at the same column m, and
+                // an odd stride spreads them over distinct shared-memory banks
+                const int64_t w2 = (t.mmax + 2) | 1;
                 if (t.z == 0) {
                     while (stab.size() % 4) stab.push_back(INF);  // 16-byte alignment of vector entries
                     F.tok_off[f] = (int32_t)stab.size();
