@@ -503,8 +503,9 @@ __device__ __forceinline__ void verify_body(const VerifyProg& V, const RunParams
 // 160-byte stride: the tile fill (thread k writes record k) hits 8 banks
 // instead of 1.
 struct __align__(16) Rec {
-    int32_t eq[MAX_EQ];
-    int32_t toklen[MAX_TOK];
+    // equality codes at [0, n_eq), token-row lengths right after them at
+    // [n_eq, n_eq + n_tok): with few features one 16-byte load fetches all
+    int32_t head[MAX_EQ + MAX_TOK];
     uint4 toksig[MAX_TOK];
     uint2 tokhash[MAX_TOK];
     int32_t strlen_[MAX_STR];
@@ -847,7 +848,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
             alive[r] = AllValid ? base : m_gate(jj >= o[r].jj_lo && jj != o[r].jj_skip, base);
 #pragma unroll
             for (int f = 0; f < MAX_EQ; f++)
-                if (f < RB_NEQ && !RB_EQ_STAGE2(f)) m_kill(alive[r], o[r].ocode[f] != T.r[jj].eq[f], RB_EQ_KILL(f));
+                if (f < RB_NEQ && !RB_EQ_STAGE2(f)) m_kill(alive[r], o[r].ocode[f] != T.r[jj].head[f], RB_EQ_KILL(f));
         }
         // token tests kept for stage 2 (always-evaluated features only)
         int u_keep[ROWS][MAX_TOK];
@@ -861,7 +862,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
 #pragma unroll
             for (int r = 0; r < ROWS; r++) need |= m_hits(alive[r], RB_TOK_RULES(f));
             if (!RB_TOK_ALWAYS(f) && !__any_sync(FULL, need)) continue;
-            const int m = T.r[jj].toklen[f];
+            const int m = T.r[jj].head[RB_NEQ + f];
             const uint32_t mo = (uint32_t)(m * RB_TOK_NJP(f)) << 2;  // byte offset of column m within a need[n] row
             const uint4 is = T.r[jj].toksig[f];
             const uint2 h = T.r[jj].tokhash[f];
@@ -876,7 +877,15 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                 int need2d[4] = {0, 0, 0, 0};
                 u_keep[r][f] = u;
                 hash_keep[f] = h.x;
-                if (RB_TOK2D && RB_TOK_NJ(f) > 0) {  // one vector load: every jaccard slot's need[n][m]
+                bool split = false;  // a stage-2 Jaccard slot: load only the stage-1 thresholds now
+#pragma unroll
+                for (int z = 0; z < MAX_FSLOTS; z++) split |= RB_GATE && z < RB_TOK_NJ(f) && RB_TOK_STAGE2(f, z);
+                if (RB_TOK2D && RB_TOK_NJ(f) > 0 && split) {
+                    const uint32_t a = o[r].orow[f] + mo;
+#pragma unroll
+                    for (int z = 0; z < MAX_FSLOTS; z++)
+                        if (z < RB_TOK_NJ(f) && !RB_TOK_STAGE2(f, z)) need2d[z] = lds_s32(a + 4u * z);
+                } else if (RB_TOK2D && RB_TOK_NJ(f) > 0) {  // one vector load: every jaccard slot's need[n][m]
                     const uint32_t a = o[r].orow[f] + mo;
                     if (RB_TOK_NJP(f) == 1) {
                         need2d[0] = lds_s32(a);
@@ -933,14 +942,16 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
 #pragma unroll
                 for (int f = 0; f < MAX_EQ; f++)
                     if (f < RB_NEQ && RB_EQ_STAGE2(f))
-                        m_kill(alive[r], o[r].ocode[f] != T.r[jj].eq[f], RB_EQ_KILL(f));
+                        m_kill(alive[r], o[r].ocode[f] != T.r[jj].head[f], RB_EQ_KILL(f));
 #pragma unroll
                 for (int f = 0; f < MAX_TOK; f++) {
 #pragma unroll
                     for (int z = 0; z < MAX_FSLOTS; z++) {
                         if (f < RB_NTOK && z < RB_TOK_NS(f) && RB_TOK_STAGE2(f, z)) {
                             // 2-D Jaccard tables or the exact_token hash (stage 2 needs TOK2D)
-                            const bool ok = z < RB_TOK_NJ(f) ? u_keep[r][f] >= need_keep[r][f][z]
+                            // a stage-2 Jaccard threshold is read only now (rarely)
+                            const uint32_t mo2 = (uint32_t)(T.r[jj].head[RB_NEQ + f] * RB_TOK_NJP(f)) << 2;
+                            const bool ok = z < RB_TOK_NJ(f) ? u_keep[r][f] >= lds_s32(o[r].orow[f] + mo2 + 4u * z)
                                                              : hash_keep[f] == o[r].ohash[f].x;
                             m_kill(alive[r], !ok, RB_TOK_KILL(f, z));
                         }
@@ -1055,11 +1066,11 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
                 T.r[k].tid = sj;
 #pragma unroll
                 for (int f = 0; f < MAX_EQ; f++)
-                    if (f < RB_NEQ) T.r[k].eq[f] = __ldg(F.eq_inner[f] + sj);
+                    if (f < RB_NEQ) T.r[k].head[f] = __ldg(F.eq_inner[f] + sj);
 #pragma unroll
                 for (int f = 0; f < MAX_TOK; f++)
                     if (f < RB_NTOK) {
-                        T.r[k].toklen[f] = __ldg(F.tok_ilen[f] + sj);
+                        T.r[k].head[RB_NEQ + f] = __ldg(F.tok_ilen[f] + sj);
                         uint4 sg = __ldg(F.tok_isig[f] + sj);
                         if (RB_TOK_SIG64(f)) sg = make_uint4(sg.x | sg.z, sg.y | sg.w, 0u, 0u);
                         T.r[k].toksig[f] = sg;
