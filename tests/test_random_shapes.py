@@ -24,12 +24,19 @@ def test_generator_shapes():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("seed", range(24))
-@pytest.mark.parametrize("flavour", ["specialized", "generic"])
+@pytest.mark.parametrize("flavour", ["specialized", "generic", "plain"])
 def test_random_shapes_gpu_vs_oracle(seed, flavour, monkeypatch):
+    """specialized: the default kernel (composite keys, implied kills, stage-1
+    gate); generic: the statically built kernel; plain: specialised without
+    composite keys and without the gate."""
+    monkeypatch.delenv("RB_JIT", raising=False)
+    monkeypatch.delenv("RB_GATE", raising=False)
+    monkeypatch.delenv("RB_COMPOSITE", raising=False)
     if flavour == "generic":
         monkeypatch.setenv("RB_JIT", "0")
-    else:
-        monkeypatch.delenv("RB_JIT", raising=False)
+    elif flavour == "plain":
+        monkeypatch.setenv("RB_GATE", "0")
+        monkeypatch.setenv("RB_COMPOSITE", "0")
     rel, rules, path = randwork.make(seed)
     rng = random.Random(seed)
     n = len(rel)
