@@ -43,6 +43,7 @@ WORKLOAD_DESC = {
     "edit_heavy": "BASELINE config 3: edit-distance-heavy rules, 64-256-char strings, maxd 2-5",
     "linkage": "BASELINE config 5: two-table linkage, Zipf(1.3) blocks, one cross run per block, batched",
     "citation3_parts": "config 2 relation in 512-tuple partitions (the reference pipeline's default), batched",
+    "citation_small": "BASELINE config 1: the reference's citation_benchmark (4,591 tuples) with its frozen plan",
 }
 UNIT = "pairs/s"
 

@@ -15,6 +15,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import json
+
 import numpy as np
 
 from .encode import COL_CHARS, COL_CODES, COL_TOKENS, Column, Encoded
@@ -440,5 +442,29 @@ def citation3_parts(n: int = 1_000_000, seed: int = 2024, part: int = 512) -> Wo
     return w
 
 
+def citation_small(n: int = 0, seed: int = 2024) -> Workload:
+    """BASELINE config 1: the reference's own small benchmark relation --
+    ``citation_benchmark(seed=2024)`` (datasets.py:332-398, 4,591 tuples)
+    with its frozen plan, as recorded from the reference in
+    tests/golden/citation.json.gz -- one symmetric partition (1.05e7 pairs).
+    ``n`` and ``seed`` are fixed by the fixture."""
+    import gzip
+    import os
+
+    from .encode import RelationEncoding
+    from .plan import path_from_dict
+    from .relation import relation_from_rows
+
+    here = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                        "citation.json.gz")
+    with gzip.open(here, "rt") as fh:
+        doc = json.load(fh)
+    r = doc["relation"]
+    rel = relation_from_rows(r["names"], r["kinds"], r["rows"])
+    path = path_from_dict(doc["path"])
+    enc = RelationEncoding(rel).prepare(path.predicate_table)
+    return Workload("citation_small", enc, None, path, len(rel))
+
+
 WORKLOADS = {"citation3": citation3, "edit_heavy": edit_heavy, "linkage": linkage, "person5": person5,
-             "citation3_parts": citation3_parts}
+             "citation3_parts": citation3_parts, "citation_small": citation_small}
