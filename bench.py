@@ -178,13 +178,17 @@ def cpu_sample(w, prog, rows, nthreads):
 
 
 def sample_rows(n, budget_pairs, k=8):
-    """k row slices spread over the triangle whose pairs sum to ~budget."""
+    """k disjoint row slices spread over the triangle whose pairs sum to
+    ~budget; the whole triangle when it is within budget."""
+    if n * (n - 1) // 2 <= budget_pairs:
+        return [(0, n)]
     per = max(1, budget_pairs // k)
     out = []
     for q in range(k):
         lo = int(q * n / k)
+        nxt = int((q + 1) * n / k)
         rows = max(1, per // max(1, n - lo - 1))
-        out.append((lo, min(n - 1, lo + rows)))
+        out.append((lo, min(nxt, lo + rows)))
     return out
 
 

@@ -922,8 +922,8 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         return rc;
     };
 
-    // ---- work items: BLOCK * rows outer rows x CHUNK inner columns, per part
-    auto build_items = [&](int64_t rows_per_item) {
+    // ---- work items: BLOCK * rows outer rows x `chunk` inner columns, per part
+    auto build_items = [&](int64_t rows_per_item, int64_t chunk) {
         std::vector<Item> items;
         for (size_t pi = 0; pi < parts.size(); pi++) {
             const Part& pt = parts[pi];
@@ -935,11 +935,11 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             for (int64_t r0 = rlo; r0 < rhi; r0 += rows_per_item) {
                 const int64_t rend = std::min<int64_t>(r0 + rows_per_item, rhi);
                 int64_t c0 = cross ? pt.base + pt.split : (mode == MODE_SYM ? r0 + 1 : pt.base);
-                for (; c0 < end; c0 += CHUNK) {
+                for (; c0 < end; c0 += chunk) {
                     Item it{};
                     it.row0 = (int32_t)r0;
                     it.col0 = (int32_t)c0;
-                    it.col1 = (int32_t)std::min<int64_t>(c0 + CHUNK, end);
+                    it.col1 = (int32_t)std::min<int64_t>(c0 + chunk, end);
                     it.row_hi = (int32_t)rend;
                     it.mode = mode;
                     it.part = (int32_t)pi;
@@ -962,7 +962,14 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         if (P->jit_small.ok) jp = &P->jit_small;
     }
     const JitKernel& J = *jp;
-    std::vector<Item> items = build_items((int64_t)BLOCK * (J.ok ? J.rows : 1));
+    const int64_t rows_per_item = (int64_t)BLOCK * (J.ok ? J.rows : 1);
+    std::vector<Item> items = build_items(rows_per_item, CHUNK);
+    {
+        // small runs: narrower column chunks until every CTA has work (down to one tile)
+        const size_t target = 2 * (size_t)c->sm_count * (size_t)(J.ok ? J.blocks_per_sm : c->blocks_per_sm);
+        for (int64_t chunk = CHUNK / 2; items.size() < target && chunk >= TJ; chunk /= 2)
+            items = build_items(rows_per_item, chunk);
+    }
     int n_items = (int)items.size();
     const int64_t n = total;
     if (n_items == 0) {

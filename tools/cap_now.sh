@@ -1,5 +1,4 @@
 set -x
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 2 --warmup 3 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; echo n2 rc=$?; tail -1 gpurun_out/bench_n2.json | cut -c1-200
-bash profiles/capture.sh r1s24p person5 1000000 4
-bash profiles/capture.sh r1s24l linkage 1000000 5
-bash tools/scale_runs.sh
+timeout 1500 python -m pytest tests/ -q -m gpu -x 2>&1 | tail -25 > gpurun_out/gpu_tests.log; tail -2 gpurun_out/gpu_tests.log
+bash tools/gpu_perf.sh s26
+timeout 600 python bench.py --workload citation_small --steps 5 > gpurun_out/citation_small.json 2> gpurun_out/citation_small.err; tail -1 gpurun_out/citation_small.json | cut -c1-300
