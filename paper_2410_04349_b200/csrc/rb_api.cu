@@ -114,6 +114,11 @@ struct rb_prog {
     JitKernel jit;
     JitKernel jit_small;  // 2-row variant for batches of small partitions (compiled on first use)
     bool jit_small_tried = false;
+    // ungated variants, used once a run showed the stage-1 gate passing almost
+    // every warp iteration (its tests never fail inside these partitions)
+    JitKernel jit_nogate, jit_small_nogate;
+    bool jit_nogate_tried = false, jit_small_nogate_tried = false;
+    bool gate_off = false;
     long long last_rows = 0;  // output size of the previous run: sizes the next buffer
     long long last_surv = 0;  // survivors of the previous run: sizes the deferred-verification buffer
     double surv_rate = -1.0;  // survivors per work item in the previous run (-1: none yet)
@@ -166,7 +171,7 @@ int rb_ctx_create(int device, rb_ctx** out) {
         cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
     }
     cudaGetLastError();
-    if (cudaMallocHost(&c->host_ctr, sizeof(unsigned long long) * (8 + RB_MAX_SLOTS)) != cudaSuccess) {
+    if (cudaMallocHost(&c->host_ctr, sizeof(unsigned long long) * (16 + RB_MAX_SLOTS)) != cudaSuccess) {
         cudaGetLastError();
         c->host_ctr = nullptr;
     }
@@ -949,17 +954,33 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         }
         return items;
     };
-    // a 3-row kernel's 768-row items would leave threads idle on small
-    // partitions: batches whose average part is shorter use a 2-row variant
+    // Kernel variant: a 3-row kernel's 768-row items would leave threads idle
+    // on small partitions (batches whose average part is shorter use a 2-row
+    // variant), and a program whose gate proved useless runs ungated.  The
+    // variants are compiled on first use.
     const JitKernel* jp = &P->jit;
-    if (P->jit.ok && P->jit.rows > 2 && !parts.empty() && total / (int64_t)parts.size() < (int64_t)BLOCK * P->jit.rows) {
-        static std::mutex small_mu;  // programs may be shared by host threads
-        std::lock_guard<std::mutex> lock(small_mu);
-        if (!P->jit_small_tried) {
-            P->jit_small = jit_pair_kernel(P->F, c->device, 2);
-            P->jit_small_tried = true;
+    if (P->jit.ok) {
+        const bool small = P->jit.rows > 2 && !parts.empty() &&
+                           total / (int64_t)parts.size() < (int64_t)BLOCK * P->jit.rows;
+        const bool nogate = P->gate_off && P->jit.gated;
+        if (small || nogate) {
+            static std::mutex variant_mu;  // programs may be shared by host threads
+            std::lock_guard<std::mutex> lock(variant_mu);
+            JitKernel& slot = nogate ? (small ? P->jit_small_nogate : P->jit_nogate) : P->jit_small;
+            bool& tried = nogate ? (small ? P->jit_small_nogate_tried : P->jit_nogate_tried) : P->jit_small_tried;
+            if (!tried) {
+                FilterPlan Fv = P->F;
+                if (nogate) {
+                    Fv.gate = 0;
+                    for (int f = 0; f < MAX_EQ; f++) Fv.eq_stage2[f] = 0;
+                    for (int f = 0; f < MAX_TOK; f++)
+                        for (int z = 0; z < MAX_FSLOTS; z++) Fv.tok_slot[f][z].stage2 = 0;
+                }
+                slot = jit_pair_kernel(Fv, c->device, small ? 2 : 0);
+                tried = true;
+            }
+            if (slot.ok) jp = &slot;
         }
-        if (P->jit_small.ok) jp = &P->jit_small;
     }
     const JitKernel& J = *jp;
     const int64_t rows_per_item = (int64_t)BLOCK * (J.ok ? J.rows : 1);
@@ -982,9 +1003,10 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         if (cudaError_t e = c->refs.grow(sizeof(int32_t) * n, c->stream)) return cleanup(fail(RB_ERR_CUDA, "refs: %s", cudaGetErrorString(e)));
     // counters: [0] item counter (u32, padded), [1] out_count, [2] pairs, [3] survivors, [4..68) slot evals,
     // [68] entries appended to the deferred survivor buffer
-    const size_t n_counters = 6 + RB_MAX_SLOTS;
+    const size_t n_counters = 8 + RB_MAX_SLOTS;
     const size_t SURV = 4 + RB_MAX_SLOTS;
-    const size_t BAD = 5 + RB_MAX_SLOTS;  // set by refs_check_kernel
+    const size_t BAD = 5 + RB_MAX_SLOTS;   // set by refs_check_kernel
+    const size_t GATE = 6 + RB_MAX_SLOTS;  // warp iterations past the stage-1 gate, then all gated iterations
     // deferred verification: buffered survivors up to this many entries (16 B each); a
     // run that needs more falls back to the generic kernel, which decides them in place
     // RB_SURV_LIMIT / RB_SURV_MIN override both bounds (tests drive the retry and fallback paths with them)
@@ -1073,6 +1095,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         R.scratch = (int32_t*)c->scratch.p;
         R.scratch_stride = stride;
         R.surv_count = &ctr[SURV];
+        R.stat_gate = &ctr[GATE];
         const long long per_row = (flags & RB_ENUMERATE) ? std::max(1, P->F.n_rules) : 1;
         // Ranges are sized from the survivors per item seen so far (the
         // program's previous run, else a probe of 1/64 of the items), so a
@@ -1189,6 +1212,9 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             done_surv += surv;
         }
         P->surv_rate = done_items ? (double)done_surv / (double)done_items : -1.0;
+        // a gate that nearly every warp iteration passes only costs its vote:
+        // later runs of this program use the ungated kernel
+        if (J.gated && base[GATE + 1] > 0 && (double)base[GATE] > 0.95 * (double)base[GATE + 1]) P->gate_off = true;
         const long long rows = (long long)base[1];
         res->count = rows;
         res->stats.comparisons = (int64_t)base[2];

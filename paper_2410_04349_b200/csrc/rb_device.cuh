@@ -194,6 +194,7 @@ struct RunParams {
     long long cap;
     unsigned long long* stat_pairs;
     unsigned long long* stat_surv;
+    unsigned long long* stat_gate;  // warp iterations that passed the stage-1 gate (gated kernels)
     unsigned long long* slot_evals;
     int32_t* scratch;
     int64_t scratch_stride;
@@ -821,7 +822,7 @@ template <typename Mask, int ROWS, bool AllValid, bool DEFER>
 __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg& V, const RunParams& R, const Tile& T,
                                           const int32_t* tab, Outer<Mask> (&o)[ROWS], int jj0, int tn, int2* q, int& qn,
                                           int part, const int* cp_rule, int32_t* scratch,
-                                          unsigned long long& my_surv) {
+                                          unsigned long long& my_surv, unsigned& gate_hits, unsigned& gate_iters) {
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << (threadIdx.x & 31)) - 1u;
     const uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tab);
@@ -832,6 +833,9 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
     // any pair let through here is still decided by the exact interpreter.
     Mask all_rules;
     m_init(all_rules, RB_ALL_RULES);
+#endif
+#if RB_GATE
+    gate_iters += (unsigned)(tn - jj0);
 #endif
 #if defined(RB_SPEC) && SPEC_UNROLL > 1
 #pragma unroll SPEC_UNROLL
@@ -937,6 +941,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
 #pragma unroll
             for (int r = 0; r < ROWS; r++) any |= m_any(alive[r]);
             if (!__any_sync(FULL, any)) continue;
+            gate_hits++;
 #pragma unroll
             for (int r = 0; r < ROWS; r++) {
 #pragma unroll
@@ -1032,6 +1037,7 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
     int2* q = queue[warp];
     int qn = 0;
     unsigned long long my_pairs = 0, my_surv = 0;
+    unsigned gate_hits = 0, gate_iters = 0;  // stage-1 gate passes / inner tuples visited (per warp)
     int32_t* scratch = R.scratch + (int64_t)(blockIdx.x * BLOCK + threadIdx.x) * R.scratch_stride;
 
     if (R.bad_refs && *R.bad_refs) return;  // the host reports the bad ref
@@ -1101,10 +1107,11 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
             const int jj0 = __reduce_min_sync(FULL, lo);
             if (jj0 >= tn) continue;
             if (__all_sync(FULL, all_valid))
-                tile_loop<Mask, ROWS, true, DEFER>(F, V, R, T, tab, o, 0, tn, q, qn, part, cp_rule, scratch, my_surv);
+                tile_loop<Mask, ROWS, true, DEFER>(F, V, R, T, tab, o, 0, tn, q, qn, part, cp_rule, scratch, my_surv,
+                                                   gate_hits, gate_iters);
             else
                 tile_loop<Mask, ROWS, false, DEFER>(F, V, R, T, tab, o, jj0, tn, q, qn, part, cp_rule, scratch,
-                                                    my_surv);
+                                                    my_surv, gate_hits, gate_iters);
         }
         if (qn) {
             __syncwarp();
@@ -1126,6 +1133,12 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
     if (lane == 0) {
         atomicAdd(R.stat_pairs, my_pairs);
         atomicAdd(R.stat_surv, my_surv);
+#if RB_GATE
+        if (R.stat_gate) {  // warp-uniform counts
+            atomicAdd(R.stat_gate, (unsigned long long)gate_hits);
+            atomicAdd(R.stat_gate + 1, (unsigned long long)gate_iters);
+        }
+#endif
     }
 }
 

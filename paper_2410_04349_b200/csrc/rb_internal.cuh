@@ -40,6 +40,7 @@ struct JitKernel {
     int blocks_per_sm = 1;
     int rows = 1;  // outer rows per thread
     bool defer = false;  // survivors go to a buffer decided by `verify` (see RunParams::surv)
+    bool gated = false;  // compiled with the stage-1 gate (counts gate passes in RunParams::stat_gate)
     cudaKernel_t verify = nullptr;
     int verify_blocks_per_sm = 1;
     double compile_ms = 0;
