@@ -331,7 +331,7 @@ int rb_relation_add_chars(rb_rel* r, const int64_t* offsets, const void* chars, 
     dc.data = d_chars;
     dc.len = (const int32_t*)d_len;
     dc.bag = (const uint4*)d_bag;
-    return add_column(r, dc, max_len, col);
+    return add_column(r, dc, max_len, col, r->n ? (double)nnz / (double)r->n : 0.0);
 }
 
 int rb_relation_destroy(rb_rel* r) {
@@ -667,6 +667,18 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             if (uses && !earlier) F.str_always[f] = 1;
         }
     }
+    // ---- folded bags: for long strings with tight edit thresholds, buckets i
+    // and i+8 are summed (saturating) -- still a bag-distance lower bound, half
+    // the byte-SAD work per pair, and far above maxd for unrelated strings
+    for (int f = 0; f < F.n_str; f++) {
+        double dmin = 1.0;
+        for (int z = 0; z < F.str_nslots[f]; z++) dmin = std::min(dmin, F.str_slot[f][z].delta);
+        const int s0 = F.str_slot[f][0].slot;
+        const double mean = std::min(rel->mean_len[slots[s0].lhs], rel->mean_len[slots[s0].rhs]);
+        const char* env_fold = std::getenv("RB_FOLD_BAG");
+        F.str_fold[f] = (env_fold ? env_fold[0] == '1' : (mean >= 48.0 && dmin >= 0.9)) ? 1 : 0;
+    }
+
     // ---- implied kills: a failed test also rules out every rule that needs
     // a test implying it.  The threshold tables are monotone in delta, so a
     // Jaccard (edit) slot failing implies every slot on the same feature

@@ -157,6 +157,7 @@ struct FilterPlan {
     uint64_t str_rules[MAX_STR];
     uint64_t str_kill[MAX_STR];  // a missing outer string fails every slot on the feature
     int32_t str_always[MAX_STR];
+    int32_t str_fold[MAX_STR];  // 8-bucket (folded) bags for this string feature
     FSlot str_slot[MAX_STR][MAX_FSLOTS];
 };
 
@@ -534,6 +535,7 @@ struct __align__(16) Tile {
 #define RB_TOK_NJP(f) (RB_TOK_NJ(f) <= 1 ? 1 : RB_TOK_NJ(f) <= 2 ? 2 : 4)
 #define RB_STR_NS(f) ((f) == 0 ? SPEC_STR0_NS : SPEC_STR1_NS)
 #define RB_STR_ALWAYS(f) ((f) == 0 ? SPEC_STR0_ALWAYS : SPEC_STR1_ALWAYS)
+#define RB_STR_FOLD(f) ((f) == 0 ? SPEC_STR0_FOLD : SPEC_STR1_FOLD)
 #define RB_FULLTAB SPEC_FULLTAB
 #define RB_TOK2D SPEC_TOK2D
 // rule masks are compile-time constants too: a failed test becomes one
@@ -568,6 +570,7 @@ struct __align__(16) Tile {
 #define RB_TOK_NJP(f) F.tok_njp[f]
 #define RB_STR_NS(f) F.str_nslots[f]
 #define RB_STR_ALWAYS(f) F.str_always[f]
+#define RB_STR_FOLD(f) F.str_fold[f]
 #define RB_FULLTAB F.full_tab
 #define RB_TOK2D F.tok2d
 #define RB_ALL_RULES F.all_rules
@@ -612,6 +615,13 @@ static __device__ __forceinline__ int str_m2(const int32_t* tab, const FSlot& fs
     if (len < 0) return -1;
     if ((unsigned)len >= (unsigned)fs.cap0) return INT_MAX;
     return tab[off + 2 * len + 1];
+}
+
+// buckets i and i+8 summed with byte saturation (x,y), z = w = 0: the
+// 8-bucket bag; saturation is 1-Lipschitz, so the bag distance of folded
+// bags is still a lower bound of the 16-bucket one
+static __device__ __forceinline__ uint4 fold_bag(uint4 b) {
+    return make_uint4(__vaddus4(b.x, b.z), __vaddus4(b.y, b.w), 0u, 0u);
 }
 
 // sum over the four bytes of |a_i - b_i|, plus c (VABSDIFF4 with accumulate)
@@ -792,6 +802,7 @@ struct Outer {
                 obag[f] = __ldg(F.str_obag[f] + ti);
                 m_kill(alive0, oslen[f] < 0, RB_STR_ROWKILL(f));  // missing t side: edit is false
                 if (oslen[f] < 0) obag[f] = make_uint4(0, 0, 0, 0);  // with gap = |s| + 1 the bag bound fails on its own
+                if (RB_STR_FOLD(f)) obag[f] = fold_bag(obag[f]);
 #pragma unroll
                 for (int z = 0; z < MAX_FSLOTS; z++)
                     if (z < RB_STR_NS(f)) om2[f][z] = str_m2(tab, F.str_slot[f][z], RB_STR_OFF(f, z), oslen[f]);
@@ -980,11 +991,9 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                 // t = bag distance + |la - lb| in five accumulating SAD steps;
                 // lev <= maxd[L] implies t <= 2*maxd[L] <= max(2*maxd[la], 2*maxd[lb])
                 // (L is one of la, lb), so no max, no table lookup per pair
-                const int t = (int)vsad4_acc(o[r].obag[f].w, ib.w,
-                                             vsad4_acc(o[r].obag[f].z, ib.z,
-                                                       vsad4_acc(o[r].obag[f].y, ib.y,
-                                                                 vsad4_acc(o[r].obag[f].x, ib.x,
-                                                                           __sad(la, lb, 0u)))));
+                const uint32_t t2 = vsad4_acc(o[r].obag[f].y, ib.y, vsad4_acc(o[r].obag[f].x, ib.x, __sad(la, lb, 0u)));
+                const int t = RB_STR_FOLD(f) ? (int)t2
+                                             : (int)vsad4_acc(o[r].obag[f].w, ib.w, vsad4_acc(o[r].obag[f].z, ib.z, t2));
 #pragma unroll
                 for (int z = 0; z < MAX_FSLOTS; z++) {
                     if (z < RB_STR_NS(f)) {
@@ -1087,7 +1096,8 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
                     if (f < RB_NSTR) {
                         const int lb = __ldg(F.str_ilen[f] + sj);
                         T.r[k].strlen_[f] = lb;
-                        T.r[k].strbag[f] = __ldg(F.str_ibag[f] + sj);
+                        const uint4 bg = __ldg(F.str_ibag[f] + sj);
+                        T.r[k].strbag[f] = RB_STR_FOLD(f) ? fold_bag(bg) : bg;
 #pragma unroll
                         for (int z = 0; z < MAX_FSLOTS; z++)
                             if (z < RB_STR_NS(f)) T.r[k].strm2[f][z] = str_m2(tab, F.str_slot[f][z], RB_STR_OFF(f, z), lb);

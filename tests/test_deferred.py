@@ -100,3 +100,45 @@ def test_batched_output_growth_keeps_parts(monkeypatch):
     monkeypatch.setenv("RB_OUT_MIN", "2")
     got = [cs.sorted_pairs() for cs in run_partitions(parts, rel, path)]
     assert got == want and sum(map(len, want)) > 10
+
+
+@pytest.mark.gpu
+def test_useless_gate_switches_off_and_stays_exact(monkeypatch):
+    """Stage-1 equality key that every pair passes (a constant column): after
+    the first run the program switches to its ungated variant; every run must
+    match the oracle."""
+    import json
+    import random
+
+    from paper_2410_04349_b200 import EngineConfig
+    from paper_2410_04349_b200.engine import PathProgram, _encoding_for
+    from paper_2410_04349_b200.plan import plan_from_stats
+    from paper_2410_04349_b200.relation import relation_from_rows
+    from paper_2410_04349_b200.rules import parse_ruleset, predicate_universe
+
+    monkeypatch.delenv("RB_JIT", raising=False)
+    monkeypatch.delenv("RB_GATE", raising=False)
+    rng = random.Random(3)
+    words = ["alpha", "beta", "gamma", "delta", "eps", "zeta", "eta", "theta"]
+    rows = [["k", " ".join(rng.choices(words, k=rng.randint(2, 6))), "".join(rng.choices("abc", k=rng.randint(3, 9))),
+             f"z{rng.randrange(3)}"] for _ in range(900)]
+    rel = relation_from_rows(["blk", "title", "name", "zip"], ["short_text", "long_text", "short_text", "short_text"],
+                             rows)
+    rules = parse_ruleset(json.dumps([
+        {"id": "A", "when": [{"t_attr": "blk", "op": "eq", "s_attr": "blk"},
+                             {"t_attr": "title", "op": "sim", "s_attr": "title", "measure": "jaccard",
+                              "threshold": 0.6}]},
+        {"id": "B", "when": [{"t_attr": "blk", "op": "eq", "s_attr": "blk"},
+                             {"t_attr": "zip", "op": "eq", "s_attr": "zip"},
+                             {"t_attr": "name", "op": "sim", "s_attr": "name", "measure": "edit", "threshold": 0.7}]}]))
+    uni = predicate_universe(rules)
+    path = plan_from_stats(rules, {p: (0.1 if p.comparator == "eq" else 1.0) for p in uni}, {p: 0.5 for p in uni})
+    enc = _encoding_for(rel, None)
+    enc.prepare(path.predicate_table)
+    prog = PathProgram(path, enc)
+    case = {"symmetric": True, "enumerate": False, "refs": None, "left": None, "right": None}
+    want, cmp = goldens.oracle_rows(rel, path, case)
+    for _ in range(3):
+        cs = run_partition(DataPartition(0, tuple(range(len(rel)))), rel, path, EngineConfig(), program=prog)
+        assert sorted(cs.pairs) == want and cs.stats.total_comparisons() == cmp
+    assert len(want) > 0

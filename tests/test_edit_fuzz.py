@@ -58,7 +58,13 @@ def make(seed, n=160, unicode=False):
 @pytest.mark.gpu
 @pytest.mark.parametrize("seed", range(10))
 @pytest.mark.parametrize("unicode", [False, True])
-def test_edit_distance_gpu_vs_oracle(seed, unicode):
+@pytest.mark.parametrize("fold", ["auto", "1"])
+def test_edit_distance_gpu_vs_oracle(seed, unicode, fold, monkeypatch):
+    """fold=1 forces the 8-bucket (folded) bag filter on every string feature."""
+    if fold == "auto":
+        monkeypatch.delenv("RB_FOLD_BAG", raising=False)
+    else:
+        monkeypatch.setenv("RB_FOLD_BAG", fold)
     rel, path = make(seed, unicode=unicode)
     refs = list(range(len(rel)))
     random.Random(seed).shuffle(refs)
