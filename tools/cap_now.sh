@@ -1,5 +1,4 @@
 set -x
-timeout 1500 python -m pytest tests/ -q -m gpu -x 2>&1 | tail -25 > gpurun_out/gpu_tests.log; tail -2 gpurun_out/gpu_tests.log
-bash tools/gpu_perf.sh s28
-bash tools/gpu_variants.sh var28 edit_heavy "RB_FOLD_BAG=0"
-bash tools/gpu_variants.sh var28 linkage "RB_FOLD_BAG=1"
+timeout 900 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err; tail -1 gpurun_out/final_bench.json | cut -c1-200
+bash profiles/capture.sh r1s29c citation3 1000000 2024
+bash profiles/capture.sh r1s29e edit_heavy 1000000 11
