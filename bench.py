@@ -499,6 +499,16 @@ def main():
             got = sorted(zip(gt.tolist(), gs.tolist(), gr.tolist()))
             ok &= want == got
         parity = {"rows_checked": int(len(orc_rows)), "pairs_checked": int(orc_pairs), "bit_exact": bool(ok)}
+        # every row of the last timed step: a true match (refs = identity, so t is the
+        # lower tid), carrying the oracle's first witness, no pair twice
+        from oracle import oracle as _orc
+
+        at, as_, ar = (np.asarray(x) for x in rows)
+        wit = _orc.witness(w.enc, prog.program, at, as_, nthreads=cores)
+        key = at.astype(np.int64) * w.n + as_
+        parity["all_step_rows"] = {"rows": int(len(at)), "witness_exact": bool((wit == ar).all()),
+                                   "ordered": bool((at < as_).all()), "distinct": bool(len(np.unique(key)) == len(key)),
+                                   "check": "oracle.witness on every emitted (t, s): rule == oracle first witness"}
         bpp, terms = algorithmic_bytes_per_pair(w.enc, w.path, orc_evals / max(1, orc_pairs), n_rows / pairs_step)
         k_ms = float(np.mean(kms))
         achieved = bpp * pairs_step / (k_ms / 1e3) / 1e9

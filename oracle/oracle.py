@@ -47,6 +47,13 @@ def lib():
             build()
         L = ctypes.CDLL(LIB_PATH)
         L.orc_slot_size.restype = ctypes.c_int32
+        L.orc_witness_pairs.restype = None
+        L.orc_witness_pairs.argtypes = [
+            ctypes.c_void_p,
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+            ctypes.c_void_p, ctypes.c_int32,
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+        ]
         L.orc_run.restype = ctypes.c_int64
         L.orc_run.argtypes = [
             ctypes.c_void_p, ctypes.c_int32,
@@ -63,6 +70,37 @@ def lib():
 
 def _ptr(a):
     return None if a is None else a.ctypes.data
+
+
+def _columns(enc):
+    keep = []
+    cols = (OrcColumn * max(1, len(enc.columns)))()
+    for k, c in enumerate(enc.columns):
+        data = np.ascontiguousarray(c.data)
+        offs = None if c.offsets is None else np.ascontiguousarray(c.offsets, dtype=np.int64)
+        miss = None if c.missing is None else np.ascontiguousarray(c.missing, dtype=np.uint8)
+        keep += [data, offs, miss]
+        cols[k].kind = c.kind
+        cols[k].width = c.width
+        cols[k].data = _ptr(data)
+        cols[k].offsets = _ptr(offs)
+        cols[k].missing = _ptr(miss)
+    return cols, keep
+
+
+def witness(enc, prog, t, s, *, nthreads=0):
+    """Rule of the first checkpoint each pair (t[k], s[k]) reaches, evaluated
+    t-then-s (engine.py:531-559, first witness); -1 where no rule holds."""
+    L = lib()
+    cols, keep = _columns(enc)
+    t = np.ascontiguousarray(t, dtype=np.int32)
+    s = np.ascontiguousarray(s, dtype=np.int32)
+    out = np.empty(len(t), dtype=np.int32)
+    slots = np.ascontiguousarray(prog.slots)
+    L.orc_witness_pairs(cols, _ptr(prog.ins_op), _ptr(prog.ins_slot), _ptr(prog.ins_fail), _ptr(prog.ins_rule),
+                        len(prog.ins_op), _ptr(slots), prog.n_slots, _ptr(t), _ptr(s), len(t), nthreads, _ptr(out))
+    del keep
+    return out
 
 
 def run(enc, prog, refs, n, *, split=-1, row_lo=0, row_hi=None, flags=1, nthreads=0):

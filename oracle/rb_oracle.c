@@ -257,6 +257,38 @@ int64_t orc_run(const orc_column* cols, int32_t n_cols, const int32_t* op, const
     return out.count;
 }
 
+/*
+ * Witness of each given pair (t[k], s[k]) in evaluation order t-then-s:
+ * rule_out[k] = the rule of the first checkpoint reached (engine.py:531-559,
+ * not enumerating), -1 when no rule holds.  Used to check every row a device
+ * run emitted (the caller passes t = lower position).
+ */
+void orc_witness_pairs(const orc_column* cols, const int32_t* op, const int32_t* slot, const int32_t* fail,
+                       const int32_t* rule, int32_t n_ins, const rb_slot* slots, int32_t n_slots, const int32_t* t,
+                       const int32_t* s, int64_t n_pairs, int32_t nthreads, int32_t* rule_out) {
+    orc_prog P = {cols, op, slot, fail, rule, n_ins, slots, n_slots};
+    if (nthreads > 0) {
+#ifdef _OPENMP
+        extern void omp_set_num_threads(int);
+        omp_set_num_threads(nthreads);
+#endif
+    }
+#pragma omp parallel
+    {
+        int64_t evals[RB_MAX_SLOTS] = {0};
+        scratch sc = {NULL, NULL, 0};
+        int32_t one_t, one_s, one_r;
+#pragma omp for schedule(dynamic, 256)
+        for (int64_t k = 0; k < n_pairs; k++) {
+            sink out = {&one_t, &one_s, &one_r, 1, 0};
+            walk_pair(&P, t[k], s[k], 0u, &out, evals, &sc);
+            rule_out[k] = out.count ? one_r : -1;
+        }
+        free(sc.prev);
+        free(sc.cur);
+    }
+}
+
 /* struct layout check for the ctypes mirror */
 int32_t orc_slot_size(void) { return (int32_t)sizeof(rb_slot); }
 int32_t orc_column_size(void) { return (int32_t)sizeof(orc_column); }

@@ -1,4 +1,3 @@
 set -x
-timeout 900 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err; tail -1 gpurun_out/final_bench.json | cut -c1-200
-bash profiles/capture.sh r1s29c citation3 1000000 2024
-bash profiles/capture.sh r1s29e edit_heavy 1000000 11
+timeout 900 python bench.py > gpurun_out/bench_full_parity.json 2> gpurun_out/bench_full_parity.err
+tail -1 gpurun_out/bench_full_parity.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], json.dumps(d['parity']))"
