@@ -44,6 +44,9 @@ WORKLOAD_DESC = {
     "linkage": "BASELINE config 5: two-table linkage, Zipf(1.3) blocks, one cross run per block, batched",
     "citation3_parts": "config 2 relation in 512-tuple partitions (the reference pipeline's default), batched",
     "citation_small": "BASELINE config 1: the reference's citation_benchmark (4,591 tuples) with its frozen plan",
+    "person5": "BASELINE config 4 (ii): person relation, 5 rules, data-aware plan, one partition",
+    "person5_parts": "BASELINE config 4 (i): person relation, 5 rules, the pipeline's plan-derived partitions "
+                     "(max_partition_size 65536) plus sibling pulls, batched",
 }
 UNIT = "pairs/s"
 
@@ -192,6 +195,31 @@ def sample_rows(n, budget_pairs, k=8):
     return out
 
 
+def ncu_capture(w, pairs_step):
+    """(dram bytes per launch, pipe utilisation) of the committed ncu capture
+    of this workload at this size (profiles/traffic.json), or (None, None)."""
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    pipe = None
+    if os.path.exists(tfile):
+        try:  # ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, same workload and size
+            entry = json.load(open(tfile)).get(w.name, {})
+            if entry.get("n") == w.n:
+                traffic = entry.get("bytes_per_launch")
+                m = entry.get("metrics", {})
+                pipe = {k: float(m[k]["value"]) for k in (
+                    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+                    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+                    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                    "smsp__issue_active.avg.pct_of_peak_sustained_active") if k in m}
+                if "smsp__inst_executed.sum" in m:  # the per-pair instruction cost of the capture
+                    pipe["warp_instructions_per_pair"] = float(m["smsp__inst_executed.sum"]["value"]) / pairs_step
+                pipe["source"] = entry.get("capture")
+        except Exception:
+            traffic = None
+    return traffic, pipe
+
+
 def blocks_cpu_parity(w, prog, budget, kms, pairs_step, n_rows):
     """Block workloads: oracle on a seeded sample of whole blocks (CPU
     baseline), the same blocks re-run on the GPU for bit-exact parity."""
@@ -233,8 +261,9 @@ def blocks_cpu_parity(w, prog, budget, kms, pairs_step, n_rows):
     bpp, terms = algorithmic_bytes_per_pair(w.enc, w.path, evals / max(1, cmp_total), n_rows / max(1, pairs_step))
     k_ms = float(np.mean(kms))
     achieved = bpp * pairs_step / (k_ms / 1e3) / 1e9
+    traffic, pipe = ncu_capture(w, pairs_step)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "peak_kind": peak_kind, "bytes_per_pair": bpp, "kernel_ms": k_ms, "terms": terms,
+            "traffic": traffic, "ncu_pipes": pipe, "peak_kind": peak_kind, "bytes_per_pair": bpp, "kernel_ms": k_ms, "terms": terms,
             "model": "SURVEY 8d streaming bytes: sum_s E_s*b_s + 10 B per row; E_s from oracle first-touch counts"}
     return cpu, parity, roof
 
@@ -512,25 +541,7 @@ def main():
         bpp, terms = algorithmic_bytes_per_pair(w.enc, w.path, orc_evals / max(1, orc_pairs), n_rows / pairs_step)
         k_ms = float(np.mean(kms))
         achieved = bpp * pairs_step / (k_ms / 1e3) / 1e9
-        traffic = None
-        tfile = os.path.join(ROOT, "profiles", "traffic.json")
-        pipe = None
-        if os.path.exists(tfile):
-            try:  # ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, same workload and size
-                entry = json.load(open(tfile)).get(w.name, {})
-                if entry.get("n") == w.n:
-                    traffic = entry.get("bytes_per_launch")
-                    m = entry.get("metrics", {})
-                    pipe = {k: float(m[k]["value"]) for k in (
-                        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
-                        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
-                        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
-                        "smsp__issue_active.avg.pct_of_peak_sustained_active") if k in m}
-                    if "smsp__inst_executed.sum" in m:  # the per-pair instruction cost of the capture
-                        pipe["warp_instructions_per_pair"] = float(m["smsp__inst_executed.sum"]["value"]) / pairs_step
-                    pipe["source"] = entry.get("capture")
-            except Exception:
-                traffic = None
+        traffic, pipe = ncu_capture(w, pairs_step)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_kind": peak_kind,
                 "true_bound": "integer pipes: XU (POPC) and ALU issue (inner tuples are reused from shared "

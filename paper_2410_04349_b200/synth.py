@@ -442,6 +442,50 @@ def citation3_parts(n: int = 1_000_000, seed: int = 2024, part: int = 512) -> Wo
     return w
 
 
+def plan_partitions(enc: Encoded, path, max_partition_size: int = 65536) -> list:
+    """The reference pipeline's partitions and sibling pulls for a plan whose
+    root edges are all same-attribute equalities (iter_partitions,
+    partitioning.py:93-131; sibling_pull_pairs, 144-157), from the encoded
+    code columns: one branch per root edge, one partition per distinct key
+    (tids ascending; missing values form their own key group, as the
+    reference's MISSING_KEY), a group above ``max_partition_size`` dealt
+    round-robin into ceil(|g| / max) siblings, and every sibling pair pulled
+    as a cross block.  Returns [(refs int32, split)] with split = -1 for a
+    partition and |left| for a pull; single-tuple partitions (no pairs) are
+    dropped as pipeline_run drops them in symmetric mode."""
+    from .pipeline import root_predicates
+
+    blocks = []
+    for pred in root_predicates(path):
+        if pred.comparator != "eq" or pred.is_cross_attr:
+            raise ValueError(f"plan_partitions handles equality roots only, not {pred.describe()}")
+        codes = enc.columns[enc.get(("codes", pred.lhs_attr))].data
+        order = np.argsort(codes, kind="stable")  # tids ascending inside each key
+        sc = codes[order]
+        cuts = np.flatnonzero(sc[1:] != sc[:-1]) + 1
+        for g in np.split(order.astype(np.int32), cuts):
+            if len(g) <= max_partition_size:
+                if len(g) > 1:
+                    blocks.append((g, -1))
+                continue
+            k = -(-len(g) // max_partition_size)
+            subs = [g[i::k] for i in range(k)]
+            blocks += [(x, -1) for x in subs if len(x) > 1]
+            blocks += [(np.concatenate([subs[i], subs[j]]), len(subs[i])) for i in range(k) for j in range(i + 1, k)]
+    return blocks
+
+
+def person5_parts(n: int = 1_000_000, seed: int = 4, max_partition_size: int = 65536) -> Workload:
+    """BASELINE config 4 (i): person5's relation and frozen plan, evaluated
+    over the reference pipeline's plan-derived partitions (one branch per
+    equality root, max_partition_size = 65536) plus sibling pulls, in one
+    batched launch."""
+    w = person5(n, seed)
+    w.blocks = plan_partitions(w.enc, w.path, max_partition_size)
+    w.name = "person5_parts"
+    return w
+
+
 def citation_small(n: int = 0, seed: int = 2024) -> Workload:
     """BASELINE config 1: the reference's own small benchmark relation --
     ``citation_benchmark(seed=2024)`` (datasets.py:332-398, 4,591 tuples)
@@ -467,4 +511,5 @@ def citation_small(n: int = 0, seed: int = 2024) -> Workload:
 
 
 WORKLOADS = {"citation3": citation3, "edit_heavy": edit_heavy, "linkage": linkage, "person5": person5,
-             "citation3_parts": citation3_parts, "citation_small": citation_small}
+             "citation3_parts": citation3_parts, "citation_small": citation_small,
+             "person5_parts": person5_parts}

@@ -58,3 +58,36 @@ def test_collect_keeps_earliest_rule_per_pair():
     b = CandidateSet(arrays=(np.array([1, 4]), np.array([5, 7]), np.array([1, 2])), rule_ids=["a", "b", "c"])
     cs = collect([a, b], ["a", "b", "c"])
     assert sorted(cs.pairs) == [(1, 5, "a"), (2, 3, "b"), (4, 7, "c")]
+
+
+@pytest.mark.parametrize("max_size", [2, 5, 64])
+def test_plan_partitions_equal_pipeline(max_size):
+    """synth.plan_partitions (the config 4 (i) bench blocks, from encoded code
+    columns) yields exactly pipeline_run's partitions and sibling pulls."""
+    import random
+
+    from paper_2410_04349_b200.encode import RelationEncoding
+    from paper_2410_04349_b200.plan import plan_from_stats
+    from paper_2410_04349_b200.relation import MISSING, relation_from_rows
+    from paper_2410_04349_b200.rules import parse_ruleset, predicate_universe
+    from paper_2410_04349_b200.synth import plan_partitions
+
+    rng = random.Random(max_size)
+    rows = [[rng.choice(["x", " x", "y", "z ", MISSING]), float(rng.randint(0, 3)), rng.choice(["ab", "abc", "b"])]
+            for _ in range(120)]
+    rel = relation_from_rows(["k", "n", "s"], ["short_text", "numeric", "short_text"], rows)
+    doc = [{"id": "a", "when": [{"t_attr": "k", "op": "eq", "s_attr": "k"},
+                               {"t_attr": "s", "op": "sim", "s_attr": "s", "measure": "edit", "threshold": 0.6}]},
+           {"id": "b", "when": [{"t_attr": "n", "op": "eq", "s_attr": "n"}]}]
+    rules = parse_ruleset(json.dumps(doc))
+    uni = predicate_universe(rules)
+    path = plan_from_stats(rules, {p: 1.0 for p in uni}, {p: 0.5 for p in uni})
+    enc = RelationEncoding(rel).prepare(path.predicate_table)
+    parts = list(iter_partitions(rel, path, max_size))
+    by = {p.pid: p for p in parts}
+    want = [(tuple(p.tuple_refs), -1) for p in parts if len(p.tuple_refs) > 1]
+    want += [(tuple(by[a].tuple_refs) + tuple(by[b].tuple_refs), len(by[a].tuple_refs))
+             for a, b in sibling_pull_pairs(parts)]
+    got = [(tuple(int(x) for x in r), int(sp)) for r, sp in plan_partitions(enc, path, max_size)]
+    assert sorted(got) == sorted(want)
+    assert any(sp >= 0 for _, sp in got) == (max_size < 40)
