@@ -1,7 +1,9 @@
 set -x
-timeout 900 python bench.py --workload person5_parts > gpurun_out/bench_p5parts.json 2> gpurun_out/bench_p5parts.err
-tail -1 gpurun_out/bench_p5parts.json | cut -c1-1500
-tail -5 gpurun_out/bench_p5parts.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/p5parts_launches.csv timeout 600 python bench.py --workload person5_parts --steps 1 --warmup 3 --no-cpu --e2e-steps 1 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:rb_pair_kernel_spec -s 3 -c 1 -o gpurun_out/p5parts_full timeout 900 python bench.py --workload person5_parts --steps 1 --warmup 3 --no-cpu --e2e-steps 1 > /dev/null 2>&1
-ls gpurun_out
+mkdir -p gpurun_out/final
+timeout 1500 python -m pytest tests/ -q -m gpu > gpurun_out/final/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/final/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.log 2>&1; echo "smoke rc=$?"
+for wl in citation3 edit_heavy person5 person5_parts linkage citation3_parts citation_small; do
+  timeout 900 python bench.py --workload $wl > gpurun_out/final/$wl.json 2> gpurun_out/final/$wl.err
+  echo "$wl rc=$? $(tail -1 gpurun_out/final/$wl.json | cut -c1-200)"
+done
+timeout 900 python bench.py --impl reference > gpurun_out/final/reference_arm.json 2> gpurun_out/final/reference_arm.err; echo "ref rc=$?"
