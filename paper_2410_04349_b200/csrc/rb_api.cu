@@ -11,11 +11,13 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -76,6 +78,42 @@ struct DevBuf {
     }
 };
 
+// Growable array in pinned host memory: the work items are built straight
+// into it and copied to the device asynchronously at full link speed (a
+// batch of many small partitions has one item per partition).  Reused by
+// every run on the context; a run synchronises its stream before returning,
+// so the buffer is never overwritten under an in-flight copy.
+template <typename T>
+struct PinnedVec {
+    T* p = nullptr;
+    size_t n = 0, cap = 0;
+    bool failed = false;
+    void clear() { n = 0; }
+    void push_back(const T& v) {
+        if (n == cap && !grow(cap ? 2 * cap : 4096)) return;
+        p[n++] = v;
+    }
+    bool grow(size_t want) {
+        T* q = nullptr;
+        if (cudaMallocHost((void**)&q, sizeof(T) * want) != cudaSuccess) {
+            failed = true;
+            return false;
+        }
+        if (n) std::memcpy(q, p, sizeof(T) * n);
+        if (p) cudaFreeHost(p);
+        p = q;
+        cap = want;
+        return true;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = cap = 0;
+    }
+    size_t size() const { return n; }
+    const T* data() const { return p; }
+};
+
 }  // namespace
 
 struct rb_ctx {
@@ -90,6 +128,7 @@ struct rb_ctx {
     int32_t* pool[3] = {nullptr, nullptr, nullptr};
     long long pool_cap = 0;
     unsigned long long* host_ctr = nullptr;  // pinned: counters read back after each run
+    PinnedVec<Item> host_items;              // the last run's work items
 };
 
 struct rb_rel {
@@ -203,6 +242,7 @@ int rb_ctx_destroy(rb_ctx* c) {
     for (int k = 0; k < 3; k++) dev_free(c->pool[k], c->stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->host_ctr) cudaFreeHost(c->host_ctr);
+    c->host_items.release();
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return RB_OK;
@@ -907,6 +947,11 @@ struct Part {
     int64_t base, n, split;  // split < 0: a partition; else cross, left = [base, base+split)
 };
 
+// RB_HOST_TIMING=1: host-side phase times of every run on stderr (diagnostics)
+static double host_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
                int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out) {
     if (!c || !rel || !P || !out) return fail(RB_ERR_INVALID, "run: null argument");
@@ -926,6 +971,18 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         return fail(RB_ERR_INVALID, "identity partition of %lld tuples exceeds the relation", (long long)total);
     }
     *out = nullptr;
+    static const bool timing = std::getenv("RB_HOST_TIMING") != nullptr;
+    double tm[8] = {timing ? host_ms() : 0};
+    int ntm = 1;
+    auto mark = [&]() {
+        if (timing && ntm < 8) tm[ntm++] = host_ms();
+    };
+    auto report = [&]() {
+        if (!timing) return;
+        fprintf(stderr, "rb run: parts %zu items %zu |", parts.size(), (size_t)c->host_items.size());
+        for (int k = 1; k < ntm; k++) fprintf(stderr, " %.3f", tm[k] - tm[k - 1]);
+        fprintf(stderr, " ms\n");
+    };
     CK(cudaSetDevice(c->device));
     rb_result* res = new (std::nothrow) rb_result();
     if (!res) return fail(RB_ERR_OOM, "host allocation failed");
@@ -940,9 +997,11 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     };
 
     // ---- work items: BLOCK * rows outer rows x `chunk` inner columns, per part
-    auto build_items = [&](int64_t rows_per_item, int64_t chunk) {
-        std::vector<Item> items;
-        for (size_t pi = 0; pi < parts.size(); pi++) {
+    PinnedVec<Item>& items = c->host_items;
+    // the items of parts [p0, p1), written at `at` (when non-null); returns their count
+    auto part_items = [&](size_t p0, size_t p1, int64_t rows_per_item, int64_t chunk, Item* at) {
+        size_t k = 0;
+        for (size_t pi = p0; pi < p1; pi++) {
             const Part& pt = parts[pi];
             const bool cross = pt.split >= 0;
             const int32_t mode = cross ? MODE_CROSS : ((flags & RB_SYMMETRIC) ? MODE_SYM : MODE_ASYM);
@@ -952,19 +1011,45 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             for (int64_t r0 = rlo; r0 < rhi; r0 += rows_per_item) {
                 const int64_t rend = std::min<int64_t>(r0 + rows_per_item, rhi);
                 int64_t c0 = cross ? pt.base + pt.split : (mode == MODE_SYM ? r0 + 1 : pt.base);
-                for (; c0 < end; c0 += chunk) {
-                    Item it{};
+                for (; c0 < end; c0 += chunk, k++) {
+                    if (!at) continue;
+                    Item& it = at[k];
                     it.row0 = (int32_t)r0;
                     it.col0 = (int32_t)c0;
                     it.col1 = (int32_t)std::min<int64_t>(c0 + chunk, end);
                     it.row_hi = (int32_t)rend;
                     it.mode = mode;
                     it.part = (int32_t)pi;
-                    items.push_back(it);
+                    it.pad0 = it.pad1 = 0;
                 }
             }
         }
-        return items;
+        return k;
+    };
+    // A batch of many parts (one item or more each) is laid out by several
+    // host threads: count per part range, then fill at the ranges' offsets
+    // (same order as one thread).  Writing ~10^5 items is memory-bound work.
+    const char* env_par = std::getenv("RB_ITEM_THREADS_MIN");
+    const size_t par_min = env_par ? (size_t)std::max(1ll, std::atoll(env_par)) : 16384;
+    auto build_items = [&](int64_t rows_per_item, int64_t chunk) {
+        items.clear();
+        const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+        const size_t nt = parts.size() >= par_min ? std::min<size_t>(hw, parts.size()) : 1;
+        std::vector<size_t> cut(nt + 1), off(nt + 1, 0);
+        for (size_t t = 0; t <= nt; t++) cut[t] = parts.size() * t / nt;
+        std::vector<std::thread> pool;
+        std::vector<size_t> cnt(nt, 0);
+        auto run_all = [&](auto&& fn) {
+            pool.clear();
+            for (size_t t = 1; t < nt; t++) pool.emplace_back(fn, t);
+            fn(0);
+            for (auto& th : pool) th.join();
+        };
+        run_all([&](size_t t) { cnt[t] = part_items(cut[t], cut[t + 1], rows_per_item, chunk, nullptr); });
+        for (size_t t = 0; t < nt; t++) off[t + 1] = off[t] + cnt[t];
+        if (off[nt] > items.cap && !items.grow(std::max(off[nt], 2 * items.cap))) return;
+        run_all([&](size_t t) { part_items(cut[t], cut[t + 1], rows_per_item, chunk, items.p + off[t]); });
+        items.n = off[nt];
     };
     // Kernel variant: a 3-row kernel's 768-row items would leave threads idle
     // on small partitions (batches whose average part is shorter use a 2-row
@@ -996,12 +1081,17 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     }
     const JitKernel& J = *jp;
     const int64_t rows_per_item = (int64_t)BLOCK * (J.ok ? J.rows : 1);
-    std::vector<Item> items = build_items(rows_per_item, CHUNK);
+    mark();  // [1] variant selection
+    build_items(rows_per_item, CHUNK);
     {
         // small runs: narrower column chunks until every CTA has work (down to one tile)
         const size_t target = 2 * (size_t)c->sm_count * (size_t)(J.ok ? J.blocks_per_sm : c->blocks_per_sm);
         for (int64_t chunk = CHUNK / 2; items.size() < target && chunk >= TJ; chunk /= 2)
-            items = build_items(rows_per_item, chunk);
+            build_items(rows_per_item, chunk);
+    }
+    if (items.failed) {
+        items.failed = false;
+        return cleanup(fail(RB_ERR_OOM, "pinned host buffer for %zu work items", items.size() + 1));
     }
     int n_items = (int)items.size();
     const int64_t n = total;
@@ -1049,6 +1139,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
                                 (long long)(sizeof(int32_t) * stride * slices), cudaGetErrorString(e)));
     }
 
+    mark();  // [2] items built, device buffers sized
     CK(cudaMemcpyAsync(c->items.p, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice, c->stream));
     if (refs) CK(cudaMemcpyAsync(c->refs.p, refs, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
 
@@ -1165,6 +1256,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             res->stats.kernel_ms += pms;
             res->stats.launches += 1;
             const long long surv = (long long)host_ctr[SURV];
+            mark();  // [3] (first range) pair kernel done
             if (surv > scap) {  // roll this range back, then retry it with room or in halves
                 retries++;
                 CK(cudaMemcpyAsync(ctr, base.data(), sizeof(unsigned long long) * n_counters, cudaMemcpyHostToDevice,
@@ -1237,6 +1329,8 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         res->stats.jit_compile_ms = J.compile_ms;
         P->last_rows = rows;
         for (int s = 0; s < RB_MAX_SLOTS; s++) res->stats.slot_evals[s] = (int64_t)base[4 + s];
+        mark();  // verify done
+        report();
         *out = res;
         return RB_OK;
     }

@@ -142,3 +142,31 @@ def test_useless_gate_switches_off_and_stays_exact(monkeypatch):
         cs = run_partition(DataPartition(0, tuple(range(len(rel)))), rel, path, EngineConfig(), program=prog)
         assert sorted(cs.pairs) == want and cs.stats.total_comparisons() == cmp
     assert len(want) > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("symmetric", [True, False])
+def test_many_part_batch_items_built_by_threads(symmetric, monkeypatch):
+    """A batch of many partitions has its work items laid out by several
+    host threads (forced here for any size with RB_ITEM_THREADS_MIN=1): the
+    rows of every partition equal its own single run."""
+    import random
+
+    from paper_2410_04349_b200 import run_partitions
+
+    monkeypatch.delenv("RB_JIT", raising=False)
+    rel, path, _ = goldens.load("citation")
+    rng = random.Random(7)
+    parts, k = [], 0
+    while len(parts) < 300:
+        size = rng.choice([1, 2, 3, 5, 9, 17, 40, 130, 700, 1300])
+        refs = rng.sample(range(len(rel)), size)
+        parts.append(DataPartition(k, tuple(refs)))
+        k += 1
+    cfg = EngineConfig(symmetric_mode=symmetric)
+    want = [run_partition(p, rel, path, cfg).sorted_pairs() for p in parts]
+    for threads_min in ("1", "1000000"):
+        monkeypatch.setenv("RB_ITEM_THREADS_MIN", threads_min)
+        got = [cs.sorted_pairs() for cs in run_partitions(parts, rel, path, cfg)]
+        assert got == want
+    assert sum(map(len, want)) > 50
