@@ -122,7 +122,7 @@ struct rb_ctx {
     bool own_stream = false;
     int sm_count = 0;
     int blocks_per_sm = 1;
-    DevBuf items, refs, counters, scratch, surv;
+    DevBuf items, refs, counters, scratch, surv, offs;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr;
     // output buffers of the last destroyed result, reused by the next run
     int32_t* pool[3] = {nullptr, nullptr, nullptr};
@@ -157,6 +157,8 @@ struct rb_prog {
     // every warp iteration (its tests never fail inside these partitions)
     JitKernel jit_nogate, jit_small_nogate;
     bool jit_nogate_tried = false, jit_small_nogate_tried = false;
+    JitKernel jit_packed;  // 2-row variant taking packed items: batches of tiny partitions
+    bool jit_packed_tried = false;
     bool gate_off = false;
     long long last_rows = 0;  // output size of the previous run: sizes the next buffer
     long long last_surv = 0;  // survivors of the previous run: sizes the deferred-verification buffer
@@ -236,6 +238,7 @@ int rb_ctx_destroy(rb_ctx* c) {
     c->counters.release(c->stream);
     c->scratch.release(c->stream);
     c->surv.release(c->stream);
+    c->offs.release(c->stream);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->ev_mid) cudaEventDestroy(c->ev_mid);
@@ -1031,7 +1034,48 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     // (same order as one thread).  Writing ~10^5 items is memory-bound work.
     const char* env_par = std::getenv("RB_ITEM_THREADS_MIN");
     const size_t par_min = env_par ? (size_t)std::max(1ll, std::atoll(env_par)) : 16384;
+    // packed variant: runs of tiny symmetric partitions share items, larger parts get their own
+    bool packed_items = false;
+    const char* env_pack = std::getenv("RB_PACK_MAX");
+    const int64_t pack_max = env_pack ? std::atoll(env_pack) : 64;
+    auto build_packed = [&](int64_t rows_per_item, int64_t chunk) {
+        items.clear();
+        size_t first = 0, n_in = 0;  // the open pack: parts [first, first + n_in)
+        int64_t rows = 0;
+        auto close = [&]() {
+            if (!n_in) return;
+            const Part& a = parts[first];
+            const Part& b = parts[first + n_in - 1];
+            Item it{};
+            it.row0 = (int32_t)a.base;
+            it.col0 = (int32_t)(a.base + 1);
+            it.col1 = it.row_hi = (int32_t)(b.base + b.n);
+            it.mode = MODE_PACKED;
+            it.part = (int32_t)first;
+            it.pad0 = (int32_t)(first + n_in);
+            items.push_back(it);
+            n_in = 0;
+            rows = 0;
+        };
+        for (size_t pi = 0; pi < parts.size(); pi++) {
+            const Part& pt = parts[pi];
+            if (pt.split < 0 && pt.n >= 2 && pt.n <= pack_max) {
+                if (n_in && rows + pt.n > rows_per_item) close();
+                if (!n_in) first = pi;
+                n_in++;
+                rows += pt.n;
+                continue;
+            }
+            close();
+            const size_t k = part_items(pi, pi + 1, rows_per_item, chunk, nullptr);
+            if (items.n + k > items.cap && !items.grow(std::max(items.n + k, 2 * items.cap))) return;
+            part_items(pi, pi + 1, rows_per_item, chunk, items.p + items.n);
+            items.n += k;
+        }
+        close();
+    };
     auto build_items = [&](int64_t rows_per_item, int64_t chunk) {
+        if (packed_items) return build_packed(rows_per_item, chunk);
         items.clear();
         const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
         const size_t nt = parts.size() >= par_min ? std::min<size_t>(hw, parts.size()) : 1;
@@ -1055,8 +1099,21 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     // on small partitions (batches whose average part is shorter use a 2-row
     // variant), and a program whose gate proved useless runs ungated.  The
     // variants are compiled on first use.
+    // Batches of tiny symmetric partitions (average <= RB_PACK_MAX tuples, 64 by
+    // default; 0 disables) run the packed variant: whole partitions of up to
+    // that size go back to back into one item, so every warp of a CTA has rows.
     const JitKernel* jp = &P->jit;
-    if (P->jit.ok) {
+    if (P->jit.ok && P->jit.defer && (flags & RB_SYMMETRIC) && parts.size() > 1 && pack_max >= 2 &&
+        total / (int64_t)parts.size() <= pack_max) {
+        static std::mutex packed_mu;
+        std::lock_guard<std::mutex> lock(packed_mu);
+        if (!P->jit_packed_tried) {
+            P->jit_packed = jit_pair_kernel(P->F, c->device, 2, true);
+            P->jit_packed_tried = true;
+        }
+        if (P->jit_packed.ok && P->jit_packed.packed) jp = &P->jit_packed;
+    }
+    if (P->jit.ok && jp == &P->jit) {
         const bool small = P->jit.rows > 2 && !parts.empty() &&
                            total / (int64_t)parts.size() < (int64_t)BLOCK * P->jit.rows;
         const bool nogate = P->gate_off && P->jit.gated;
@@ -1080,6 +1137,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         }
     }
     const JitKernel& J = *jp;
+    packed_items = J.ok && J.packed;
     const int64_t rows_per_item = (int64_t)BLOCK * (J.ok ? J.rows : 1);
     mark();  // [1] variant selection
     build_items(rows_per_item, CHUNK);
@@ -1139,6 +1197,15 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
                                 (long long)(sizeof(int32_t) * stride * slices), cudaGetErrorString(e)));
     }
 
+    if (packed_items) {  // start position of every part (+ the end) for the packed items' row -> part lookup
+        std::vector<int32_t> po(parts.size() + 1);
+        for (size_t k = 0; k < parts.size(); k++) po[k] = (int32_t)parts[k].base;
+        po[parts.size()] = (int32_t)total;
+        if (cudaError_t e = c->offs.grow(sizeof(int32_t) * po.size(), c->stream))
+            return cleanup(fail(RB_ERR_CUDA, "part offsets: %s", cudaGetErrorString(e)));
+        CK(cudaMemcpyAsync(c->offs.p, po.data(), sizeof(int32_t) * po.size(), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));  // po is a local (pageable) vector
+    }
     mark();  // [2] items built, device buffers sized
     CK(cudaMemcpyAsync(c->items.p, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice, c->stream));
     if (refs) CK(cudaMemcpyAsync(c->refs.p, refs, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
@@ -1199,6 +1266,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         R.scratch_stride = stride;
         R.surv_count = &ctr[SURV];
         R.stat_gate = &ctr[GATE];
+        R.part_off = packed_items ? (const int32_t*)c->offs.p : nullptr;
         const long long per_row = (flags & RB_ENUMERATE) ? std::max(1, P->F.n_rules) : 1;
         // Ranges are sized from the survivors per item seen so far (the
         // program's previous run, else a probe of 1/64 of the items), so a

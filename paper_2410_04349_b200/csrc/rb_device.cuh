@@ -57,6 +57,10 @@ typedef unsigned long long uintptr_t;
 namespace rb {
 
 constexpr int MAX_COLS = 64;
+#ifndef SPEC_PACKED
+#define SPEC_PACKED 0  // 1: the kernel also takes MODE_PACKED items (batches of tiny partitions)
+#endif
+
 constexpr int MAX_EQ = 6;      // equality features filtered in the pair loop
 constexpr int MAX_TOK = 2;     // token-set features (jaccard / exact_token)
 constexpr int MAX_STR = 2;     // string features (edit)
@@ -71,7 +75,11 @@ constexpr int QCAP = 256;      // survivor queue entries per warp
 constexpr int NWARPS = BLOCK / 32;
 constexpr int64_t CHUNK = 16384;  // inner columns per work item
 
-enum RunMode : int32_t { MODE_SYM = 0, MODE_ASYM = 1, MODE_CROSS = 2 };
+// MODE_PACKED: several whole symmetric partitions of a batch back to back in
+// one item (rows [row0, row_hi), parts [part, pad0)); a row pairs only with
+// the later rows of its own partition.  Only the packed kernel variant
+// (SPEC_PACKED) is given such items.
+enum RunMode : int32_t { MODE_SYM = 0, MODE_ASYM = 1, MODE_CROSS = 2, MODE_PACKED = 3 };
 
 struct DevColumn {
     int32_t kind;
@@ -205,7 +213,20 @@ struct RunParams {
     long long surv_cap;
     unsigned long long* surv_count;
     const unsigned long long* bad_refs;  // non-zero: a tuple ref is out of range, evaluate nothing
+    const int32_t* part_off;  // packed items: start position of every part of the batch (+ the end)
 };
+
+// the part of a packed item (parts [lo, hi)) holding position pos
+static __device__ __forceinline__ int find_part(const RunParams& R, int lo, int hi, int64_t pos) {
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(R.part_off + mid) <= pos)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
 
 // device-side helpers shared by kernels
 __host__ __device__ inline uint32_t sig_bit(int32_t id) { return ((uint32_t)id * 0x9E3779B1u) >> 25; }
@@ -465,7 +486,10 @@ static __device__ __noinline__ void drain_queue(const VerifyProg& V, const RunPa
 // Deferred form: the warp appends its queue to the global survivor buffer
 // (one atomicAdd, coalesced 16-byte stores).  Entries past the capacity are
 // counted but not stored; the host then re-runs with room for all of them.
-static __device__ __forceinline__ void flush_survivors(const RunParams& R, const int2* q, int qn, int part) {
+// part_hi >= 0: a packed item (parts [part, part_hi)); its queue entries
+// carry the outer position instead of the tid
+static __device__ __forceinline__ void flush_survivors(const RunParams& R, const int2* q, int qn, int part,
+                                                       int part_hi = -1) {
     const int lane = threadIdx.x & 31;
     unsigned long long at = 0;
     if (lane == 0) at = atomicAdd(R.surv_count, (unsigned long long)qn);
@@ -473,7 +497,10 @@ static __device__ __forceinline__ void flush_survivors(const RunParams& R, const
     for (int k = lane; k < qn; k += 32)
         if (at + k < (unsigned long long)R.surv_cap) {
             const int2 e = q[k];
-            R.surv[at + k] = make_int4(e.x, e.y, part, 0);
+            if (part_hi >= 0)
+                R.surv[at + k] = make_int4(R.refs ? __ldg(R.refs + e.x) : e.x, e.y, find_part(R, part, part_hi, e.x), 0);
+            else
+                R.surv[at + k] = make_int4(e.x, e.y, part, 0);
         }
 }
 
@@ -702,6 +729,9 @@ struct Outer {
     Mask alive0;  // rules still possible after the t-only tests
     Mask alive_c; // rules still possible after the t-only constant tests alone
     int32_t jj_lo, jj_skip;
+#if SPEC_PACKED
+    int32_t jj_hi, pend;  // packed items: first invalid tile column, end position of the row's part
+#endif
     int32_t ocode[MAX_EQ];
     int32_t olen[MAX_TOK], orem[MAX_TOK];
     uint32_t orow[MAX_TOK];  // 2-D jaccard: shared-memory byte address of need[n][0][0]
@@ -713,9 +743,16 @@ struct Outer {
 
     __device__ __forceinline__ void load(const FilterPlan& F, const RunParams& R, const int32_t* tab, int mode,
                                          int64_t i_, int64_t row_hi, int64_t col0, int64_t col1,
-                                         unsigned long long& my_pairs) {
+                                         unsigned long long& my_pairs, int part_lo = 0, int part_hi = -1) {
         i = i_;
         ok = i < row_hi;
+#if SPEC_PACKED
+        pend = 0;
+        if (mode == MODE_PACKED && ok) {
+            pend = __ldg(R.part_off + find_part(R, part_lo, part_hi, i) + 1);
+            col1 = pend;
+        }
+#endif
         ti = 0;
         m_init(alive0, 0);
         m_init(alive_c, 0);
@@ -723,7 +760,7 @@ struct Outer {
             ti = R.refs ? R.refs[i] : (int32_t)i;
             m_init(alive0, RB_ALL_RULES);
             m_init(alive_c, RB_ALL_RULES);
-            if (mode == MODE_SYM) {
+            if (mode == MODE_SYM || mode == MODE_PACKED) {
                 const int64_t lo = col0 > i + 1 ? col0 : i + 1;
                 my_pairs += (unsigned long long)(col1 > lo ? col1 - lo : 0);
             } else if (mode == MODE_ASYM) {
@@ -814,6 +851,16 @@ struct Outer {
     __device__ __forceinline__ bool tile(int mode, int64_t jt) {
         jj_lo = 0;
         jj_skip = -1;
+#if SPEC_PACKED
+        jj_hi = TJ + 1;
+        if (mode == MODE_PACKED) {
+            const int64_t d = i - jt + 1, e = (int64_t)pend - jt;
+            jj_lo = d < 0 ? 0 : (d > TJ + 1 ? TJ + 1 : (int)d);
+            jj_hi = e < 0 ? 0 : (e > TJ + 1 ? TJ + 1 : (int)e);
+            if (!ok || jj_hi <= jj_lo) jj_lo = TJ + 1;
+            return false;
+        }
+#endif
         if (!ok) {
             jj_lo = TJ + 1;
         } else if (mode == MODE_SYM) {
@@ -832,7 +879,7 @@ struct Outer {
 template <typename Mask, int ROWS, bool AllValid, bool DEFER>
 __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg& V, const RunParams& R, const Tile& T,
                                           const int32_t* tab, Outer<Mask> (&o)[ROWS], int jj0, int tn, int2* q, int& qn,
-                                          int part, const int* cp_rule, int32_t* scratch,
+                                          int part, int part_hi, const int* cp_rule, int32_t* scratch,
                                           unsigned long long& my_surv, unsigned& gate_hits, unsigned& gate_iters) {
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << (threadIdx.x & 31)) - 1u;
@@ -860,7 +907,11 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
 #else
             const Mask& base = o[r].alive0;
 #endif
+#if SPEC_PACKED
+            alive[r] = AllValid ? base : m_gate(jj >= o[r].jj_lo && jj != o[r].jj_skip && jj < o[r].jj_hi, base);
+#else
             alive[r] = AllValid ? base : m_gate(jj >= o[r].jj_lo && jj != o[r].jj_skip, base);
+#endif
 #pragma unroll
             for (int f = 0; f < MAX_EQ; f++)
                 if (f < RB_NEQ && !RB_EQ_STAGE2(f)) m_kill(alive[r], o[r].ocode[f] != T.r[jj].head[f], RB_EQ_KILL(f));
@@ -1013,14 +1064,14 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
             for (int r = 0; r < ROWS; r++) {
                 const bool surv = m_any(alive[r]);
                 const unsigned bal = __ballot_sync(FULL, surv);
-                if (surv) q[qn + __popc(bal & lt_mask)] = make_int2(o[r].ti, T.r[jj].tid);
+                if (surv) q[qn + __popc(bal & lt_mask)] = make_int2(part_hi >= 0 ? (int)o[r].i : o[r].ti, T.r[jj].tid);
                 qn += __popc(bal);
                 my_surv += surv ? 1 : 0;
             }
             if (qn > QCAP - 32 * ROWS) {
                 __syncwarp();
                 if (DEFER)
-                    flush_survivors(R, q, qn, part);
+                    flush_survivors(R, q, qn, part, part_hi);
                 else
                     drain_queue(V, R, q, qn, part, cp_rule, scratch);
                 __syncwarp();
@@ -1062,6 +1113,7 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
         const Item item = R.items[it];
         const int64_t col0 = item.col0, col1 = item.col1;
         const int part = item.part;
+        const int part_hi = SPEC_PACKED && item.mode == MODE_PACKED ? item.pad0 : -1;
 
         Outer<Mask> o[ROWS];
 #pragma unroll
@@ -1070,7 +1122,7 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
             // symmetric diagonal together (tight jj0 skip, more all-valid tiles)
             o[r].load(F, R, tab, item.mode, (int64_t)item.row0 + (warp * ROWS + r) * 32 + lane, (int64_t)item.row_hi,
                       col0, col1,
-                      my_pairs);
+                      my_pairs, part, part_hi);
 
         for (int64_t jt = col0; jt < col1; jt += TJ) {
             const int tn = (int)(col1 - jt < TJ ? col1 - jt : TJ);
@@ -1116,17 +1168,25 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
             // triangle's diagonal tiles (and small partitions) skip the dead part
             const int jj0 = __reduce_min_sync(FULL, lo);
             if (jj0 >= tn) continue;
+#if SPEC_PACKED
+            int hi = 0;
+#pragma unroll
+            for (int r = 0; r < ROWS; r++) hi = max(hi, o[r].jj_lo <= TJ ? o[r].jj_hi : 0);
+            const int tn_w = min(tn, (int)__reduce_max_sync(FULL, (unsigned)hi));  // the warp's last valid column + 1
+#else
+            const int tn_w = tn;
+#endif
             if (__all_sync(FULL, all_valid))
-                tile_loop<Mask, ROWS, true, DEFER>(F, V, R, T, tab, o, 0, tn, q, qn, part, cp_rule, scratch, my_surv,
+                tile_loop<Mask, ROWS, true, DEFER>(F, V, R, T, tab, o, 0, tn, q, qn, part, part_hi, cp_rule, scratch, my_surv,
                                                    gate_hits, gate_iters);
             else
-                tile_loop<Mask, ROWS, false, DEFER>(F, V, R, T, tab, o, jj0, tn, q, qn, part, cp_rule, scratch,
+                tile_loop<Mask, ROWS, false, DEFER>(F, V, R, T, tab, o, jj0, tn_w, q, qn, part, part_hi, cp_rule, scratch,
                                                     my_surv, gate_hits, gate_iters);
         }
         if (qn) {
             __syncwarp();
             if (DEFER)
-                flush_survivors(R, q, qn, part);
+                flush_survivors(R, q, qn, part, part_hi);
             else
                 drain_queue(V, R, q, qn, part, cp_rule, scratch);
             __syncwarp();

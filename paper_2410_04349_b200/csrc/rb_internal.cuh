@@ -41,14 +41,16 @@ struct JitKernel {
     int rows = 1;  // outer rows per thread
     bool defer = false;  // survivors go to a buffer decided by `verify` (see RunParams::surv)
     bool gated = false;  // compiled with the stage-1 gate (counts gate passes in RunParams::stat_gate)
+    bool packed = false;  // takes MODE_PACKED items (several tiny partitions per item)
     cudaKernel_t verify = nullptr;
     int verify_blocks_per_sm = 1;
     double compile_ms = 0;
     std::string key;
     std::string log;
 };
-// force_rows > 0 compiles that many outer rows per thread (the small-partition variant)
-JitKernel jit_pair_kernel(const FilterPlan& F, int device, int force_rows = 0);
+// force_rows > 0 compiles that many outer rows per thread (the small-partition variant);
+// packed: the variant also takes MODE_PACKED items (deferred kernels only)
+JitKernel jit_pair_kernel(const FilterPlan& F, int device, int force_rows = 0, bool packed = false);
 cudaError_t launch_jit_kernel(const JitKernel& k, const FilterPlan& F, const VerifyProg& V, const RunParams& R,
                               int grid, cudaStream_t st);
 cudaError_t launch_jit_verify(const JitKernel& k, const VerifyProg& V, const RunParams& R, int grid, cudaStream_t st);

@@ -146,27 +146,35 @@ def test_useless_gate_switches_off_and_stays_exact(monkeypatch):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("symmetric", [True, False])
-def test_many_part_batch_items_built_by_threads(symmetric, monkeypatch):
+@pytest.mark.parametrize("sizes", ["mixed", "tiny"])
+def test_many_part_batch_items_built_by_threads(symmetric, sizes, monkeypatch):
     """A batch of many partitions has its work items laid out by several
-    host threads (forced here for any size with RB_ITEM_THREADS_MIN=1): the
-    rows of every partition equal its own single run."""
+    host threads (forced here for any size with RB_ITEM_THREADS_MIN=1), and a
+    batch of tiny symmetric partitions runs packed (several partitions per
+    item; RB_PACK_MAX=0 turns packing off): the rows of every partition
+    equal its own single run."""
     import random
 
     from paper_2410_04349_b200 import run_partitions
 
     monkeypatch.delenv("RB_JIT", raising=False)
+    monkeypatch.delenv("RB_PACK_MAX", raising=False)
     rel, path, _ = goldens.load("citation")
     rng = random.Random(7)
     parts, k = [], 0
+    choice = [1, 2, 3, 5, 9, 17, 40, 130, 700, 1300] if sizes == "mixed" else [1, 2, 3, 5, 9, 17, 33, 64, 65, 90]
     while len(parts) < 300:
-        size = rng.choice([1, 2, 3, 5, 9, 17, 40, 130, 700, 1300])
+        size = rng.choice(choice)
         refs = rng.sample(range(len(rel)), size)
         parts.append(DataPartition(k, tuple(refs)))
         k += 1
     cfg = EngineConfig(symmetric_mode=symmetric)
     want = [run_partition(p, rel, path, cfg).sorted_pairs() for p in parts]
-    for threads_min in ("1", "1000000"):
+    for threads_min, pack in (("1", "64"), ("1000000", "64"), ("1", "0"), ("1", "100")):
         monkeypatch.setenv("RB_ITEM_THREADS_MIN", threads_min)
+        monkeypatch.setenv("RB_PACK_MAX", pack)
         got = [cs.sorted_pairs() for cs in run_partitions(parts, rel, path, cfg)]
-        assert got == want
+        assert got == want, (threads_min, pack)
+        assert [cs.stats.total_comparisons() for cs in run_partitions(parts, rel, path, cfg)] == \
+               [len(p.tuple_refs) * (len(p.tuple_refs) - 1) // (2 if symmetric else 1) for p in parts]
     assert sum(map(len, want)) > 50
