@@ -146,7 +146,7 @@ def test_useless_gate_switches_off_and_stays_exact(monkeypatch):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("symmetric", [True, False])
-@pytest.mark.parametrize("sizes", ["mixed", "tiny"])
+@pytest.mark.parametrize("sizes", ["mixed", "tiny", "tiny_enumerate"])
 def test_many_part_batch_items_built_by_threads(symmetric, sizes, monkeypatch):
     """A batch of many partitions has its work items laid out by several
     host threads (forced here for any size with RB_ITEM_THREADS_MIN=1), and a
@@ -168,7 +168,7 @@ def test_many_part_batch_items_built_by_threads(symmetric, sizes, monkeypatch):
         refs = rng.sample(range(len(rel)), size)
         parts.append(DataPartition(k, tuple(refs)))
         k += 1
-    cfg = EngineConfig(symmetric_mode=symmetric)
+    cfg = EngineConfig(symmetric_mode=symmetric, enumerate_witnesses=sizes.endswith("enumerate"))
     want = [run_partition(p, rel, path, cfg).sorted_pairs() for p in parts]
     for threads_min, pack in (("1", "64"), ("1000000", "64"), ("1", "0"), ("1", "100")):
         monkeypatch.setenv("RB_ITEM_THREADS_MIN", threads_min)
