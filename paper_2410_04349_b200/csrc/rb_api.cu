@@ -1038,28 +1038,32 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     bool packed_items = false;
     const char* env_pack = std::getenv("RB_PACK_MAX");
     const int64_t pack_max = env_pack ? std::atoll(env_pack) : 64;
-    auto build_packed = [&](int64_t rows_per_item, int64_t chunk) {
-        items.clear();
-        size_t first = 0, n_in = 0;  // the open pack: parts [first, first + n_in)
+    // the items of parts [p0, p1) in the packed layout (packs never cross p1),
+    // written at `at` when non-null; returns their count
+    auto packed_items_of = [&](size_t p0, size_t p1, int64_t rows_per_item, int64_t chunk, Item* at) {
+        size_t k = 0, first = 0, n_in = 0;  // the open pack: parts [first, first + n_in)
         int64_t rows = 0;
         auto close = [&]() {
             if (!n_in) return;
-            const Part& a = parts[first];
-            const Part& b = parts[first + n_in - 1];
-            Item it{};
-            it.row0 = (int32_t)a.base;
-            it.col0 = (int32_t)(a.base + 1);
-            it.col1 = it.row_hi = (int32_t)(b.base + b.n);
-            it.mode = MODE_PACKED;
-            it.part = (int32_t)first;
-            it.pad0 = (int32_t)(first + n_in);
-            items.push_back(it);
+            if (at) {
+                const Part& a = parts[first];
+                const Part& b = parts[first + n_in - 1];
+                Item& it = at[k];
+                it.row0 = (int32_t)a.base;
+                it.col0 = (int32_t)(a.base + 1);
+                it.col1 = it.row_hi = (int32_t)(b.base + b.n);
+                it.mode = MODE_PACKED;
+                it.part = (int32_t)first;
+                it.pad0 = (int32_t)(first + n_in);
+                it.pad1 = 0;
+            }
+            k++;
             n_in = 0;
             rows = 0;
         };
-        for (size_t pi = 0; pi < parts.size(); pi++) {
+        for (size_t pi = p0; pi < p1; pi++) {
             const Part& pt = parts[pi];
-            if (pt.split < 0 && pt.n >= 2 && pt.n <= pack_max) {
+            if (pt.split < 0 && pt.n >= 2 && pt.n <= pack_max && pt.n <= rows_per_item) {  // a pack fits one item
                 if (n_in && rows + pt.n > rows_per_item) close();
                 if (!n_in) first = pi;
                 n_in++;
@@ -1067,15 +1071,12 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
                 continue;
             }
             close();
-            const size_t k = part_items(pi, pi + 1, rows_per_item, chunk, nullptr);
-            if (items.n + k > items.cap && !items.grow(std::max(items.n + k, 2 * items.cap))) return;
-            part_items(pi, pi + 1, rows_per_item, chunk, items.p + items.n);
-            items.n += k;
+            k += part_items(pi, pi + 1, rows_per_item, chunk, at ? at + k : nullptr);
         }
         close();
+        return k;
     };
     auto build_items = [&](int64_t rows_per_item, int64_t chunk) {
-        if (packed_items) return build_packed(rows_per_item, chunk);
         items.clear();
         const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
         const size_t nt = parts.size() >= par_min ? std::min<size_t>(hw, parts.size()) : 1;
@@ -1089,10 +1090,14 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             fn(0);
             for (auto& th : pool) th.join();
         };
-        run_all([&](size_t t) { cnt[t] = part_items(cut[t], cut[t + 1], rows_per_item, chunk, nullptr); });
+        auto layout = [&](size_t t, Item* at) {
+            return packed_items ? packed_items_of(cut[t], cut[t + 1], rows_per_item, chunk, at)
+                                : part_items(cut[t], cut[t + 1], rows_per_item, chunk, at);
+        };
+        run_all([&](size_t t) { cnt[t] = layout(t, nullptr); });
         for (size_t t = 0; t < nt; t++) off[t + 1] = off[t] + cnt[t];
         if (off[nt] > items.cap && !items.grow(std::max(off[nt], 2 * items.cap))) return;
-        run_all([&](size_t t) { part_items(cut[t], cut[t + 1], rows_per_item, chunk, items.p + off[t]); });
+        run_all([&](size_t t) { layout(t, items.p + off[t]); });
         items.n = off[nt];
     };
     // Kernel variant: a 3-row kernel's 768-row items would leave threads idle

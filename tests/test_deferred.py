@@ -170,7 +170,7 @@ def test_many_part_batch_items_built_by_threads(symmetric, sizes, monkeypatch):
         k += 1
     cfg = EngineConfig(symmetric_mode=symmetric, enumerate_witnesses=sizes.endswith("enumerate"))
     want = [run_partition(p, rel, path, cfg).sorted_pairs() for p in parts]
-    for threads_min, pack in (("1", "64"), ("1000000", "64"), ("1", "0"), ("1", "100")):
+    for threads_min, pack in (("1", "64"), ("1000000", "64"), ("1", "0"), ("1", "100"), ("1", "100000")):
         monkeypatch.setenv("RB_ITEM_THREADS_MIN", threads_min)
         monkeypatch.setenv("RB_PACK_MAX", pack)
         got = [cs.sorted_pairs() for cs in run_partitions(parts, rel, path, cfg)]
