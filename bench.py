@@ -215,6 +215,14 @@ def ncu_capture(w, pairs_step):
                 if "smsp__inst_executed.sum" in m:  # the per-pair instruction cost of the capture
                     pipe["warp_instructions_per_pair"] = float(m["smsp__inst_executed.sum"]["value"]) / pairs_step
                 pipe["source"] = entry.get("capture")
+                # the busiest issue pipe of the capture: the kernel's speed-of-light fraction
+                # (the inner tuples are reused from shared memory, so DRAM is not the bound)
+                names = {"sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "ALU",
+                         "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "XU",
+                         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "shared memory"}
+                busiest = max((k for k in names if k in pipe), key=lambda k: pipe[k], default=None)
+                if busiest:
+                    pipe["binding"] = {"pipe": names[busiest], "frac": pipe[busiest] / 100.0}
         except Exception:
             traffic = None
     return traffic, pipe
