@@ -463,7 +463,8 @@ def main():
             vms.append(st.kernel_ms - kms[-1])  # deferred verification kernel
             print(f"step: events {times[-1]:.1f} ms, kernels {st.kernel_ms:.1f} ms (pair {kms[-1]:.1f}), "
                   f"host {1e3 * (h1 - h0):.1f} ms, "
-                  f"survivors {st.survivors}, rows {len(rows[0])}", file=sys.stderr)
+                  f"survivors {st.survivors}, rows {len(rows[0])}, launches {st.launches}, retries {st.retries}",
+                  file=sys.stderr)
             assert st.comparisons == pairs_step and len(rows[0]) == n_rows
     barrier()
     t_total = torch.tensor([sum(times)], dtype=torch.float64, device=red_dev)
@@ -499,6 +500,8 @@ def main():
         q2 = time.perf_counter()
         rows2, st2 = step(p2, host=True)  # evaluate + D2H of the rows
         q3 = time.perf_counter()
+        print(f"e2e step: kernels {st2.kernel_ms:.1f} ms (pair {st2.pair_ms:.1f}), launches {st2.launches}, "
+              f"retries {st2.retries}", file=sys.stderr)
         assert len(rows2[0]) == n_rows
         p2.close()
         drel.close()

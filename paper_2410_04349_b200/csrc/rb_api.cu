@@ -163,6 +163,12 @@ struct rb_prog {
     long long last_rows = 0;  // output size of the previous run: sizes the next buffer
     long long last_surv = 0;  // survivors of the previous run: sizes the deferred-verification buffer
     double surv_rate = -1.0;  // survivors per work item in the previous run (-1: none yet)
+    // item ranges that fit the survivor buffer in the previous run, and its item count: a
+    // run over the same items (a repeated batch) replays them instead of re-learning where
+    // the survivors concentrate (each range that overflows is re-run)
+    std::vector<std::pair<int, int>> last_ranges;
+    int last_n_items = -1;
+    std::mutex ranges_mu;  // guards last_ranges / last_n_items (a program may be run from several threads)
 };
 
 struct rb_result {
@@ -1277,12 +1283,27 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         // program's previous run, else a probe of 1/64 of the items), so a
         // range rarely overflows the buffer; one that does is rolled back and
         // re-run larger or in halves (the `ranges` stack).
-        std::vector<std::pair<int, int>> ranges;
+        std::vector<std::pair<int, int>> ranges, done_ranges, plan;
+        size_t replay = 0;
+        {
+            std::lock_guard<std::mutex> lock(P->ranges_mu);
+            if (P->last_n_items == n_items) plan = P->last_ranges;
+        }
+        if (!plan.empty() && P->last_surv > scap) {  // replayed ranges: the buffer the last run ended with
+            scap = P->last_surv;
+            if (cudaError_t e = c->surv.grow(sizeof(int4) * (size_t)scap, c->stream))
+                return cleanup(fail(RB_ERR_OOM, "survivor buffer of %lld entries: %s", scap, cudaGetErrorString(e)));
+        }
         int retries = 0, next = 0;
         long long done_items = 0, done_surv = 0;
         for (;;) {
             if (ranges.empty()) {
                 if (next >= n_items) break;
+                if (replay < plan.size() && plan[replay].first == next) {
+                    ranges.push_back(plan[replay++]);
+                    next = ranges.back().second;
+                    continue;
+                }
                 const double rate = done_items ? (double)done_surv / (double)done_items : P->surv_rate;
                 long long size;
                 if (rate < 0) {
@@ -1385,10 +1406,16 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             res->stats.launches += 1;
             std::copy(host_ctr, host_ctr + n_counters, base.begin());
             P->last_surv = std::max(P->last_surv, surv);
+            done_ranges.push_back({lo, hi});
             done_items += hi - lo;
             done_surv += surv;
         }
         P->surv_rate = done_items ? (double)done_surv / (double)done_items : -1.0;
+        {
+            std::lock_guard<std::mutex> lock(P->ranges_mu);
+            P->last_ranges.swap(done_ranges);
+            P->last_n_items = n_items;
+        }
         // a gate that nearly every warp iteration passes only costs its vote:
         // later runs of this program use the ungated kernel
         if (J.gated && base[GATE + 1] > 0 && (double)base[GATE] > 0.95 * (double)base[GATE + 1]) P->gate_off = true;

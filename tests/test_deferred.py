@@ -178,3 +178,27 @@ def test_many_part_batch_items_built_by_threads(symmetric, sizes, monkeypatch):
         assert [cs.stats.total_comparisons() for cs in run_partitions(parts, rel, path, cfg)] == \
                [len(p.tuple_refs) * (len(p.tuple_refs) - 1) // (2 if symmetric else 1) for p in parts]
     assert sum(map(len, want)) > 50
+
+
+@pytest.mark.gpu
+def test_repeated_run_replays_the_ranges_that_fit(monkeypatch):
+    """A program run again over the same items replays the previous run's
+    survivor ranges: no overflow re-runs the second time, same rows."""
+    import numpy as np
+
+    from paper_2410_04349_b200._lib import RB_SYMMETRIC
+    from paper_2410_04349_b200.encode import RelationEncoding
+    from paper_2410_04349_b200.engine import PathProgram
+
+    monkeypatch.delenv("RB_JIT", raising=False)
+    monkeypatch.setenv("RB_SURV_MIN", "2")
+    monkeypatch.setenv("RB_SURV_LIMIT", "64")
+    rel, path, _ = goldens.load("citation")
+    enc = RelationEncoding(rel).prepare(path.predicate_table)
+    prog = PathProgram(path, enc, device=0)
+    (t1, s1, r1), st1 = prog.run_raw(None, len(rel), RB_SYMMETRIC)
+    (t2, s2, r2), st2 = prog.run_raw(None, len(rel), RB_SYMMETRIC)
+    rows1 = sorted(zip(t1.tolist(), s1.tolist(), r1.tolist()))
+    assert rows1 == sorted(zip(t2.tolist(), s2.tolist(), r2.tolist())) and len(rows1) > 100
+    assert st1.retries > 0 and st2.retries == 0 and st2.launches < st1.launches
+    assert st1.comparisons == st2.comparisons == len(rel) * (len(rel) - 1) // 2

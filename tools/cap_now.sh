@@ -1,4 +1,3 @@
-timeout 900 python -m pytest tests/test_deferred.py tests/test_pipeline.py tests/test_scheduler.py tests/test_gpu_parity.py -q -m gpu -x 2>&1 | tail -3
-RB_HOST_TIMING=1 timeout 600 python tools/batch_phases.py person5_parts 2>&1 | tail -2
-timeout 600 python bench.py --workload person5_parts > gpurun_out/p5parts_packed2.json 2>/dev/null; python -c "
-import json; d=json.loads(open('gpurun_out/p5parts_packed2.json').read().strip().splitlines()[-1]); print(d['value'], d['e2e']['value'], d['parity'])"
+timeout 1500 python -m pytest tests/ -q -m gpu -x 2>&1 | tail -4
+timeout 1800 python bench.py --workload person5 --tuples 10000000 --no-cpu --steps 3 > gpurun_out/p5_10M.json 2> gpurun_out/p5_10M.err; echo rc=$?; grep step gpurun_out/p5_10M.err | tail -4; tail -1 gpurun_out/p5_10M.json | cut -c1-200
+timeout 1800 python bench.py --workload person5_parts --tuples 10000000 > gpurun_out/p5parts_10M_d.json 2> gpurun_out/p5parts_10M_d.err; echo rc=$?; grep step gpurun_out/p5parts_10M_d.err | tail -3
