@@ -1040,7 +1040,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     // (same order as one thread).  Writing ~10^5 items is memory-bound work.
     const char* env_par = std::getenv("RB_ITEM_THREADS_MIN");
     const size_t par_min = env_par ? (size_t)std::max(1ll, std::atoll(env_par)) : 16384;
-    // packed variant: runs of tiny symmetric partitions share items, larger parts get their own
+    // packed variant: runs of tiny partitions share items, larger parts and cross blocks get their own
     bool packed_items = false;
     const char* env_pack = std::getenv("RB_PACK_MAX");
     const int64_t pack_max = env_pack ? std::atoll(env_pack) : 64;
@@ -1056,7 +1056,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
                 const Part& b = parts[first + n_in - 1];
                 Item& it = at[k];
                 it.row0 = (int32_t)a.base;
-                it.col0 = (int32_t)(a.base + 1);
+                it.col0 = (int32_t)((flags & RB_SYMMETRIC) ? a.base + 1 : a.base);
                 it.col1 = it.row_hi = (int32_t)(b.base + b.n);
                 it.mode = MODE_PACKED;
                 it.part = (int32_t)first;
@@ -1110,11 +1110,11 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     // on small partitions (batches whose average part is shorter use a 2-row
     // variant), and a program whose gate proved useless runs ungated.  The
     // variants are compiled on first use.
-    // Batches of tiny symmetric partitions (average <= RB_PACK_MAX tuples, 64 by
+    // Batches of tiny partitions (average <= RB_PACK_MAX tuples, 64 by
     // default; 0 disables) run the packed variant: whole partitions of up to
     // that size go back to back into one item, so every warp of a CTA has rows.
     const JitKernel* jp = &P->jit;
-    if (P->jit.ok && P->jit.defer && (flags & RB_SYMMETRIC) && parts.size() > 1 && pack_max >= 2 &&
+    if (P->jit.ok && P->jit.defer && parts.size() > 1 && pack_max >= 2 &&
         total / (int64_t)parts.size() <= pack_max) {
         static std::mutex packed_mu;
         std::lock_guard<std::mutex> lock(packed_mu);

@@ -75,10 +75,10 @@ constexpr int QCAP = 256;      // survivor queue entries per warp
 constexpr int NWARPS = BLOCK / 32;
 constexpr int64_t CHUNK = 16384;  // inner columns per work item
 
-// MODE_PACKED: several whole symmetric partitions of a batch back to back in
-// one item (rows [row0, row_hi), parts [part, pad0)); a row pairs only with
-// the later rows of its own partition.  Only the packed kernel variant
-// (SPEC_PACKED) is given such items.
+// MODE_PACKED: several whole partitions of a batch back to back in one item
+// (rows [row0, row_hi), parts [part, pad0)); a row pairs only with the later
+// rows (symmetric) or the other rows (asymmetric) of its own partition.  Only
+// the packed kernel variant (SPEC_PACKED) is given such items.
 enum RunMode : int32_t { MODE_SYM = 0, MODE_ASYM = 1, MODE_CROSS = 2, MODE_PACKED = 3 };
 
 struct DevColumn {
@@ -730,7 +730,8 @@ struct Outer {
     Mask alive_c; // rules still possible after the t-only constant tests alone
     int32_t jj_lo, jj_skip;
 #if SPEC_PACKED
-    int32_t jj_hi, pend;  // packed items: first invalid tile column, end position of the row's part
+    int32_t jj_hi;       // packed items: first invalid tile column
+    int32_t pbeg, pend;  // packed items: the row's valid inner positions [pbeg, pend) (minus i itself)
 #endif
     int32_t ocode[MAX_EQ];
     int32_t olen[MAX_TOK], orem[MAX_TOK];
@@ -747,10 +748,13 @@ struct Outer {
         i = i_;
         ok = i < row_hi;
 #if SPEC_PACKED
-        pend = 0;
+        pbeg = pend = 0;
         if (mode == MODE_PACKED && ok) {
-            pend = __ldg(R.part_off + find_part(R, part_lo, part_hi, i) + 1);
-            col1 = pend;
+            // symmetric: the later rows of its own partition; asymmetric: every other row of it
+            const int k = find_part(R, part_lo, part_hi, i);
+            pbeg = (R.flags & RB_SYMMETRIC) ? (int32_t)i + 1 : __ldg(R.part_off + k);
+            pend = __ldg(R.part_off + k + 1);
+            my_pairs += (unsigned long long)(pend - pbeg - (pbeg <= i ? 1 : 0));
         }
 #endif
         ti = 0;
@@ -760,7 +764,9 @@ struct Outer {
             ti = R.refs ? R.refs[i] : (int32_t)i;
             m_init(alive0, RB_ALL_RULES);
             m_init(alive_c, RB_ALL_RULES);
-            if (mode == MODE_SYM || mode == MODE_PACKED) {
+            if (mode == MODE_PACKED) {
+                // counted above
+            } else if (mode == MODE_SYM) {
                 const int64_t lo = col0 > i + 1 ? col0 : i + 1;
                 my_pairs += (unsigned long long)(col1 > lo ? col1 - lo : 0);
             } else if (mode == MODE_ASYM) {
@@ -854,9 +860,10 @@ struct Outer {
 #if SPEC_PACKED
         jj_hi = TJ + 1;
         if (mode == MODE_PACKED) {
-            const int64_t d = i - jt + 1, e = (int64_t)pend - jt;
+            const int64_t d = (int64_t)pbeg - jt, e = (int64_t)pend - jt, x = i - jt;
             jj_lo = d < 0 ? 0 : (d > TJ + 1 ? TJ + 1 : (int)d);
             jj_hi = e < 0 ? 0 : (e > TJ + 1 ? TJ + 1 : (int)e);
+            jj_skip = (pbeg <= i && x >= 0 && x < TJ) ? (int)x : -1;
             if (!ok || jj_hi <= jj_lo) jj_lo = TJ + 1;
             return false;
         }
