@@ -1284,6 +1284,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         // range rarely overflows the buffer; one that does is rolled back and
         // re-run larger or in halves (the `ranges` stack).
         std::vector<std::pair<int, int>> ranges, done_ranges, plan;
+        std::vector<long long> done_counts;  // survivors of each completed range
         size_t replay = 0;
         {
             std::lock_guard<std::mutex> lock(P->ranges_mu);
@@ -1407,13 +1408,30 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             std::copy(host_ctr, host_ctr + n_counters, base.begin());
             P->last_surv = std::max(P->last_surv, surv);
             done_ranges.push_back({lo, hi});
+            done_counts.push_back(surv);
             done_items += hi - lo;
             done_surv += surv;
         }
         P->surv_rate = done_items ? (double)done_surv / (double)done_items : -1.0;
+        // the plan for the next run: adjacent ranges merged while their survivors fit the
+        // streaming budget (so a probe range or an over-cautious split is not replayed)
+        std::vector<std::pair<int, int>> merged;
+        long long acc = 0, widest = 0;
+        for (size_t k = 0; k < done_ranges.size(); k++) {
+            if (!merged.empty() && merged.back().second == done_ranges[k].first &&
+                acc + done_counts[k] <= (long long)(0.8 * (double)SURV_LIMIT)) {
+                merged.back().second = done_ranges[k].second;
+                acc += done_counts[k];
+            } else {
+                merged.push_back(done_ranges[k]);
+                acc = done_counts[k];
+            }
+            widest = std::max(widest, acc);  // survivors of the largest merged range: the buffer a replay needs
+        }
+        P->last_surv = std::max(P->last_surv, widest);
         {
             std::lock_guard<std::mutex> lock(P->ranges_mu);
-            P->last_ranges.swap(done_ranges);
+            P->last_ranges.swap(merged);
             P->last_n_items = n_items;
         }
         // a gate that nearly every warp iteration passes only costs its vote:
