@@ -1,4 +1,7 @@
-timeout 900 python -m pytest tests/test_deferred.py tests/test_pipeline.py tests/test_scheduler.py tests/test_gpu_parity.py tests/test_distributed.py -q -m gpu -x 2>&1 | tail -3
-for wl in linkage citation3_parts person5_parts; do timeout 900 python bench.py --workload $wl --no-cpu > gpurun_out/rp_$wl.json 2> gpurun_out/rp_$wl.err; echo "$wl $(grep '^step' gpurun_out/rp_$wl.err | tail -1)"; python -c "
-import json; d=json.loads(open('gpurun_out/rp_$wl.json').read().strip().splitlines()[-1]); print('%.4g'%d['value'])"; done
-timeout 1800 python bench.py --workload person5_parts --tuples 10000000 --no-cpu --steps 3 > gpurun_out/rp_10M.json 2> gpurun_out/rp_10M.err; grep step gpurun_out/rp_10M.err | tail -2
+mkdir -p gpurun_out/final5
+for wl in citation3 edit_heavy person5 person5_parts linkage citation3_parts citation_small; do
+  timeout 900 python bench.py --workload $wl > gpurun_out/final5/$wl.json 2> gpurun_out/final5/$wl.err
+  echo "$wl rc=$?"
+done
+timeout 900 python bench.py --impl reference > gpurun_out/final5/reference_arm.json 2> gpurun_out/final5/reference_arm.err; echo "ref rc=$?"
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
