@@ -166,6 +166,49 @@ int rb_result_device(const rb_result* res, const int32_t** t, const int32_t** s,
                      const int32_t** part);
 int rb_result_destroy(rb_result* res);
 
+/* ---- the callers either side of the path, on the device ------------------
+ * Plan-derived partitioning (partitioning.py:93-131 iter_partitions,
+ * 144-157 sibling_pull_pairs; the device half of pipeline_run,
+ * pipeline.py:245-433).  Branch b keys tuple tid with keys[b*n + tid]
+ * (int64): equal keys form one group, groups come in ascending key order,
+ * tuple ids ascend inside a group -- the reference's sorted(groups) when the
+ * keys are ranks of its key strings.  A group of more than
+ * max_partition_size tuples is dealt round-robin into ceil(|g| / max)
+ * sibling partitions (refs[sub::n_parts]); with RB_PART_PULLS every sibling
+ * pair (i < j) also becomes a cross block, left = sibling i.  The sorted
+ * tuple ids stay on the device as the refs of rb_run_parts.
+ * rb_partition_codes keys branch b on the relation's CODES column cols[b]
+ * (negative codes = missing: one group, ordered first), with no upload. */
+#define RB_PART_PULLS 1u       /* PipelineConfig.enable_pulls               */
+#define RB_PART_KEYS_DEVICE 2u /* keys is a device pointer                  */
+typedef struct rb_parts rb_parts;
+int rb_partition(rb_ctx* ctx, rb_rel* rel, const int64_t* keys, const int32_t* branch_ids, int32_t n_branches,
+                 int64_t max_partition_size, uint32_t flags, rb_parts** out);
+int rb_partition_codes(rb_ctx* ctx, rb_rel* rel, const int32_t* cols, const int32_t* branch_ids, int32_t n_branches,
+                       int64_t max_partition_size, uint32_t flags, rb_parts** out);
+int rb_parts_info(const rb_parts* parts, int64_t* n_partitions, int64_t* n_pulls, int64_t* n_refs, int64_t* n_groups);
+/* host copies (any pointer may be NULL): refs[n_refs]; per partition, then
+ * per pull: base position in refs, size, split (-1 partition, else |left|),
+ * rbase (right side start of a pull, else -1), branch id, sibling group
+ * (0 none, else 1-based in order of appearance) */
+int rb_parts_copy(const rb_parts* parts, int32_t* refs, int64_t* base, int64_t* size, int64_t* split, int64_t* rbase,
+                  int32_t* branch, int32_t* sibling);
+int rb_parts_destroy(rb_parts* parts);
+/* One batched run over every partition with pairs and every pull of
+ * `parts` that rank `rank` of `world` owns: static longest-processing-time
+ * placement on pair counts, identical on every rank (world 1: all). */
+int rb_run_parts(rb_ctx* ctx, rb_rel* rel, rb_prog* prog, const rb_parts* parts, int32_t rank, int32_t world,
+                 uint32_t flags, rb_result** out);
+/* Collect (pipeline.py:407-421): the rows sorted by (t, s), one row per
+ * (t, s) carrying its smallest rule index (rule-set order), in place.  The
+ * rows' part indices are dropped. */
+int rb_result_collect(rb_result* res, int64_t n_tuples, int32_t n_rules);
+/* the same over caller-owned device arrays (e.g. rows exchanged between
+ * GPUs), ordered on the context's stream: out_* hold >= count rows */
+int rb_collect_device(rb_ctx* ctx, const int32_t* t, const int32_t* s, const int32_t* rule, int64_t count,
+                      int64_t n_tuples, int32_t n_rules, int32_t* out_t, int32_t* out_s, int32_t* out_rule,
+                      int64_t* out_count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,6 +23,7 @@ HEADERS = [HEADER, os.path.join(os.path.dirname(HERE), "include", "rbencode.h")]
 RB_OK = 0
 RB_ERR_INVALID, RB_ERR_CUDA, RB_ERR_OOM, RB_ERR_LIMIT, RB_ERR_INTERNAL = -1, -2, -3, -4, -5
 RB_SYMMETRIC, RB_ENUMERATE, RB_STATS = 1, 2, 4
+RB_PART_PULLS, RB_PART_KEYS_DEVICE = 1, 2
 MAX_SLOTS = 64
 
 c_i32p = ctypes.POINTER(ctypes.c_int32)
@@ -82,6 +83,17 @@ _SIGNATURES = {
     "rb_result_stats": (ctypes.c_int, [c_vp, ctypes.POINTER(RbStats)]),
     "rb_result_destroy": (ctypes.c_int, [c_vp]),
     "rb_result_device": (ctypes.c_int, [c_vp, c_vpp, c_vpp, c_vpp, c_vpp]),
+    "rb_partition": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, c_vpp]),
+    "rb_partition_codes": (
+        ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, c_vpp]),
+    "rb_parts_info": (ctypes.c_int, [c_vp, c_i64p, c_i64p, c_i64p, c_i64p]),
+    "rb_parts_copy": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "rb_parts_destroy": (ctypes.c_int, [c_vp]),
+    "rb_run_parts": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, c_vpp]),
+    "rb_result_collect": (ctypes.c_int, [c_vp, ctypes.c_int64, ctypes.c_int32]),
+    "rb_collect_device": (
+        ctypes.c_int,
+        [c_vp, c_vp, c_vp, c_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, c_vp, c_vp, c_vp, c_i64p]),
     # include/rbencode.h
     "rb_encode_eq_codes": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int64, c_vp]),
     "rb_encode_tokens": (ctypes.c_int64, [c_vp, c_vp, c_vp, ctypes.c_int64, c_vp, c_vp, c_i32p]),

@@ -21,11 +21,11 @@
 #include <utility>
 #include <vector>
 
-#include "rb_internal.cuh"
+#include "rb_state.cuh"
 
 using namespace rb;
 
-namespace {
+namespace rb {
 
 thread_local std::string g_err;
 
@@ -39,149 +39,9 @@ int fail(int code, const char* fmt, ...) {
     return code;
 }
 
-#define CK(call)                                                                                    \
-    do {                                                                                            \
-        cudaError_t e_ = (call);                                                                    \
-        if (e_ != cudaSuccess)                                                                      \
-            return fail(e_ == cudaErrorMemoryAllocation ? RB_ERR_OOM : RB_ERR_CUDA, "%s: %s (%s:%d)", \
-                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
-    } while (0)
+}  // namespace rb
 
-// Device memory comes from the device's stream-ordered pool (cudaMallocAsync
-// with an unbounded release threshold): relations, programs and results are
-// created and dropped per call on the e2e path, and plain cudaFree there
-// costs tens to hundreds of milliseconds.
-inline cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st) {
-    return cudaMallocAsync(p, std::max(bytes, (size_t)16), st);
-}
-inline void dev_free(void* p, cudaStream_t st) {
-    if (p) cudaFreeAsync(p, st);
-}
-
-struct DevBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    cudaError_t grow(size_t need, cudaStream_t st) {
-        if (need <= bytes) return cudaSuccess;
-        dev_free(p, st);
-        p = nullptr;
-        bytes = 0;
-        size_t want = std::max(need, (size_t)256);
-        cudaError_t e = dev_alloc(&p, want, st);
-        if (e == cudaSuccess) bytes = want;
-        return e;
-    }
-    void release(cudaStream_t st) {
-        dev_free(p, st);
-        p = nullptr;
-        bytes = 0;
-    }
-};
-
-// Growable array in pinned host memory: the work items are built straight
-// into it and copied to the device asynchronously at full link speed (a
-// batch of many small partitions has one item per partition).  Reused by
-// every run on the context; a run synchronises its stream before returning,
-// so the buffer is never overwritten under an in-flight copy.
-template <typename T>
-struct PinnedVec {
-    T* p = nullptr;
-    size_t n = 0, cap = 0;
-    bool failed = false;
-    void clear() { n = 0; }
-    void push_back(const T& v) {
-        if (n == cap && !grow(cap ? 2 * cap : 4096)) return;
-        p[n++] = v;
-    }
-    bool grow(size_t want) {
-        T* q = nullptr;
-        if (cudaMallocHost((void**)&q, sizeof(T) * want) != cudaSuccess) {
-            failed = true;
-            return false;
-        }
-        if (n) std::memcpy(q, p, sizeof(T) * n);
-        if (p) cudaFreeHost(p);
-        p = q;
-        cap = want;
-        return true;
-    }
-    void release() {
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        n = cap = 0;
-    }
-    size_t size() const { return n; }
-    const T* data() const { return p; }
-};
-
-}  // namespace
-
-struct rb_ctx {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    bool own_stream = false;
-    int sm_count = 0;
-    int blocks_per_sm = 1;
-    DevBuf items, refs, counters, scratch, surv, offs;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr;
-    // output buffers of the last destroyed result, reused by the next run
-    int32_t* pool[3] = {nullptr, nullptr, nullptr};
-    long long pool_cap = 0;
-    unsigned long long* host_ctr = nullptr;  // pinned: counters read back after each run
-    PinnedVec<Item> host_items;              // the last run's work items
-};
-
-struct rb_rel {
-    rb_ctx* ctx = nullptr;
-    int64_t n = 0;
-    std::vector<DevColumn> cols;
-    std::vector<int64_t> max_len;
-    std::vector<double> mean_len;
-    std::vector<void*> allocs;
-    void* d_cols = nullptr;
-    bool cols_dirty = true;
-};
-
-struct rb_prog {
-    rb_ctx* ctx = nullptr;
-    rb_rel* rel = nullptr;
-    FilterPlan F{};
-    VerifyProg V{};
-    int32_t n_slots = 0;
-    int64_t lmax_edit = -1;  // longest string any edit slot reads (-1: no edit slot)
-    std::vector<void*> allocs;
-    JitKernel jit;
-    JitKernel jit_small;  // 2-row variant for batches of small partitions (compiled on first use)
-    bool jit_small_tried = false;
-    // ungated variants, used once a run showed the stage-1 gate passing almost
-    // every warp iteration (its tests never fail inside these partitions)
-    JitKernel jit_nogate, jit_small_nogate;
-    bool jit_nogate_tried = false, jit_small_nogate_tried = false;
-    JitKernel jit_packed;  // 2-row variant taking packed items: batches of tiny partitions
-    bool jit_packed_tried = false;
-    bool gate_off = false;
-    long long last_rows = 0;  // output size of the previous run: sizes the next buffer
-    long long last_surv = 0;  // survivors of the previous run: sizes the deferred-verification buffer
-    double surv_rate = -1.0;  // survivors per work item in the previous run (-1: none yet)
-    // item ranges that fit the survivor buffer in the previous run, and its item count: a
-    // run over the same items (a repeated batch) replays them instead of re-learning where
-    // the survivors concentrate (each range that overflows is re-run)
-    std::vector<std::pair<int, int>> last_ranges;
-    int last_n_items = -1;
-    std::mutex ranges_mu;  // guards last_ranges / last_n_items (a program may be run from several threads)
-};
-
-struct rb_result {
-    rb_ctx* ctx = nullptr;
-    long long cap = 0;
-    int64_t count = 0;
-    int32_t* d_t = nullptr;
-    int32_t* d_s = nullptr;
-    int32_t* d_r = nullptr;
-    int32_t* d_p = nullptr;  // batched runs: partition index per row
-    cudaStream_t stream = nullptr;
-    rb_stats stats{};
-};
+using rb::g_err;
 
 extern "C" {
 
@@ -252,6 +112,7 @@ int rb_ctx_destroy(rb_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->host_ctr) cudaFreeHost(c->host_ctr);
     c->host_items.release();
+    c->host_offs.release();
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return RB_OK;
@@ -952,24 +813,26 @@ int rb_program_destroy(rb_prog* P) {
 // ---------------------------------------------------------------------------
 // runs
 
-struct Part {
-    int64_t base, n, split;  // split < 0: a partition; else cross, left = [base, base+split)
-};
+}  // extern "C"
 
 // RB_HOST_TIMING=1: host-side phase times of every run on stderr (diagnostics)
 static double host_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
-               int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out) {
+int rb::run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
+            int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device) {
     if (!c || !rel || !P || !out) return fail(RB_ERR_INVALID, "run: null argument");
+    // every run on a context shares its scratch (items, counters, survivor
+    // buffer, output pool) and its program's adaptive state: one at a time
+    std::lock_guard<std::mutex> ctx_lock(c->mu);
     if (P->rel != rel || rel->ctx != c) return fail(RB_ERR_INVALID, "run: program/relation/context mismatch");
     if (total < 0 || total > INT32_MAX) return fail(RB_ERR_INVALID, "run: partition size out of range");
     // tuple refs are range-checked on the device (refs_check_kernel, ahead of
     // the pair kernel, which then does nothing); the host scans only to name
     // the bad position (bad_refs below)
     auto bad_refs = [&]() {
+        if (refs_on_device) return fail(RB_ERR_INVALID, "tuple ref outside the relation");
         for (int64_t k = 0; k < total; k++)
             if (refs[k] < 0 || refs[k] >= rel->n)
                 return fail(RB_ERR_INVALID, "tuple ref %d at position %lld outside the relation", refs[k],
@@ -1014,12 +877,12 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
             const Part& pt = parts[pi];
             const bool cross = pt.split >= 0;
             const int32_t mode = cross ? MODE_CROSS : ((flags & RB_SYMMETRIC) ? MODE_SYM : MODE_ASYM);
-            const int64_t end = pt.base + pt.n;
+            const int64_t end = cross ? pt.rbase + (pt.n - pt.split) : pt.base + pt.n;
             const int64_t rlo = pt.base + std::max<int64_t>(0, row_lo);
             const int64_t rhi = pt.base + std::min<int64_t>(row_hi, cross ? pt.split : pt.n);
             for (int64_t r0 = rlo; r0 < rhi; r0 += rows_per_item) {
                 const int64_t rend = std::min<int64_t>(r0 + rows_per_item, rhi);
-                int64_t c0 = cross ? pt.base + pt.split : (mode == MODE_SYM ? r0 + 1 : pt.base);
+                int64_t c0 = cross ? pt.rbase : (mode == MODE_SYM ? r0 + 1 : pt.base);
                 for (; c0 < end; c0 += chunk, k++) {
                     if (!at) continue;
                     Item& it = at[k];
@@ -1070,7 +933,10 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         for (size_t pi = p0; pi < p1; pi++) {
             const Part& pt = parts[pi];
             if (pt.split < 0 && pt.n >= 2 && pt.n <= pack_max && pt.n <= rows_per_item) {  // a pack fits one item
-                if (n_in && rows + pt.n > rows_per_item) close();
+                // a pack covers consecutive positions: parts must follow each other in refs
+                if (n_in && (rows + pt.n > rows_per_item ||
+                             parts[first + n_in - 1].base + parts[first + n_in - 1].n != pt.base))
+                    close();
                 if (!n_in) first = pi;
                 n_in++;
                 rows += pt.n;
@@ -1170,7 +1036,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     }
 
     if (cudaError_t e = c->items.grow(sizeof(Item) * items.size(), c->stream)) return cleanup(fail(RB_ERR_CUDA, "items: %s", cudaGetErrorString(e)));
-    if (refs)
+    if (refs && !refs_on_device)
         if (cudaError_t e = c->refs.grow(sizeof(int32_t) * n, c->stream)) return cleanup(fail(RB_ERR_CUDA, "refs: %s", cudaGetErrorString(e)));
     // counters: [0] item counter (u32, padded), [1] out_count, [2] pairs, [3] survivors, [4..68) slot evals,
     // [68] entries appended to the deferred survivor buffer
@@ -1208,18 +1074,27 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
                                 (long long)(sizeof(int32_t) * stride * slices), cudaGetErrorString(e)));
     }
 
-    if (packed_items) {  // start position of every part (+ the end) for the packed items' row -> part lookup
-        std::vector<int32_t> po(parts.size() + 1);
-        for (size_t k = 0; k < parts.size(); k++) po[k] = (int32_t)parts[k].base;
-        po[parts.size()] = (int32_t)total;
-        if (cudaError_t e = c->offs.grow(sizeof(int32_t) * po.size(), c->stream))
+    if (packed_items) {  // start and end position of every part: the packed items' row -> part lookup
+        PinnedVec<int32_t>& po = c->host_offs;  // pinned: the copy stays asynchronous
+        const size_t np = parts.size();
+        po.clear();
+        if (2 * np + 1 > po.cap && !po.grow(2 * np + 1))
+            return cleanup(fail(RB_ERR_OOM, "pinned part offsets (%zu)", 2 * np + 1));
+        for (size_t k = 0; k < np; k++) {
+            po.p[k] = (int32_t)parts[k].base;
+            po.p[np + 1 + k] = (int32_t)(parts[k].base + parts[k].n);
+        }
+        po.p[np] = (int32_t)total;
+        po.n = 2 * np + 1;
+        if (cudaError_t e = c->offs.grow(sizeof(int32_t) * po.n, c->stream))
             return cleanup(fail(RB_ERR_CUDA, "part offsets: %s", cudaGetErrorString(e)));
-        CK(cudaMemcpyAsync(c->offs.p, po.data(), sizeof(int32_t) * po.size(), cudaMemcpyHostToDevice, c->stream));
-        CK(cudaStreamSynchronize(c->stream));  // po is a local (pageable) vector
+        CK(cudaMemcpyAsync(c->offs.p, po.p, sizeof(int32_t) * po.n, cudaMemcpyHostToDevice, c->stream));
     }
     mark();  // [2] items built, device buffers sized
     CK(cudaMemcpyAsync(c->items.p, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice, c->stream));
-    if (refs) CK(cudaMemcpyAsync(c->refs.p, refs, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    if (refs && !refs_on_device)
+        CK(cudaMemcpyAsync(c->refs.p, refs, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    const int32_t* d_refs = refs_on_device ? refs : (const int32_t*)c->refs.p;
 
     // output rows: the previous run's count + 25%, at least RB_OUT_MIN (1M; tests lower it
     // to drive the grow-in-place path)
@@ -1260,12 +1135,12 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         std::vector<unsigned long long> base(n_counters, 0);  // counters after the last completed range
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * n_counters, c->stream));
         if (refs) {
-            CK(launch_refs_check((const int32_t*)c->refs.p, n, rel->n, &ctr[BAD], c->stream));
+            CK(launch_refs_check(d_refs, n, rel->n, &ctr[BAD], c->stream));
             res->stats.launches += 1;
         }
         RunParams R{};
         R.bad_refs = refs ? &ctr[BAD] : nullptr;
-        R.refs = refs ? (const int32_t*)c->refs.p : nullptr;
+        R.refs = refs ? d_refs : nullptr;
         R.n = n;
         R.flags = flags;
         R.item_counter = (unsigned int*)&ctr[0];
@@ -1278,6 +1153,7 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         R.surv_count = &ctr[SURV];
         R.stat_gate = &ctr[GATE];
         R.part_off = packed_items ? (const int32_t*)c->offs.p : nullptr;
+        R.part_end = packed_items ? (const int32_t*)c->offs.p + parts.size() + 1 : nullptr;
         const long long per_row = (flags & RB_ENUMERATE) ? std::max(1, P->F.n_rules) : 1;
         // Ranges are sized from the survivors per item seen so far (the
         // program's previous run, else a probe of 1/64 of the items), so a
@@ -1479,13 +1355,13 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
         }
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * n_counters, c->stream));
         if (refs) {
-            CK(launch_refs_check((const int32_t*)c->refs.p, n, rel->n, &ctr[BAD], c->stream));
+            CK(launch_refs_check(d_refs, n, rel->n, &ctr[BAD], c->stream));
             res->stats.launches += 1;
         }
 
         RunParams R{};
         R.bad_refs = refs ? &ctr[BAD] : nullptr;
-        R.refs = refs ? (const int32_t*)c->refs.p : nullptr;
+        R.refs = refs ? d_refs : nullptr;
         R.n = n;
         R.flags = flags;
         R.items = (const Item*)c->items.p;
@@ -1541,14 +1417,16 @@ static int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t 
     return RB_OK;
 }
 
+extern "C" {
+
 int rb_run_partition(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t n, uint32_t flags,
                      rb_result** out) {
-    return run(c, rel, P, refs, n, {Part{0, n, -1}}, 0, n, flags, false, out);
+    return run(c, rel, P, refs, n, {Part{0, n, -1, 0}}, 0, n, flags, false, out);
 }
 
 int rb_run_partition_rows(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t n, int64_t row_lo,
                           int64_t row_hi, uint32_t flags, rb_result** out) {
-    return run(c, rel, P, refs, n, {Part{0, n, -1}}, row_lo, row_hi, flags, false, out);
+    return run(c, rel, P, refs, n, {Part{0, n, -1, 0}}, row_lo, row_hi, flags, false, out);
 }
 
 int rb_run_cross(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* left, int64_t nl, const int32_t* right,
@@ -1557,7 +1435,7 @@ int rb_run_cross(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* left, int64_
     std::vector<int32_t> both((size_t)(nl + nr));
     if (nl) memcpy(both.data(), left, sizeof(int32_t) * nl);
     if (nr) memcpy(both.data() + nl, right, sizeof(int32_t) * nr);
-    return run(c, rel, P, both.data(), nl + nr, {Part{0, nl + nr, nl}}, 0, nl + nr, flags, false, out);
+    return run(c, rel, P, both.data(), nl + nr, {Part{0, nl + nr, nl, nl}}, 0, nl + nr, flags, false, out);
 }
 
 int rb_run_batch(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, const int64_t* offsets,
@@ -1571,7 +1449,7 @@ int rb_run_batch(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, const 
         if (len < 0) return fail(RB_ERR_INVALID, "rb_run_batch: offsets not monotone at %d", k);
         const int64_t sp = splits ? splits[k] : -1;
         if (sp > len) return fail(RB_ERR_INVALID, "rb_run_batch: split %lld beyond part %d", (long long)sp, k);
-        parts.push_back(Part{offsets[k], len, sp});
+        parts.push_back(Part{offsets[k], len, sp, sp >= 0 ? offsets[k] + sp : 0});
     }
     const int64_t total = n_parts ? offsets[n_parts] : 0;
     return run(c, rel, P, refs, total, parts, 0, INT64_MAX, flags, true, out);
@@ -1624,6 +1502,8 @@ int rb_result_stats(const rb_result* r, rb_stats* out) {
 int rb_result_destroy(rb_result* r) {
     if (!r) return RB_OK;
     rb_ctx* c = r->ctx;
+    std::unique_lock<std::mutex> lock;
+    if (c) lock = std::unique_lock<std::mutex>(c->mu);  // the pool is context state
     if (c && r->d_t && r->cap > c->pool_cap) {  // keep the larger buffers for the next run
         for (int k = 0; k < 3; k++) dev_free(c->pool[k], r->stream);
         c->pool[0] = r->d_t;

@@ -214,6 +214,7 @@ struct RunParams {
     unsigned long long* surv_count;
     const unsigned long long* bad_refs;  // non-zero: a tuple ref is out of range, evaluate nothing
     const int32_t* part_off;  // packed items: start position of every part of the batch (+ the end)
+    const int32_t* part_end;  // packed items: end position of every part (parts of a pack are adjacent)
 };
 
 // the part of a packed item (parts [lo, hi)) holding position pos
@@ -753,7 +754,7 @@ struct Outer {
             // symmetric: the later rows of its own partition; asymmetric: every other row of it
             const int k = find_part(R, part_lo, part_hi, i);
             pbeg = (R.flags & RB_SYMMETRIC) ? (int32_t)i + 1 : __ldg(R.part_off + k);
-            pend = __ldg(R.part_off + k + 1);
+            pend = __ldg(R.part_end + k);
             my_pairs += (unsigned long long)(pend - pbeg - (pbeg <= i ? 1 : 0));
         }
 #endif

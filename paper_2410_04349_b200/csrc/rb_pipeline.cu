@@ -1,0 +1,569 @@
+// rb_pipeline.cu -- the callers on either side of the evaluation path, on the
+// device: plan-derived partitioning and the collect step.
+//
+//   partitioning  pkg/src/ruleblock/partitioning.py:93-131 (iter_partitions)
+//                 and 144-157 (sibling_pull_pairs)
+//   collect       pkg/src/ruleblock/pipeline.py:407-421
+//
+// Partitioning a branch is a stable radix sort of (key, tid) -- equal keys
+// become one group with its tuple ids ascending, groups in key order -- a
+// run-length pass for the group sizes, and a round-robin deal of every
+// oversize group into contiguous sibling ranges.  The sorted tuple ids stay
+// in HBM as the refs of the batched run; only the group sizes come back to
+// the host, which lays out the partition list (the run's work items are
+// built from it as for rb_run_batch).  Collect sorts the rows on one 64-bit
+// key ((t, s) then the rule index) and keeps the first row of every (t, s):
+// the earliest rule in rule-set order, as the reference's lexsort + keep.
+// All of it is HBM streaming (sort passes): no tensor-core work here.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_select.cuh>
+
+#include <numeric>
+#include <queue>
+
+#include "rb_state.cuh"
+
+using namespace rb;
+
+struct rb_parts {
+    rb_ctx* ctx = nullptr;
+    int64_t n = 0;            // tuples per branch
+    int32_t n_branches = 0;
+    int32_t* d_refs = nullptr;  // n_branches * n tuple ids, branch by branch
+    std::vector<Part> parts;    // partitions (in iter_partitions order), then pulls
+    std::vector<int32_t> branch, sibling;
+    int64_t n_partitions = 0, n_pulls = 0, n_groups = 0;
+};
+
+namespace {
+
+constexpr int PB = 256;  // threads per block of the streaming kernels
+
+int grid_for(int64_t n, int sms) {
+    const int64_t g = (n + PB - 1) / PB;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)sms * 8));
+}
+
+int bits_for(uint64_t v) {
+    int b = 0;
+    while (b < 64 && (v >> b)) b++;
+    return b;
+}
+
+// key of tuple tid: codes (int32, < 0 = missing: one group, ordered first)
+// or int64 keys shifted by their minimum; ids 0..n-1 as the sort values
+__global__ void keys_from_codes(const int32_t* __restrict__ codes, int64_t n, uint64_t* __restrict__ key,
+                                int32_t* __restrict__ tid) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = __ldg(codes + i);
+        key[i] = c < 0 ? 0ull : (uint64_t)c + 1ull;
+        tid[i] = (int32_t)i;
+    }
+}
+
+__global__ void keys_from_int64(const int64_t* __restrict__ in, int64_t n, int64_t lo, uint64_t* __restrict__ key,
+                                int32_t* __restrict__ tid) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        key[i] = (uint64_t)(in[i] - lo);
+        tid[i] = (int32_t)i;
+    }
+}
+
+__global__ void minmax_int64(const int64_t* __restrict__ in, int64_t n, unsigned long long* out) {
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        lo = min(lo, (long long)in[i]);
+        hi = max(hi, (long long)in[i]);
+    }
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        // order-preserving map of signed to unsigned for the atomics
+        atomicMin(out, (unsigned long long)lo ^ 0x8000000000000000ull);
+        atomicMax(out + 1, (unsigned long long)hi ^ 0x8000000000000000ull);
+    }
+}
+
+// Deal every oversize group round-robin into k contiguous siblings:
+// element i of the group goes to sibling i % k at index i / k
+// (refs[sub::n_parts], partitioning.py:121-131).  One CTA per group.
+struct Deal {
+    int64_t start, m, k;
+};
+__global__ void deal_siblings(const Deal* __restrict__ deals, const int32_t* __restrict__ src, int32_t* __restrict__ dst) {
+    const Deal d = deals[blockIdx.x];
+    const int64_t q = d.m / d.k, r = d.m % d.k;
+    for (int64_t i = threadIdx.x; i < d.m; i += blockDim.x) {
+        const int64_t sub = i % d.k, idx = i / d.k;
+        const int64_t pos = sub * q + (sub < r ? sub : r) + idx;
+        dst[d.start + pos] = src[d.start + i];
+    }
+}
+
+// collect: rows -> one sortable key (t, s, rule) when it fits 64 bits
+__global__ void pack_rows(const int32_t* __restrict__ t, const int32_t* __restrict__ s, const int32_t* __restrict__ r,
+                          int64_t k, int sb, int rb, uint64_t* __restrict__ key) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+        key[i] = ((((uint64_t)(uint32_t)t[i] << sb) | (uint64_t)(uint32_t)s[i]) << rb) | (uint64_t)(uint32_t)r[i];
+}
+
+// first row of every (t, s) run of the sorted keys
+__global__ void flag_firsts(const uint64_t* __restrict__ key, int64_t k, int rb, uint8_t* __restrict__ flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = (i == 0 || (key[i] >> rb) != (key[i - 1] >> rb)) ? 1 : 0;
+}
+
+__global__ void unpack_rows(const uint64_t* __restrict__ key, const int64_t* __restrict__ count, int sb, int rb,
+                            int32_t* __restrict__ t, int32_t* __restrict__ s, int32_t* __restrict__ r) {
+    const int64_t k = *count;
+    const uint64_t smask = (sb >= 64) ? ~0ull : ((1ull << sb) - 1), rmask = rb ? ((1ull << rb) - 1) : 0ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = key[i];
+        r[i] = (int32_t)(x & rmask);
+        s[i] = (int32_t)((x >> rb) & smask);
+        t[i] = (int32_t)(x >> (rb + sb));
+    }
+}
+
+// wide keys: (t, s) sorted with the rule as value; the smallest rule per run
+__global__ void pack_ts(const int32_t* __restrict__ t, const int32_t* __restrict__ s, int64_t k,
+                        uint64_t* __restrict__ key) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+        key[i] = ((uint64_t)(uint32_t)t[i] << 32) | (uint64_t)(uint32_t)s[i];
+}
+
+__global__ void min_rule_runs(const uint64_t* __restrict__ key, const int32_t* __restrict__ rule, int64_t k,
+                              uint64_t* __restrict__ out_key, int32_t* __restrict__ out_rule, uint8_t* __restrict__ flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        const bool first = i == 0 || key[i] != key[i - 1];
+        flag[i] = first ? 1 : 0;
+        if (!first) continue;
+        int32_t m = rule[i];
+        for (int64_t j = i + 1; j < k && key[j] == key[i]; j++) m = min(m, rule[j]);
+        out_key[i] = key[i];
+        out_rule[i] = m;
+    }
+}
+
+__global__ void unpack_ts(const uint64_t* __restrict__ key, const int32_t* __restrict__ rule,
+                          const int64_t* __restrict__ count, int32_t* __restrict__ t, int32_t* __restrict__ s,
+                          int32_t* __restrict__ r) {
+    const int64_t k = *count;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        t[i] = (int32_t)(key[i] >> 32);
+        s[i] = (int32_t)(key[i] & 0xffffffffull);
+        r[i] = rule[i];
+    }
+}
+
+// scoped stream-ordered scratch
+struct Scratch {
+    cudaStream_t st;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t s) : st(s) {}
+    template <typename T>
+    cudaError_t get(T** p, size_t count) {
+        void* q = nullptr;
+        cudaError_t e = dev_alloc(&q, sizeof(T) * std::max<size_t>(count, 1), st);
+        if (e == cudaSuccess) ptrs.push_back(q);
+        *p = (T*)q;
+        return e;
+    }
+    ~Scratch() {
+        for (void* p : ptrs) dev_free(p, st);
+    }
+};
+
+#define CKS(call)                                                                                   \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail(e_ == cudaErrorMemoryAllocation ? RB_ERR_OOM : RB_ERR_CUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+    } while (0)
+
+// One branch: sort, run-length groups, deal oversize groups; appends the
+// branch's partitions to P (positions offset by `base`), returns the sibling
+// ranges of every oversize group for the pulls.
+int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, int key_bits, int64_t base,
+                     int32_t branch, int64_t maxp, int& sibling_counter,
+                     std::vector<std::vector<std::pair<int64_t, int64_t>>>& sib_ranges) {
+    rb_ctx* c = P->ctx;
+    cudaStream_t st = c->stream;
+    const int64_t n = P->n;
+    Scratch S(st);
+    uint64_t *key_out, *uniq;
+    int32_t *counts, *tid_out;
+    int64_t* d_runs;
+    CKS(S.get(&key_out, n));
+    CKS(S.get(&tid_out, n));
+    CKS(S.get(&uniq, n));
+    CKS(S.get(&counts, n));
+    CKS(S.get(&d_runs, 1));
+    size_t tb1 = 0, tb2 = 0;
+    CKS(cub::DeviceRadixSort::SortPairs(nullptr, tb1, d_key_in, key_out, d_tid_in, tid_out, n, 0,
+                                        std::max(1, key_bits), st));
+    CKS(cub::DeviceRunLengthEncode::Encode(nullptr, tb2, key_out, uniq, counts, d_runs, n, st));
+    void* temp;
+    CKS(S.get((char**)&temp, std::max(tb1, tb2)));
+    size_t tb = std::max(tb1, tb2);
+    CKS(cub::DeviceRadixSort::SortPairs(temp, tb, d_key_in, key_out, d_tid_in, tid_out, n, 0,
+                                        std::max(1, key_bits), st));
+    tb = std::max(tb1, tb2);
+    CKS(cub::DeviceRunLengthEncode::Encode(temp, tb, key_out, uniq, counts, d_runs, n, st));
+    int64_t runs = 0;
+    CKS(cudaMemcpyAsync(&runs, d_runs, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CKS(cudaStreamSynchronize(st));
+    std::vector<int32_t> h_counts((size_t)runs);
+    if (runs) CKS(cudaMemcpyAsync(h_counts.data(), counts, sizeof(int32_t) * runs, cudaMemcpyDeviceToHost, st));
+    int32_t* dst = P->d_refs + base;
+    CKS(cudaMemcpyAsync(dst, tid_out, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+    CKS(cudaStreamSynchronize(st));
+    std::vector<Deal> deals;
+    int64_t start = 0;
+    for (int64_t g = 0; g < runs; g++) {
+        const int64_t m = h_counts[(size_t)g];
+        if (m <= maxp) {
+            P->parts.push_back(Part{base + start, m, -1, 0});
+            P->branch.push_back(branch);
+            P->sibling.push_back(0);
+        } else {
+            const int64_t k = (m + maxp - 1) / maxp, q = m / k, r = m % k;
+            deals.push_back(Deal{start, m, k});  // positions relative to the branch
+            sibling_counter++;
+            std::vector<std::pair<int64_t, int64_t>> ranges;
+            int64_t at = base + start;
+            for (int64_t sub = 0; sub < k; sub++) {
+                const int64_t sz = q + (sub < r ? 1 : 0);
+                P->parts.push_back(Part{at, sz, -1, 0});
+                P->branch.push_back(branch);
+                P->sibling.push_back(sibling_counter);
+                ranges.push_back({at, sz});
+                at += sz;
+            }
+            sib_ranges.push_back(std::move(ranges));
+        }
+        start += m;
+    }
+    P->n_groups += runs;
+    if (!deals.empty()) {
+        // the deal reads the sorted ids (tid_out) and rewrites the oversize groups of dst
+        Deal* d_deals;
+        CKS(S.get(&d_deals, deals.size()));
+        CKS(cudaMemcpyAsync(d_deals, deals.data(), sizeof(Deal) * deals.size(), cudaMemcpyHostToDevice, st));
+        deal_siblings<<<(unsigned)deals.size(), 512, 0, st>>>(d_deals, tid_out, dst);
+        CKS(cudaGetLastError());
+        CKS(cudaStreamSynchronize(st));  // deals is a host vector
+    }
+    return RB_OK;
+}
+
+int finish_pulls(rb_parts* P, bool pulls, const std::vector<std::vector<std::pair<int64_t, int64_t>>>& sib_ranges,
+                 const std::vector<int32_t>& sib_branch) {
+    P->n_partitions = (int64_t)P->parts.size();
+    if (!pulls) return RB_OK;
+    int gid = 0;
+    for (size_t g = 0; g < sib_ranges.size(); g++) {
+        const auto& rg = sib_ranges[g];
+        gid++;
+        for (size_t i = 0; i < rg.size(); i++)
+            for (size_t j = i + 1; j < rg.size(); j++) {
+                P->parts.push_back(Part{rg[i].first, rg[i].second + rg[j].second, rg[i].second, rg[j].first});
+                P->branch.push_back(sib_branch[g]);
+                P->sibling.push_back(gid);
+                P->n_pulls++;
+            }
+    }
+    return RB_OK;
+}
+
+int partition_impl(rb_ctx* c, rb_rel* rel, const int32_t* cols, const int64_t* keys, const int32_t* branch_ids,
+                   int32_t nb, int64_t maxp, uint32_t flags, rb_parts** out) {
+    if (!c || !rel || !out || nb < 1 || (!cols && !keys)) return fail(RB_ERR_INVALID, "rb_partition: bad arguments");
+    if (rel->ctx != c) return fail(RB_ERR_INVALID, "rb_partition: relation belongs to another context");
+    if (maxp < 1) return fail(RB_ERR_INVALID, "max_partition_size must be >= 1");
+    const int64_t n = rel->n;
+    if ((int64_t)nb * n > INT32_MAX) return fail(RB_ERR_LIMIT, "%d branches x %lld tuples exceed the run's position range", nb, (long long)n);
+    if (cols)
+        for (int b = 0; b < nb; b++)
+            if (cols[b] < 0 || cols[b] >= (int)rel->cols.size() || rel->cols[cols[b]].kind != RB_COL_CODES)
+                return fail(RB_ERR_INVALID, "rb_partition_codes: column %d is not a codes column", cols[b]);
+    CKS(cudaSetDevice(c->device));
+    std::lock_guard<std::mutex> lock(c->mu);
+    rb_parts* P = new (std::nothrow) rb_parts();
+    if (!P) return fail(RB_ERR_OOM, "host allocation failed");
+    P->ctx = c;
+    P->n = n;
+    P->n_branches = nb;
+    cudaStream_t st = c->stream;
+    auto bail = [&](int rc) {
+        dev_free(P->d_refs, st);
+        delete P;
+        return rc;
+    };
+    if (cudaError_t e = dev_alloc((void**)&P->d_refs, sizeof(int32_t) * std::max<int64_t>(1, nb * n), st))
+        return bail(fail(RB_ERR_OOM, "partition refs: %s", cudaGetErrorString(e)));
+    int sibling_counter = 0;
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> sib_ranges;
+    std::vector<int32_t> sib_branch;
+    {
+        Scratch S(st);
+        uint64_t* key;
+        int32_t* tid;
+        int64_t* hkeys_dev = nullptr;
+        unsigned long long* mm = nullptr;
+        if (S.get(&key, n) || S.get(&tid, n) || S.get(&mm, 2) || (keys && !(flags & RB_PART_KEYS_DEVICE) && S.get(&hkeys_dev, n)))
+            return bail(fail(RB_ERR_OOM, "partition scratch for %lld tuples", (long long)n));
+        const int grid = grid_for(n, c->sm_count);
+        for (int b = 0; b < nb && n > 0; b++) {
+            const int32_t bid = branch_ids ? branch_ids[b] : b;
+            int key_bits;
+            if (cols) {
+                keys_from_codes<<<grid, PB, 0, st>>>(rel->cols[cols[b]].codes, n, key, tid);
+                key_bits = 32;
+            } else {
+                const int64_t* kin = keys + (size_t)b * n;
+                if (!(flags & RB_PART_KEYS_DEVICE)) {
+                    if (cudaError_t e = cudaMemcpyAsync(hkeys_dev, kin, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st))
+                        return bail(fail(RB_ERR_CUDA, "keys upload: %s", cudaGetErrorString(e)));
+                    kin = hkeys_dev;
+                }
+                unsigned long long init[2] = {~0ull, 0ull};
+                unsigned long long res[2];
+                if (cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, st) != cudaSuccess)
+                    return bail(fail(RB_ERR_CUDA, "keys min/max"));
+                minmax_int64<<<grid, PB, 0, st>>>(kin, n, mm);
+                if (cudaMemcpyAsync(res, mm, sizeof res, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                    cudaStreamSynchronize(st) != cudaSuccess)
+                    return bail(fail(RB_ERR_CUDA, "keys min/max: %s", cudaGetErrorString(cudaGetLastError())));
+                const int64_t lo = (int64_t)(res[0] ^ 0x8000000000000000ull), hi = (int64_t)(res[1] ^ 0x8000000000000000ull);
+                keys_from_int64<<<grid, PB, 0, st>>>(kin, n, lo, key, tid);
+                key_bits = bits_for((uint64_t)hi - (uint64_t)lo);
+            }
+            if (cudaError_t e = cudaGetLastError()) return bail(fail(RB_ERR_CUDA, "partition keys: %s", cudaGetErrorString(e)));
+            const size_t before = sib_ranges.size();
+            if (int rc = partition_branch(P, key, tid, key_bits, (int64_t)b * n, bid, maxp, sibling_counter, sib_ranges))
+                return bail(rc);
+            for (size_t g = before; g < sib_ranges.size(); g++) sib_branch.push_back(bid);
+        }
+    }
+    finish_pulls(P, (flags & RB_PART_PULLS) != 0, sib_ranges, sib_branch);
+    *out = P;
+    return RB_OK;
+}
+
+// rows (t, s, r)[k] -> sorted unique (t, s) with the smallest rule, into out_*; count in *out_k
+int collect_impl(rb_ctx* c, const int32_t* t, const int32_t* s, const int32_t* r, int64_t k, int64_t n_tuples,
+                 int32_t n_rules, int32_t* ot, int32_t* os, int32_t* orr, int64_t* out_k) {
+    cudaStream_t st = c->stream;
+    *out_k = 0;
+    if (k <= 0) return RB_OK;
+    const int sb = std::max(1, bits_for((uint64_t)std::max<int64_t>(1, n_tuples - 1)));
+    const int rb = bits_for((uint64_t)std::max(0, n_rules - 1));
+    const int grid = grid_for(k, c->sm_count);
+    Scratch S(st);
+    uint64_t *k0, *k1;
+    uint8_t* flag;
+    int64_t* d_cnt;
+    CKS(S.get(&k0, k));
+    CKS(S.get(&k1, k));
+    CKS(S.get(&flag, k));
+    CKS(S.get(&d_cnt, 1));
+    if (2 * sb + rb <= 64) {
+        pack_rows<<<grid, PB, 0, st>>>(t, s, r, k, sb, rb, k0);
+        CKS(cudaGetLastError());
+        size_t tb1 = 0, tb2 = 0;
+        CKS(cub::DeviceRadixSort::SortKeys(nullptr, tb1, k0, k1, k, 0, 2 * sb + rb, st));
+        CKS(cub::DeviceSelect::Flagged(nullptr, tb2, k1, flag, k0, d_cnt, k, st));
+        void* temp;
+        CKS(S.get((char**)&temp, std::max(tb1, tb2)));
+        size_t tb = std::max(tb1, tb2);
+        CKS(cub::DeviceRadixSort::SortKeys(temp, tb, k0, k1, k, 0, 2 * sb + rb, st));
+        flag_firsts<<<grid, PB, 0, st>>>(k1, k, rb, flag);
+        CKS(cudaGetLastError());
+        tb = std::max(tb1, tb2);
+        CKS(cub::DeviceSelect::Flagged(temp, tb, k1, flag, k0, d_cnt, k, st));
+        unpack_rows<<<grid, PB, 0, st>>>(k0, d_cnt, sb, rb, ot, os, orr);
+        CKS(cudaGetLastError());
+    } else {
+        int32_t *r1, *r2;
+        CKS(S.get(&r1, k));
+        CKS(S.get(&r2, k));
+        pack_ts<<<grid, PB, 0, st>>>(t, s, k, k0);
+        CKS(cudaGetLastError());
+        size_t tb1 = 0, tb2 = 0;
+        CKS(cub::DeviceRadixSort::SortPairs(nullptr, tb1, k0, k1, r, r1, k, 0, 64, st));
+        CKS(cub::DeviceSelect::Flagged(nullptr, tb2, k0, flag, k1, d_cnt, k, st));
+        void* temp;
+        CKS(S.get((char**)&temp, std::max(tb1, tb2)));
+        size_t tb = std::max(tb1, tb2);
+        CKS(cub::DeviceRadixSort::SortPairs(temp, tb, k0, k1, r, r1, k, 0, 64, st));
+        min_rule_runs<<<grid, PB, 0, st>>>(k1, r1, k, k0, r2, flag);
+        CKS(cudaGetLastError());
+        tb = std::max(tb1, tb2);
+        CKS(cub::DeviceSelect::Flagged(temp, tb, k0, flag, k1, d_cnt, k, st));
+        tb = std::max(tb1, tb2);
+        CKS(cub::DeviceSelect::Flagged(temp, tb, r2, flag, r1, d_cnt, k, st));
+        unpack_ts<<<grid, PB, 0, st>>>(k1, r1, d_cnt, ot, os, orr);
+        CKS(cudaGetLastError());
+    }
+    CKS(cudaMemcpyAsync(out_k, d_cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CKS(cudaStreamSynchronize(st));
+    return RB_OK;
+}
+
+int64_t pair_count(const Part& p, bool symmetric) {
+    if (p.split >= 0) return p.split * (p.n - p.split);
+    return symmetric ? p.n * (p.n - 1) / 2 : p.n * (p.n - 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+int rb_partition(rb_ctx* c, rb_rel* rel, const int64_t* keys, const int32_t* branch_ids, int32_t n_branches,
+                 int64_t max_partition_size, uint32_t flags, rb_parts** out) {
+    if (!keys) return fail(RB_ERR_INVALID, "rb_partition: keys is NULL");
+    return partition_impl(c, rel, nullptr, keys, branch_ids, n_branches, max_partition_size, flags, out);
+}
+
+int rb_partition_codes(rb_ctx* c, rb_rel* rel, const int32_t* cols, const int32_t* branch_ids, int32_t n_branches,
+                       int64_t max_partition_size, uint32_t flags, rb_parts** out) {
+    if (!cols) return fail(RB_ERR_INVALID, "rb_partition_codes: cols is NULL");
+    return partition_impl(c, rel, cols, nullptr, branch_ids, n_branches, max_partition_size, flags, out);
+}
+
+int rb_parts_info(const rb_parts* p, int64_t* n_partitions, int64_t* n_pulls, int64_t* n_refs, int64_t* n_groups) {
+    if (!p) return fail(RB_ERR_INVALID, "rb_parts_info: null parts");
+    if (n_partitions) *n_partitions = p->n_partitions;
+    if (n_pulls) *n_pulls = p->n_pulls;
+    if (n_refs) *n_refs = (int64_t)p->n_branches * p->n;
+    if (n_groups) *n_groups = p->n_groups;
+    return RB_OK;
+}
+
+int rb_parts_copy(const rb_parts* p, int32_t* refs, int64_t* base, int64_t* size, int64_t* split, int64_t* rbase,
+                  int32_t* branch, int32_t* sibling) {
+    if (!p) return fail(RB_ERR_INVALID, "rb_parts_copy: null parts");
+    rb_ctx* c = p->ctx;
+    CKS(cudaSetDevice(c->device));
+    if (refs && p->n) {
+        CKS(cudaMemcpyAsync(refs, p->d_refs, sizeof(int32_t) * p->n_branches * p->n, cudaMemcpyDeviceToHost, c->stream));
+        CKS(cudaStreamSynchronize(c->stream));
+    }
+    for (size_t k = 0; k < p->parts.size(); k++) {
+        const Part& q = p->parts[k];
+        if (base) base[k] = q.base;
+        if (size) size[k] = q.n;
+        if (split) split[k] = q.split;
+        if (rbase) rbase[k] = q.split >= 0 ? q.rbase : -1;
+        if (branch) branch[k] = p->branch[k];
+        if (sibling) sibling[k] = p->sibling[k];
+    }
+    return RB_OK;
+}
+
+int rb_parts_destroy(rb_parts* p) {
+    if (!p) return RB_OK;
+    cudaSetDevice(p->ctx->device);
+    {
+        std::lock_guard<std::mutex> lock(p->ctx->mu);
+        dev_free(p->d_refs, p->ctx->stream);
+        cudaStreamSynchronize(p->ctx->stream);
+    }
+    delete p;
+    return RB_OK;
+}
+
+int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int32_t rank, int32_t world,
+                 uint32_t flags, rb_result** out) {
+    if (!parts || !c || !out) return fail(RB_ERR_INVALID, "rb_run_parts: null argument");
+    if (parts->ctx != c) return fail(RB_ERR_INVALID, "rb_run_parts: parts belong to another context");
+    if (world < 1 || rank < 0 || rank >= world) return fail(RB_ERR_INVALID, "rb_run_parts: rank %d of %d", rank, world);
+    const bool sym = (flags & RB_SYMMETRIC) != 0;
+    // the evaluated units: partitions with pairs, and the pulls
+    std::vector<int64_t> units;
+    units.reserve(parts->parts.size());
+    for (size_t k = 0; k < parts->parts.size(); k++)
+        if (pair_count(parts->parts[k], sym) > 0) units.push_back((int64_t)k);
+    std::vector<Part> mine;
+    if (world == 1) {
+        mine.reserve(units.size());
+        for (int64_t k : units) mine.push_back(parts->parts[(size_t)k]);
+    } else {
+        // static longest-processing-time placement on pair counts (the same on
+        // every rank): units in descending cost to the least-loaded rank
+        std::vector<int64_t> order(units);
+        std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+            return pair_count(parts->parts[(size_t)a], sym) > pair_count(parts->parts[(size_t)b], sym);
+        });
+        using L = std::pair<int64_t, int32_t>;  // (load, rank)
+        std::priority_queue<L, std::vector<L>, std::greater<L>> heap;
+        for (int32_t w = 0; w < world; w++) heap.push({0, w});
+        std::vector<uint8_t> take(parts->parts.size(), 0);
+        for (int64_t k : order) {
+            L top = heap.top();
+            heap.pop();
+            if (top.second == rank) take[(size_t)k] = 1;
+            top.first += pair_count(parts->parts[(size_t)k], sym);
+            heap.push(top);
+        }
+        for (int64_t k : units)
+            if (take[(size_t)k]) mine.push_back(parts->parts[(size_t)k]);
+    }
+    return run(c, rel, P, parts->d_refs, (int64_t)parts->n_branches * parts->n, mine, 0, INT64_MAX, flags, false, out,
+               true);
+}
+
+int rb_result_collect(rb_result* res, int64_t n_tuples, int32_t n_rules) {
+    if (!res) return fail(RB_ERR_INVALID, "rb_result_collect: null result");
+    if (n_tuples < 0 || n_tuples > INT32_MAX || n_rules < 1) return fail(RB_ERR_INVALID, "rb_result_collect: bad sizes");
+    if (res->count == 0) return RB_OK;
+    rb_ctx* c = res->ctx;
+    CKS(cudaSetDevice(c->device));
+    std::lock_guard<std::mutex> lock(c->mu);
+    const int64_t k = res->count;
+    int32_t *t = nullptr, *s = nullptr, *r = nullptr;
+    cudaError_t e = dev_alloc((void**)&t, sizeof(int32_t) * k, c->stream);
+    if (!e) e = dev_alloc((void**)&s, sizeof(int32_t) * k, c->stream);
+    if (!e) e = dev_alloc((void**)&r, sizeof(int32_t) * k, c->stream);
+    if (e) {
+        dev_free(t, c->stream);
+        dev_free(s, c->stream);
+        dev_free(r, c->stream);
+        return fail(RB_ERR_OOM, "collect output of %lld rows: %s", (long long)k, cudaGetErrorString(e));
+    }
+    int64_t kept = 0;
+    if (int rc = collect_impl(c, res->d_t, res->d_s, res->d_r, k, n_tuples, n_rules, t, s, r, &kept)) {
+        dev_free(t, c->stream);
+        dev_free(s, c->stream);
+        dev_free(r, c->stream);
+        return rc;
+    }
+    dev_free(res->d_t, c->stream);
+    dev_free(res->d_s, c->stream);
+    dev_free(res->d_r, c->stream);
+    dev_free(res->d_p, c->stream);
+    res->d_t = t;
+    res->d_s = s;
+    res->d_r = r;
+    res->d_p = nullptr;
+    res->cap = k;
+    res->count = kept;
+    return RB_OK;
+}
+
+int rb_collect_device(rb_ctx* c, const int32_t* t, const int32_t* s, const int32_t* r, int64_t count, int64_t n_tuples,
+                      int32_t n_rules, int32_t* out_t, int32_t* out_s, int32_t* out_r, int64_t* out_count) {
+    if (!c || !out_count || (count > 0 && (!t || !s || !r || !out_t || !out_s || !out_r)))
+        return fail(RB_ERR_INVALID, "rb_collect_device: null argument");
+    if (n_tuples < 0 || n_tuples > INT32_MAX || n_rules < 1) return fail(RB_ERR_INVALID, "rb_collect_device: bad sizes");
+    CKS(cudaSetDevice(c->device));
+    std::lock_guard<std::mutex> lock(c->mu);
+    return collect_impl(c, t, s, r, count, n_tuples, n_rules, out_t, out_s, out_r, out_count);
+}
+
+}  // extern "C"

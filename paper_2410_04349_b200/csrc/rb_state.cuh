@@ -1,0 +1,197 @@
+// rb_state.cuh -- host-side state behind the C ABI handles (rb_ctx, rb_rel,
+// rb_prog, rb_result) shared by rb_api.cu (relations, programs, runs) and
+// rb_pipeline.cu (device partitioning and collect).  Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "rb_internal.cuh"
+
+namespace rb {
+
+// records the message of the last failure on the calling thread (rb_last_error)
+int fail(int code, const char* fmt, ...);
+
+#define CK(call)                                                                                    \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail(e_ == cudaErrorMemoryAllocation ? RB_ERR_OOM : RB_ERR_CUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+    } while (0)
+
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync
+// with an unbounded release threshold): relations, programs and results are
+// created and dropped per call on the e2e path, and plain cudaFree there
+// costs tens to hundreds of milliseconds.
+inline cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st) {
+    return cudaMallocAsync(p, std::max(bytes, (size_t)16), st);
+}
+inline void dev_free(void* p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t grow(size_t need, cudaStream_t st) {
+        if (need <= bytes) return cudaSuccess;
+        dev_free(p, st);
+        p = nullptr;
+        bytes = 0;
+        size_t want = std::max(need, (size_t)256);
+        cudaError_t e = dev_alloc(&p, want, st);
+        if (e == cudaSuccess) bytes = want;
+        return e;
+    }
+    void release(cudaStream_t st) {
+        dev_free(p, st);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+// Growable array in pinned host memory: the work items are built straight
+// into it and copied to the device asynchronously at full link speed (a
+// batch of many small partitions has one item per partition).  Reused by
+// every run on the context; a run synchronises its stream before returning,
+// so the buffer is never overwritten under an in-flight copy.
+template <typename T>
+struct PinnedVec {
+    T* p = nullptr;
+    size_t n = 0, cap = 0;
+    bool failed = false;
+    void clear() { n = 0; }
+    void push_back(const T& v) {
+        if (n == cap && !grow(cap ? 2 * cap : 4096)) return;
+        p[n++] = v;
+    }
+    bool grow(size_t want) {
+        T* q = nullptr;
+        if (cudaMallocHost((void**)&q, sizeof(T) * want) != cudaSuccess) {
+            failed = true;
+            return false;
+        }
+        if (n) std::memcpy(q, p, sizeof(T) * n);
+        if (p) cudaFreeHost(p);
+        p = q;
+        cap = want;
+        return true;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = cap = 0;
+    }
+    size_t size() const { return n; }
+    const T* data() const { return p; }
+};
+
+}  // namespace rb
+
+using rb::DevBuf;
+using rb::PinnedVec;
+using rb::fail;
+using rb::dev_alloc;
+using rb::dev_free;
+using rb::Item;
+using rb::DevColumn;
+using rb::FilterPlan;
+using rb::VerifyProg;
+using rb::JitKernel;
+
+struct rb_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 0;
+    int blocks_per_sm = 1;
+    DevBuf items, refs, counters, scratch, surv, offs;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr;
+    // output buffers of the last destroyed result, reused by the next run
+    int32_t* pool[3] = {nullptr, nullptr, nullptr};
+    long long pool_cap = 0;
+    unsigned long long* host_ctr = nullptr;  // pinned: counters read back after each run
+    PinnedVec<Item> host_items;              // the last run's work items
+    PinnedVec<int32_t> host_offs;            // the last run's part starts / ends (packed items)
+    std::mutex mu;                           // runs on one context are serialised (shared scratch)
+};
+
+struct rb_rel {
+    rb_ctx* ctx = nullptr;
+    int64_t n = 0;
+    std::vector<DevColumn> cols;
+    std::vector<int64_t> max_len;
+    std::vector<double> mean_len;
+    std::vector<void*> allocs;
+    void* d_cols = nullptr;
+    bool cols_dirty = true;
+};
+
+struct rb_prog {
+    rb_ctx* ctx = nullptr;
+    rb_rel* rel = nullptr;
+    FilterPlan F{};
+    VerifyProg V{};
+    int32_t n_slots = 0;
+    int64_t lmax_edit = -1;  // longest string any edit slot reads (-1: no edit slot)
+    std::vector<void*> allocs;
+    JitKernel jit;
+    JitKernel jit_small;  // 2-row variant for batches of small partitions (compiled on first use)
+    bool jit_small_tried = false;
+    // ungated variants, used once a run showed the stage-1 gate passing almost
+    // every warp iteration (its tests never fail inside these partitions)
+    JitKernel jit_nogate, jit_small_nogate;
+    bool jit_nogate_tried = false, jit_small_nogate_tried = false;
+    JitKernel jit_packed;  // 2-row variant taking packed items: batches of tiny partitions
+    bool jit_packed_tried = false;
+    bool gate_off = false;
+    long long last_rows = 0;  // output size of the previous run: sizes the next buffer
+    long long last_surv = 0;  // survivors of the previous run: sizes the deferred-verification buffer
+    double surv_rate = -1.0;  // survivors per work item in the previous run (-1: none yet)
+    // item ranges that fit the survivor buffer in the previous run, and its item count: a
+    // run over the same items (a repeated batch) replays them instead of re-learning where
+    // the survivors concentrate (each range that overflows is re-run)
+    std::vector<std::pair<int, int>> last_ranges;
+    int last_n_items = -1;
+    std::mutex ranges_mu;  // guards last_ranges / last_n_items (a program may be run from several threads)
+};
+
+struct rb_result {
+    rb_ctx* ctx = nullptr;
+    long long cap = 0;
+    int64_t count = 0;
+    int32_t* d_t = nullptr;
+    int32_t* d_s = nullptr;
+    int32_t* d_r = nullptr;
+    int32_t* d_p = nullptr;  // batched runs: partition index per row
+    cudaStream_t stream = nullptr;
+    rb_stats stats{};
+};
+
+
+namespace rb {
+
+// one partition / cross block of a run.  split < 0: a partition over
+// positions [base, base+n); else a cross block, left = [base, base+split),
+// right = [rbase, rbase + n - split) (rbase = base + split when contiguous)
+struct Part {
+    int64_t base, n, split, rbase;
+};
+
+// the run orchestration (rb_api.cu): refs are host tuple ids, or device ids
+// when refs_on_device; parts index positions of refs
+int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
+        int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out,
+        bool refs_on_device = false);
+
+}  // namespace rb

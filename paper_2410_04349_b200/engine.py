@@ -283,6 +283,17 @@ class PathProgram:
     def close(self) -> None:
         self._fin()
 
+    # -- device-resident results -----------------------------------------
+
+    def run_parts(self, parts, flags: int, rank: int = 0, world: int = 1) -> "DeviceResult":
+        """Every partition with pairs and every pull of a device partition
+        set (``pipeline.DeviceParts``) that rank ``rank`` of ``world`` owns,
+        in one batched run (rb_run_parts).  The rows stay on the device."""
+        res = _lib.c_vp()
+        check(lib().rb_run_parts(self.ctx.handle, self.drel.handle, self.handle, parts.handle, int(rank), int(world),
+                                 int(flags), _lib.ctypes.byref(res)))
+        return DeviceResult(res, self.ctx)
+
     # -- raw runs ---------------------------------------------------------
 
     def run_batch(self, refs, offsets, splits, flags: int, out=None):
@@ -350,6 +361,54 @@ class PathProgram:
         finally:
             L.rb_result_destroy(res)
         return (t, s, r), st
+
+
+class DeviceResult:
+    """An rb_result kept on the device: rows (t, s, rule) in HBM until copied.
+    ``collect`` deduplicates them in place (rb_result_collect)."""
+
+    def __init__(self, handle, ctx: Context):
+        self.handle = handle
+        self.ctx = ctx
+        self._fin = weakref.finalize(self, lib().rb_result_destroy, handle)
+
+    def close(self) -> None:
+        self._fin()
+
+    @property
+    def count(self) -> int:
+        cnt = _lib.ctypes.c_int64(0)
+        check(lib().rb_result_count(self.handle, _lib.ctypes.byref(cnt)))
+        return cnt.value
+
+    def stats(self):
+        st = _lib.RbStats()
+        check(lib().rb_result_stats(self.handle, _lib.ctypes.byref(st)))
+        return st
+
+    def collect(self, n_tuples: int, n_rules: int) -> "DeviceResult":
+        """pipeline.py:407-421 on the device: rows sorted by (t, s), the
+        smallest rule index per (t, s)."""
+        check(lib().rb_result_collect(self.handle, int(n_tuples), int(n_rules)))
+        return self
+
+    def copy(self, out=None):
+        """(t, s, rule) int32 host arrays (into ``out`` when it fits)."""
+        k = self.count
+        if out is not None and all(len(a) >= k and a.dtype == np.int32 and a.flags["C_CONTIGUOUS"] for a in out):
+            t, s, r = (a[:k] for a in out)
+        else:
+            t, s, r = (np.empty(k, dtype=np.int32) for _ in range(3))
+        if k:
+            check(lib().rb_result_copy(self.handle, ptr(t), ptr(s), ptr(r)))
+        return t, s, r
+
+    def device_pointers(self):
+        """(t, s, rule) device addresses, valid until close()."""
+        pt, ps, pr = _lib.c_vp(), _lib.c_vp(), _lib.c_vp()
+        check(lib().rb_result_device(self.handle, _lib.ctypes.byref(pt), _lib.ctypes.byref(ps),
+                                     _lib.ctypes.byref(pr), None))
+        return pt.value, ps.value, pr.value
 
 
 # ---------------------------------------------------------------------------

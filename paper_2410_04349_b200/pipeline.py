@@ -1,5 +1,7 @@
 """The callers on either side of the path: plan-derived partitioning, the
-device run over all partitions and pulls, and the collect step.
+device run over all partitions and pulls, and the collect step -- the
+reference's pipeline_run (pkg/src/ruleblock/pipeline.py:245-433) with its
+partitioning, execution and collect stages on the GPU.
 
 Restates the reference's partitioning and pipeline:
   * one hash partitioner per root edge of the plan     partitioning.py:40-90
@@ -14,15 +16,29 @@ Restates the reference's partitioning and pipeline:
     partition and pull, collect = union deduplicated per (t, s) keeping the
     earliest rule in rule-set order                     pipeline.py:245-433
 The group keys are byte-identical to the reference's, so the partitions
-(pids, refs, branches, sibling groups) are identical too.  The heavy part --
-minhash over every tuple's items -- is vectorised; the evaluation of all
-partitions runs batched on the GPU(s) through scheduler.MultiDeviceEngine.
+(pids, refs, branches, sibling groups) are identical too.
+
+Stages of ``pipeline_run``:
+  * keys   (host): each root edge's key strings, ranked in sorted key-string
+           order (one int64 per tuple and branch; minhash vectorised)
+  * partition (GPU, rb_partition): stable radix sort of (key, tid) per
+           branch, group sizes, round-robin sibling deal, pulls -- the sorted
+           tuple ids stay in HBM as the refs of the run
+  * execute (GPU, rb_run_parts): every partition with pairs and every pull
+           in one batched run; several GPUs split the units by LPT
+  * collect (GPU, rb_result_collect): radix sort of the rows on (t, s,
+           rule), first row per (t, s)
+Synthetic encoded relations (the benchmarks) key their equality roots on the
+device code columns directly (``run_pipeline_encoded``): same groups, pids in
+code order instead of key-string order, identical candidate set.
 """
 
 from __future__ import annotations
 
 import hashlib
+import threading
 import time
+import weakref
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -46,12 +62,20 @@ class BandingConfig:
 
 @dataclass
 class PipelineConfig:
+    """pipeline.py:63-74.  ``async_mode`` / ``stage_queue_bound`` /
+    ``rng_seed`` shaped the reference's host queues and CHBL placement and
+    never changed results; they are accepted.  ``devices`` / ``workers_per_device``
+    name the CUDA devices used when pipeline_run is not given any."""
+
+    async_mode: bool = True
+    stage_queue_bound: int = 8
     max_partition_size: int = 512
     enable_pulls: bool = False
     banding: BandingConfig = field(default_factory=BandingConfig)
+    rng_seed: int = 0
     single_partition_threshold: Optional[int] = None  # None: follows max_partition_size
     devices: tuple = (0,)
-    workers_per_device: int = 2
+    workers_per_device: int = 1
 
 
 def stable_hash64(text: str, seed: int = 0) -> int:
@@ -183,49 +207,323 @@ def collect(candidate_sets, rule_ids) -> CandidateSet:
     return CandidateSet(arrays=(t[keep], s[keep], r[keep]), rule_ids=rule_ids)
 
 
+def branch_order(path) -> list:
+    """The reference's iteration order over the root edges: equality
+    branches first, score order otherwise (partitioning.py:106-110)."""
+    roots = root_predicates(path)
+    return sorted(range(len(roots)), key=lambda b: roots[b].comparator != "eq")
+
+
+def rank_keys(keys: list) -> tuple[np.ndarray, list]:
+    """Key strings -> int64 ranks in sorted key-string order (the order of
+    ``sorted(groups)``), plus the sorted distinct keys."""
+    index: dict = {}
+    inv = np.fromiter((index.setdefault(k, len(index)) for k in keys), dtype=np.int64, count=len(keys))
+    distinct = list(index)
+    order = sorted(range(len(distinct)), key=distinct.__getitem__)
+    rank = np.empty(len(distinct), dtype=np.int64)
+    rank[np.asarray(order, dtype=np.int64)] = np.arange(len(distinct), dtype=np.int64)
+    return rank[inv], [distinct[k] for k in order]
+
+
+def partition_keys(relation, path, banding: Optional[BandingConfig] = None):
+    """Per branch in iteration order: (branch id, int64 key per tuple, sorted
+    distinct key strings).  Equal keys <=> equal reference key strings."""
+    banding = banding or BandingConfig()
+    roots = root_predicates(path)
+    out = []
+    for b in branch_order(path):
+        ranks, distinct = rank_keys(branch_keys(relation, roots[b], banding))
+        out.append((b, ranks, distinct))
+    return out
+
+
+class DeviceParts:
+    """A partition set resident on one device (rb_parts): the tuple ids of
+    every branch sorted into groups and siblings, the partition list, the
+    pulls.  ``partitions()`` / ``pulls()`` materialise the reference objects."""
+
+    def __init__(self, handle, ctx, key_groups=None):
+        from . import _lib
+
+        self.handle = handle
+        self.ctx = ctx
+        self.key_groups = key_groups  # branch id -> sorted distinct key strings (exact key_group labels)
+        self._fin = weakref.finalize(self, _lib.lib().rb_parts_destroy, handle)
+        vals = [_lib.ctypes.c_int64(0) for _ in range(4)]
+        _lib.check(_lib.lib().rb_parts_info(handle, *[_lib.ctypes.byref(v) for v in vals]))
+        self.n_partitions, self.n_pulls, self.n_refs, self.n_groups = (v.value for v in vals)
+        self._host = None
+
+    def close(self) -> None:
+        self._fin()
+
+    def host(self):
+        """refs and per-entry (base, size, split, rbase, branch, sibling) arrays."""
+        if self._host is None:
+            from . import _lib
+
+            m = self.n_partitions + self.n_pulls
+            refs = np.empty(self.n_refs, dtype=np.int32)
+            base, size, split, rbase = (np.empty(m, dtype=np.int64) for _ in range(4))
+            branch, sib = np.empty(m, dtype=np.int32), np.empty(m, dtype=np.int32)
+            _lib.check(_lib.lib().rb_parts_copy(self.handle, _lib.ptr(refs), _lib.ptr(base), _lib.ptr(size),
+                                                _lib.ptr(split), _lib.ptr(rbase), _lib.ptr(branch), _lib.ptr(sib)))
+            self._host = (refs, base, size, split, rbase, branch, sib)
+        return self._host
+
+    def partitions(self) -> list:
+        """DataPartition per partition, pids in order (iter_partitions)."""
+        refs, base, size, _, _, branch, sib = self.host()
+        out = []
+        group_of: dict = {}
+        for k in range(self.n_partitions):
+            b = int(branch[k])
+            key = None
+            if self.key_groups is not None:
+                # groups come in key order: count the distinct groups seen in this branch
+                g = group_of.setdefault(b, [-1, -1])
+                if sib[k] == 0 or sib[k] != g[1]:
+                    g[0] += 1
+                g[1] = int(sib[k]) if sib[k] else -1
+                key = self.key_groups[b][g[0]]
+            out.append(DataPartition(pid=k, tuple_refs=tuple(refs[base[k]:base[k] + size[k]].tolist()), branch_id=b,
+                                     key_group=key, sibling_group=int(sib[k]) if sib[k] else None))
+        return out
+
+    def pulls(self) -> list:
+        """(pid_a, pid_b) per pull, as sibling_pull_pairs."""
+        _, base, _, split, rbase, _, _ = self.host()
+        start_pid = {int(base[k]): k for k in range(self.n_partitions)}
+        return [(start_pid[int(base[k])], start_pid[int(rbase[k])])
+                for k in range(self.n_partitions, self.n_partitions + self.n_pulls)]
+
+
+def partition_on_device(prog, *, keys=None, code_cols=None, branch_ids, max_partition_size: int, pulls: bool,
+                        key_groups=None) -> DeviceParts:
+    """rb_partition / rb_partition_codes over the program's relation.
+    ``keys``: int64 array (branches, n) in iteration order; ``code_cols``:
+    the relation's codes columns, one per branch."""
+    from . import _lib
+
+    if max_partition_size < 1:
+        raise ConfigError("max_partition_size must be >= 1")
+    L = _lib.lib()
+    h = _lib.c_vp()
+    bids = np.ascontiguousarray(branch_ids, dtype=np.int32)
+    flags = _lib.RB_PART_PULLS if pulls else 0
+    if keys is not None:
+        k = np.ascontiguousarray(keys, dtype=np.int64)
+        _lib.check(L.rb_partition(prog.ctx.handle, prog.drel.handle, _lib.ptr(k), _lib.ptr(bids), len(bids),
+                                  int(max_partition_size), flags, _lib.ctypes.byref(h)))
+    else:
+        cols = np.ascontiguousarray(code_cols, dtype=np.int32)
+        _lib.check(L.rb_partition_codes(prog.ctx.handle, prog.drel.handle, _lib.ptr(cols), _lib.ptr(bids), len(bids),
+                                        int(max_partition_size), flags, _lib.ctypes.byref(h)))
+    return DeviceParts(h, prog.ctx, key_groups)
+
+
 @dataclass
 class PipelineResult:
+    """pipeline.py:212-220 (candidates, timings, assignment, n_partitions,
+    device_busy_s, plan) plus the device partition set."""
+
     candidates: CandidateSet
     timings: dict
+    assignment: dict
     n_partitions: int
-    partitions: list
+    device_busy_s: dict
+    plan: object = None
+    parts: object = None  # DeviceParts of the first device (partitions() / pulls())
+
+    @property
+    def partitions(self) -> list:
+        return [] if self.parts is None else self.parts.partitions()
 
 
-def pipeline_run(relation, path, pipe_cfg: Optional[PipelineConfig] = None,
-                 engine_cfg: Optional[EngineConfig] = None, reg=None, encoded=None) -> PipelineResult:
-    """The reference's pipeline_run (pipeline.py:245-433) on a frozen path:
-    partition, evaluate every partition (and sibling pull) on the GPU(s),
-    collect.  Candidate sets equal the reference's for the same plan."""
-    from .scheduler import MultiDeviceEngine
+def _cuda_devices(devices, pipe_cfg) -> list:
+    """CUDA ordinals: ints as given; the reference's simulated Device
+    objects map onto the visible GPUs by device_id."""
+    if not devices:
+        return list(pipe_cfg.devices)
+    out = []
+    for d in devices:
+        out.append(int(getattr(d, "device_id", d)))
+    return out
+
+
+def _device_stage(dev: int, enc, path, compiled, keys, code_cols, branch_ids, maxp: int, pulls: bool, cfg,
+                  rank: int, world: int, n_tuples: int, key_groups, timings: dict):
+    """One device: upload, partition, run its share, collect."""
+    from .engine import Context, DeviceRelation, PathProgram
+
+    ctx = Context(dev)
+    drel = DeviceRelation(ctx, enc)
+    prog = PathProgram(path, enc, compiled=compiled, drel=drel)
+    t0 = time.perf_counter()
+    parts = partition_on_device(prog, keys=keys, code_cols=code_cols, branch_ids=branch_ids, max_partition_size=maxp,
+                                pulls=pulls, key_groups=key_groups)
+    t1 = time.perf_counter()
+    res = prog.run_parts(parts, cfg.flags(), rank, world)
+    st = res.stats()
+    t2 = time.perf_counter()
+    res.collect(n_tuples, max(1, len(path.rule_ids)))
+    t3 = time.perf_counter()
+    timings.update(partition_s=t1 - t0, execute_s=t2 - t1, collect_s=t3 - t2)
+    return prog, parts, res, st
+
+
+def _merge_runs(runs: list, n_tuples: int, n_rules: int, device: int):
+    """Collected row runs of several devices -> one collected set (host
+    arrays): concatenated and collected once more on ``device``."""
+    if len(runs) == 1:
+        return runs[0]
+    import torch
+
+    from . import _lib
+    from .engine import context
+
+    total = sum(len(r[0]) for r in runs)
+    if total == 0:
+        return tuple(np.zeros(0, np.int32) for _ in range(3))
+    dev = torch.device("cuda", device)
+    cols = [torch.from_numpy(np.concatenate([r[c] for r in runs])).to(dev) for c in range(3)]
+    out = [torch.empty(total, dtype=torch.int32, device=dev) for _ in range(3)]
+    ctx = context(device)
+    torch.cuda.current_stream(dev).synchronize()  # the uploads precede the library's stream
+    cnt = _lib.ctypes.c_int64(0)
+    _lib.check(_lib.lib().rb_collect_device(ctx.handle, *[_lib.c_vp(x.data_ptr()) for x in cols], total, n_tuples,
+                                            n_rules, *[_lib.c_vp(x.data_ptr()) for x in out], _lib.ctypes.byref(cnt)))
+    return tuple(x[: cnt.value].cpu().numpy() for x in out)
+
+
+def run_pipeline_encoded(enc, path, pipe_cfg: Optional[PipelineConfig] = None,
+                         engine_cfg: Optional[EngineConfig] = None, *, keys=None, code_cols=None, branch_ids=None,
+                         devices=None, reg=None, key_groups=None) -> PipelineResult:
+    """The device pipeline over an encoded relation: partition (``keys``
+    int64 (branches, n) or eq-root ``code_cols``), execute on every device
+    in ``devices`` (LPT share of the units each), collect."""
+    from .encode import compile_program
 
     pipe_cfg = pipe_cfg or PipelineConfig()
     engine_cfg = engine_cfg or EngineConfig(num_blocks=1)
-    timings: dict = {}
+    devs = _cuda_devices(devices, pipe_cfg)
+    n = enc.n
+    compiled = compile_program(path, enc, reg)
+    threshold = pipe_cfg.single_partition_threshold
+    if threshold is None:
+        threshold = pipe_cfg.max_partition_size
+    maxp = pipe_cfg.max_partition_size
+    if n <= threshold:  # one partition of every tuple (pipeline.py:282-286)
+        keys, code_cols, branch_ids, key_groups = np.zeros((1, n), np.int64), None, [0], None
+        maxp = max(1, n)
+    if branch_ids is None:
+        branch_ids = branch_order(path)
     wall0 = time.perf_counter()
+    per_dev: list = [None] * len(devs)
+    errors: list = []
+
+    def work(k: int):
+        try:
+            tm: dict = {}
+            out = _device_stage(devs[k], enc, path, compiled, keys, code_cols, branch_ids, maxp,
+                                pipe_cfg.enable_pulls, engine_cfg, k, len(devs), n, key_groups, tm)
+            rows = out[2].copy()
+            per_dev[k] = (out, rows, tm)
+        except BaseException as exc:  # surfaced below
+            errors.append(exc)
+
+    if len(devs) == 1:
+        work(0)
+    else:
+        threads = [threading.Thread(target=work, args=(k,), name=f"rb-pipeline-gpu{devs[k]}") for k in range(len(devs))]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+    if errors:
+        raise errors[0]
+    t0 = time.perf_counter()
+    t, s, r = _merge_runs([x[1] for x in per_dev], n, max(1, len(path.rule_ids)), devs[0])
+    merge_s = time.perf_counter() - t0
+    timings = {k: max(x[2][k] for x in per_dev) for k in ("partition_s", "execute_s", "collect_s")}
+    timings["collect_s"] += merge_s
+    timings["total_s"] = time.perf_counter() - wall0
+    stats = [x[0][3] for x in per_dev]
+    from .engine import BlockStats
+
+    blocks = [BlockStats(block_id=k, comparisons=int(st.comparisons), survivors=int(st.survivors),
+                         emitted=int(st.emitted), busy_s=st.kernel_ms / 1e3,
+                         slot_evals=np.array(st.slot_evals[: len(path.predicate_table)], dtype=np.int64))
+              for k, st in enumerate(stats)]
+    cand = CandidateSet(arrays=(t.astype(np.int64), s.astype(np.int64), r.astype(np.int64)),
+                        rule_ids=list(path.rule_ids),
+                        stats=RunStats(blocks=blocks, wall_s=timings["total_s"],
+                                       kernel_ms=sum(st.kernel_ms for st in stats),
+                                       launches=sum(int(st.launches) for st in stats)))
+    parts = per_dev[0][0][1]
+    for x in per_dev[1:]:
+        x[0][2].close()
+    return PipelineResult(candidates=cand, timings=timings, assignment={}, n_partitions=int(parts.n_partitions),
+                          device_busy_s={devs[k]: per_dev[k][0][3].kernel_ms / 1e3 for k in range(len(devs))},
+                          plan=None, parts=parts)
+
+
+def pipeline_run(relation, rules, pipe_cfg: Optional[PipelineConfig] = None,
+                 engine_cfg: Optional[EngineConfig] = None, devices=None, planner_cfg=None, plan=None, reg=None,
+                 encoded=None) -> PipelineResult:
+    """The reference's pipeline_run (pipeline.py:245-433) on the GPU(s):
+    partition, evaluate every partition (and sibling pull), collect.
+
+    ``rules`` is the RuleSet (with ``plan``, a PlanBundle or anything with a
+    ``.path``, frozen as the reference's ``plan=``) or directly an
+    ExecutionPath.  Without a plan, a data-aware plan is derived from sampled
+    selectivities (plan generation itself is outside this path).  ``devices``:
+    CUDA ordinals or the reference's Device objects (by device_id)."""
+    from .encode import RelationEncoding
+    from .engine import _encoding_for
+
+    pipe_cfg = pipe_cfg or PipelineConfig()
+    engine_cfg = engine_cfg or EngineConfig(num_blocks=1)
+    t0 = time.perf_counter()
+    if plan is not None:
+        path = getattr(plan, "path", plan)
+    elif hasattr(rules, "predicate_table"):
+        path = rules
+    else:
+        from .synth import data_aware_plan
+
+        path = None
+    plan_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    enc = _encoding_for(relation, encoded)
+    if path is None:
+        path = data_aware_plan(RelationEncoding(relation).prepare(list(_universe(rules))), rules)
+    if isinstance(enc, RelationEncoding):
+        enc.prepare(list(path.predicate_table))
+    encode_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     threshold = pipe_cfg.single_partition_threshold
     if threshold is None:
         threshold = pipe_cfg.max_partition_size
     if len(relation) <= threshold:
-        partitions = [DataPartition(pid=0, tuple_refs=tuple(range(len(relation))))]
+        keys, bids, groups = None, None, None
     else:
-        partitions = list(iter_partitions(relation, path, pipe_cfg.max_partition_size, pipe_cfg.banding))
-    timings["partition_s"] = time.perf_counter() - t0
+        kb = partition_keys(relation, path, pipe_cfg.banding)
+        bids = [b for b, _, _ in kb]
+        keys = np.stack([k for _, k, _ in kb]) if kb else None
+        groups = {b: g for b, _, g in kb}
+    keys_s = time.perf_counter() - t0
+    res = run_pipeline_encoded(enc, path, pipe_cfg, engine_cfg, keys=keys, branch_ids=bids, devices=devices, reg=reg,
+                               key_groups=groups)
+    res.timings.update(plan_s=plan_s, encode_s=encode_s, keys_s=keys_s)
+    res.timings["partition_s"] += keys_s
+    res.timings["total_s"] += plan_s + encode_s + keys_s
+    res.plan = plan
+    return res
 
-    t0 = time.perf_counter()
-    eng = MultiDeviceEngine(relation, path, devices=pipe_cfg.devices, reg=reg, encoded=encoded,
-                            workers_per_device=pipe_cfg.workers_per_device)
-    work = [p for p in partitions if len(p.tuple_refs) > 1 or not engine_cfg.symmetric_mode]
-    results = eng.run_partitions(work, engine_cfg)
-    if pipe_cfg.enable_pulls:
-        by_pid = {p.pid: p for p in partitions}
-        pulls = [(by_pid[a], by_pid[b]) for a, b in sibling_pull_pairs(partitions)]
-        results += eng.run_crosses(pulls, engine_cfg) if pulls else []
-    timings["execute_s"] = time.perf_counter() - t0
 
-    t0 = time.perf_counter()
-    cand = collect(results, list(path.rule_ids))
-    timings["collect_s"] = time.perf_counter() - t0
-    timings["total_s"] = time.perf_counter() - wall0
-    cand.stats = RunStats(blocks=[b for cs in results for b in cs.stats.blocks], wall_s=timings["total_s"])
-    return PipelineResult(candidates=cand, timings=timings, n_partitions=len(partitions), partitions=partitions)
+def _universe(rules):
+    from .rules import predicate_universe
+
+    return predicate_universe(rules)
