@@ -1,33 +1,54 @@
 """Benchmark of the rule-evaluation hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload NAME] [--tuples N]
 
-A step evaluates every unordered tuple pair of one synthetic 1M-tuple
-citation-style relation (BASELINE config 2: 3 rules mixing equality, token
-Jaccard and edit distance) as ONE partition -- 499,999,500,000
-pairs -- and emits the surviving (t, s, rule) rows.
+Default workload: BASELINE config 4 (i) -- the metric's own configuration.
+A synthetic 10M-tuple person relation (zip, last, first, dob, phone,
+address), 5 rules with a data-aware predicate order, run through the
+product pipeline (``pipeline.ResidentPipeline``: the reference's
+pipeline_run, pkg/src/ruleblock/pipeline.py:245-433): plan-derived
+partitions (max_partition_size 65536) plus sibling pulls built on the GPU,
+every unit evaluated, the rows collected (deduplicated per (t, s), earliest
+rule).  One step = that whole pass over the resident relation.
 
-* value   -- pairs / s over the timed steps, inputs resident in HBM, timed
-             with CUDA events on the stream the engine launches on, max over
-             ranks.  L2 is flushed (a 512 MiB write) between timed steps.
-* e2e     -- the same metric through the C ABI with HOST buffers: every step
-             uploads the encoded relation and the program (H2D), evaluates,
-             and copies the result rows back (D2H).
-* roofline-- SURVEY §8d streaming-bytes model for the pair kernel.
-* cpu_baseline -- the CPU oracle (a C restatement of the reference engine,
-             oracle/rb_oracle.c) on a bounded row sample on this host's cores;
-             the same rows are also checked for bit-exact parity against the GPU.
-
-Multi-GPU (torchrun): weak scaling -- every rank evaluates its own 1M-tuple
-partition (seed + rank), no data-path collective; NCCL only reduces the
-timings and the row counts at the end.
+* value   -- pairs / s: all ranks' evaluated pairs / the step time, inputs
+             resident in HBM, timed with CUDA events on the stream the engine
+             launches on, max over ranks.  L2 is flushed (512 MiB write)
+             between timed steps (the relation is ~1 GB, > L2 anyway).
+* multi-GPU (--gpus N; re-launched under torch.distributed.run when
+             WORLD_SIZE is unset): STRONG scaling of the same relation.  Each
+             rank evaluates its longest-processing-time share of the units
+             (rb_run_parts), collects, then the ranks exchange their rows by
+             tuple-id range (one NCCL all-to-all) and collect again: the
+             collected set ends sharded by t over the ranks.
+* e2e     -- the same pass through the public API (``run_pipeline_encoded``)
+             from HOST buffers: upload of every encoded column and the
+             program (H2D), partition, execute, collect, exchange, and the
+             D2H copy of the rank's collected rows, every step.
+* secondary -- config 4 (ii): the same relation as ONE symmetric partition
+             (4.9999999e13 pairs), outer rows split by equal pair count over
+             the ranks, rows all-gathered over NCCL; one timed step.
+* roofline -- the pair kernel's binding issue pipe (ALU / XU) from the
+             committed ncu capture of the same workload, size and kernel
+             source (profiles/traffic.json), rescaled to this run's kernel
+             time and clock; the SURVEY 8d streaming-bytes model and the
+             capture's DRAM bytes are kept beside it as ``hbm_model``.
+* cpu_baseline / parity -- the CPU oracle (oracle/rb_oracle.c, a C
+             restatement of the reference engine) on a bounded sample of
+             whole units on this host's cores, the same units re-run on the
+             GPU for bit-exact parity; plus checks over the full step's
+             collected rows (sorted, distinct, witness == oracle first
+             witness on a row sample) and recall of every injected duplicate.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -39,16 +60,24 @@ sys.path.insert(0, ROOT)
 
 METRIC = "tuple pairs evaluated/sec and blocking wall-time at 1/2/4/8 B200 vs CPU ref"
 WORKLOAD_DESC = {
-    "citation3": "BASELINE config 2: 3 rules mixing eq, jaccard and edit",
-    "edit_heavy": "BASELINE config 3: edit-distance-heavy rules, 64-256-char strings, maxd 2-5",
+    "person5_pipeline": "BASELINE config 4 (i): 10M-tuple person relation, 5 rules, data-aware plan, the "
+                        "pipeline's plan-derived partitions (max_partition_size 65536) + sibling pulls, "
+                        "partition + execute + collect on the GPU",
+    "person5": "BASELINE config 4 (ii): person relation, 5 rules, data-aware plan, one partition",
+    "citation3": "BASELINE config 2: 3 rules mixing eq, jaccard and edit, one partition",
+    "edit_heavy": "BASELINE config 3: edit-distance-heavy rules, 64-256-char strings, maxd 2-5, one partition",
     "linkage": "BASELINE config 5: two-table linkage, Zipf(1.3) blocks, one cross run per block, batched",
     "citation3_parts": "config 2 relation in 512-tuple partitions (the reference pipeline's default), batched",
     "citation_small": "BASELINE config 1: the reference's citation_benchmark (4,591 tuples) with its frozen plan",
-    "person5": "BASELINE config 4 (ii): person relation, 5 rules, data-aware plan, one partition",
-    "person5_parts": "BASELINE config 4 (i): person relation, 5 rules, the pipeline's plan-derived partitions "
-                     "(max_partition_size 65536) plus sibling pulls, batched",
+    "person5_parts": "BASELINE config 4 (i) units (host-built eq-root partitions + pulls), batched, no collect",
 }
+DEFAULT_TUPLES = {"person5_pipeline": 10_000_000, "person5": 10_000_000}
 UNIT = "pairs/s"
+PIPELINE_MAXP = 65536
+# issue rate of each integer pipe, warp instructions per SM per cycle (4 SMSPs:
+# ALU 16 lanes each -> 0.5/clk/SMSP; XU 4 lanes each -> 0.125/clk/SMSP)
+PIPE_RATE = {"ALU": 2.0, "XU": 0.5, "FMA": 2.0}
+SM_COUNT = 148
 
 
 def measured_peak():
@@ -56,11 +85,29 @@ def measured_peak():
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             return float(json.load(fh)["hbm_gbs"]), "measured"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def kernel_source_sha() -> str:
+    """Hash of the device source the NVRTC specialiser compiles (a capture is
+    only attributed to a run of the same kernel source)."""
+    p = os.path.join(ROOT, "paper_2410_04349_b200", "csrc", "rb_device.cuh")
+    return hashlib.sha1(open(p, "rb").read()).hexdigest()[:12]
+
+
+def relaunch_distributed(n: int) -> int:
+    """--gpus N without a torchrun environment: re-run this command as N
+    ranks (one per GPU) under torch.distributed.run on 127.0.0.1."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 class ClockSampler:
@@ -73,6 +120,7 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.lines = []
 
     def __enter__(self):
         try:
@@ -97,7 +145,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
+        for l in self.lines:
             f = [x.strip() for x in l.split(",")]
             try:
                 sm.append(float(f[0]))
@@ -111,26 +159,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def pinned_rows(k):
-    """Three reusable pinned int32 host arrays of k rows (t, s, rule)."""
-    import torch
-
-    return tuple(torch.empty(max(1, k), dtype=torch.int32, pin_memory=True).numpy() for _ in range(3))
-
-
 def pin_array(a):
     """A pinned (page-locked) host copy of a numpy array."""
     import torch
 
-    t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
-    out = t.numpy().view(a.dtype).reshape(a.shape)
+    t = torch.empty(max(1, a.nbytes), dtype=torch.uint8, pin_memory=True)
+    out = t.numpy()[: a.nbytes].view(a.dtype).reshape(a.shape)
     out[...] = a
     return out
 
 
 def pinned_encoding(enc):
-    """A copy of an Encoded whose column arrays live in pinned (page-locked)
-    host memory, so the H2D copies of the e2e leg run at DMA speed."""
+    """A copy of an Encoded whose column arrays live in pinned host memory,
+    as a loader would leave them (pinning is outside the timed region)."""
     from paper_2410_04349_b200.encode import Column, Encoded
 
     def pin(a):
@@ -142,9 +183,14 @@ def pinned_encoding(enc):
     return pe
 
 
+def encoding_bytes(enc) -> int:
+    return int(sum(c.data.nbytes + (0 if c.offsets is None else c.offsets.nbytes)
+                   + (0 if c.missing is None else c.missing.nbytes) for c in enc.columns))
+
+
 def algorithmic_bytes_per_pair(enc, path, evals_frac, rows_per_pair):
-    """SURVEY §8d: A = sum_s E_s * b_s + C * 10 B, per pair.  E_s/pairs comes
-    from the oracle's exact first-touch counts on the sample rows."""
+    """SURVEY 8d: A = sum_s E_s * b_s + C * 10 B, per pair.  E_s/pairs comes
+    from the oracle's exact first-touch counts on the sample."""
     from paper_2410_04349_b200.encode import SLOT_EDIT, SLOT_EQ_CODE, SLOT_EXACT, SLOT_JACCARD
 
     total = 0.0
@@ -165,24 +211,263 @@ def algorithmic_bytes_per_pair(enc, path, evals_frac, rows_per_pair):
     return total + 10.0 * rows_per_pair, terms
 
 
-def cpu_sample(w, prog, rows, nthreads):
-    """Oracle on outer rows `rows` (list of (lo, hi)); returns rows, pairs, seconds, evals."""
-    from oracle import oracle
+def roofline(w_name, n, pairs_step, kernel_ms, clocks, bytes_per_pair=None, terms=None):
+    """The pair kernel against its binding pipe.  The capture (profiles/
+    traffic.json, same workload, size and kernel source) gives each pipe's
+    utilisation over the capture's cycles; the same instruction stream in
+    this run's cycles (kernel_ms x median SM clock) rescales it."""
+    peak_hbm, peak_kind = measured_peak()
+    hbm = None
+    if bytes_per_pair is not None:
+        ach = bytes_per_pair * pairs_step / (kernel_ms / 1e3) / 1e9
+        hbm = {"achieved": ach, "peak": peak_hbm, "unit": "GB/s", "frac": ach / peak_hbm, "peak_kind": peak_kind,
+               "bytes_per_pair": bytes_per_pair, "terms": terms,
+               "model": "SURVEY 8d streaming bytes: sum_s E_s*b_s + 10 B per row; E_s from oracle first-touch "
+                        "counts.  Not the bound: inner tuples are reused from shared memory, so the measured "
+                        "DRAM traffic (traffic) is far below this model."}
+    entry = {}
+    try:
+        entry = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(w_name, {})
+    except Exception:
+        pass
+    out = {"bound": None, "achieved": None, "peak": None, "unit": "warp-inst/s", "frac": None,
+           "traffic": None, "kernel_ms": kernel_ms, "hbm_model": hbm}
+    if not entry or entry.get("n") != n:
+        out["capture"] = f"no ncu capture of {w_name} at n={n} in profiles/traffic.json"
+        return out
+    m = entry.get("metrics", {})
+    val = {k: float(v["value"]) for k, v in m.items() if _num(v.get("value"))}
+    pipes = {"ALU": "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+             "XU": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+             "FMA": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"}
+    have = {p: val[k] / 100.0 for p, k in pipes.items() if k in val}
+    if not have:
+        return out
+    bind = max(have, key=have.get)
+    cap_ns = val.get("gpu__time_duration.sum")
+    if cap_ns is not None and m["gpu__time_duration.sum"].get("unit") == "msecond":
+        cap_ns *= 1e6
+    elif cap_ns is not None and m["gpu__time_duration.sum"].get("unit") == "usecond":
+        cap_ns *= 1e3
+    cap_mhz = val.get("sm__cycles_elapsed.avg.per_second")
+    if cap_mhz is not None:
+        unit = m["sm__cycles_elapsed.avg.per_second"].get("unit", "")
+        cap_mhz = cap_mhz * {"Ghz": 1e3, "GHz": 1e3, "Mhz": 1.0, "MHz": 1.0, "hz": 1e-6}.get(unit, 1.0)
+    live_mhz = (clocks or {}).get("sm_mhz") or cap_mhz or 1965.0
+    if cap_mhz is None:
+        cap_mhz = live_mhz
+    # the capture's busy cycles on the pipe, replayed in this run's cycles
+    frac = have[bind] * (cap_ns * 1e-6 * cap_mhz) / (kernel_ms * live_mhz) if cap_ns else have[bind]
+    peak = PIPE_RATE[bind] * SM_COUNT * live_mhz * 1e6
+    out.update(bound=bind.lower(), frac=frac, peak=peak, achieved=frac * peak,
+               traffic=entry.get("bytes_per_launch"),
+               capture=entry.get("capture"), capture_frac=have[bind], capture_pipes=have,
+               capture_ms=cap_ns * 1e-6 if cap_ns else None, capture_sm_mhz=cap_mhz,
+               capture_kernel_sha=entry.get("kernel_sha"), kernel_sha=kernel_source_sha(),
+               capture_current=entry.get("kernel_sha") == kernel_source_sha(),
+               issue_active=val.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0) / 100.0,
+               warp_inst_per_pair=(val["smsp__inst_executed.sum"] / pairs_step
+                                   if "smsp__inst_executed.sum" in val and entry.get("pairs") == pairs_step else None))
+    return out
 
-    out, pairs, evals, secs = [], 0, np.zeros(prog.n_slots, dtype=np.int64), 0.0
-    for lo, hi in rows:
+
+def _num(x) -> bool:
+    try:
+        float(x)
+        return True
+    except (TypeError, ValueError):
+        return False
+
+
+# ---------------------------------------------------------------------------
+# the workloads as steps
+
+
+class Job:
+    """One workload on one rank: ``step()`` is the timed hot-path pass over
+    resident inputs, ``e2e_step()`` the same through the public API from
+    host buffers."""
+
+    def __init__(self, args, w, rank, world, group, dev):
+        import torch
+
+        from paper_2410_04349_b200.engine import PathProgram, context
+
+        self.args, self.w, self.rank, self.world, self.group, self.dev = args, w, rank, world, group, dev
+        self.ctx = context(dev)
+        self.stream = torch.cuda.current_stream()
+        self.ctx.set_stream(self.stream.cuda_stream)
+        self.prog = PathProgram(w.path, w.enc, device=dev)
+        self.stage_ms = {}
+        self.h2d = encoding_bytes(w.enc) + self.prog.program.tables.nbytes + self.prog.program.slots.nbytes \
+            + 16 * len(self.prog.program.ins_op)
+        self.d2h = 0
+
+
+class PipelineJob(Job):
+    """Config 4 (i): ResidentPipeline over eq-root code columns."""
+
+    kind = "pipeline"
+
+    def __init__(self, *a):
+        super().__init__(*a)
+        self.host_out = None
+        from paper_2410_04349_b200.pipeline import ResidentPipeline, branch_order, root_predicates
+
+        from paper_2410_04349_b200._lib import RB_SYMMETRIC
+
+        w = self.w
+        roots = root_predicates(w.path)
+        if any(p.comparator != "eq" or p.is_cross_attr for p in roots):
+            raise SystemExit("pipeline workloads key equality roots on the code columns")
+        self.bids = branch_order(w.path)
+        self.cols = [w.enc.get(("codes", roots[b].lhs_attr)) for b in self.bids]
+        self.rp = ResidentPipeline(self.prog, code_cols=self.cols, branch_ids=self.bids,
+                                   max_partition_size=PIPELINE_MAXP, pulls=True, flags=RB_SYMMETRIC)
+
+    def step(self, keep_parts=False):
+        rows, st, ms = self.rp.step(self.rank, self.world, self.group, keep_parts=keep_parts)
+        self.stage_ms = ms
+        return rows, st
+
+    def e2e_step(self, host_enc):
+        from paper_2410_04349_b200.encode import compile_program
+        from paper_2410_04349_b200.engine import EngineConfig
+        from paper_2410_04349_b200.pipeline import PipelineConfig, run_pipeline_encoded
+
+        cfg = PipelineConfig(max_partition_size=PIPELINE_MAXP, enable_pulls=True, single_partition_threshold=0)
+        res = run_pipeline_encoded(host_enc, self.w.path, cfg, EngineConfig(num_blocks=1), code_cols=self.cols,
+                                   branch_ids=self.bids, group=self.group if self.world > 1 else None,
+                                   devices=[self.dev], out=self.host_out)
+        if self.host_out is None:  # reusable pinned row buffers (allocated once, outside the timed steps)
+            import torch
+
+            k = len(res.candidates) + len(res.candidates) // 4 + 1024
+            self.host_out = tuple(torch.empty(k, dtype=torch.int32, pin_memory=True).numpy() for _ in range(3))
+        res.parts.close()
+        self.d2h = 12 * len(res.candidates)
+        return len(res.candidates), res.timings
+
+
+class PartitionJob(Job):
+    """One symmetric partition of the whole relation: rank r evaluates the
+    outer rows split_rows_by_pairs(n, N)[r]; the rows are all-gathered."""
+
+    kind = "partition"
+
+    def __init__(self, *a):
+        super().__init__(*a)
+        from paper_2410_04349_b200.engine import split_rows_by_pairs
+
+        self.lo, self.hi = split_rows_by_pairs(self.w.n, self.world)[self.rank]
+
+    def step(self, lo=None, hi=None):
+        from paper_2410_04349_b200._lib import RB_SYMMETRIC
+        from paper_2410_04349_b200.distributed import gather_rows, run_rows_device
+
         t0 = time.perf_counter()
-        r, cmp, ev = oracle.run(w.enc, prog, None, w.n, row_lo=lo, row_hi=hi, flags=1, nthreads=nthreads)
-        secs += time.perf_counter() - t0
-        out.append(r)
-        pairs += cmp
-        evals += ev
-    return np.concatenate(out) if out else np.zeros((0, 3), np.int64), pairs, secs, evals
+        rows, st = run_rows_device(self.prog, None, self.w.n, RB_SYMMETRIC, self.lo if lo is None else lo,
+                                   self.hi if hi is None else hi)
+        t1 = time.perf_counter()
+        if self.world > 1 and lo is None:
+            rows = gather_rows(rows, self.group)
+        self.stage_ms = {"execute": 1e3 * (t1 - t0), "exchange": 1e3 * (time.perf_counter() - t1)}
+        return (rows[:, 0], rows[:, 1], rows[:, 2]), st
+
+    def e2e_step(self, host_enc):
+        from paper_2410_04349_b200.engine import DeviceRelation, PathProgram
+
+        drel = DeviceRelation(self.ctx, host_enc)
+        p2 = PathProgram(self.w.path, host_enc, compiled=self.prog.program, drel=drel)
+        saved, self.prog = self.prog, p2
+        try:
+            rows, _ = self.step()
+            host = rows[0].cpu(), rows[1].cpu(), rows[2].cpu()
+        finally:
+            self.prog = saved
+            p2.close()
+            drel.close()
+        self.d2h = 12 * len(host[0])
+        return len(host[0]), {}
+
+
+class BlocksJob(Job):
+    """Many partitions / cross blocks in one batched launch; several ranks
+    take LPT shares of the blocks (disjoint pair sets: no exchange)."""
+
+    kind = "blocks"
+
+    def __init__(self, *a):
+        super().__init__(*a)
+        w = self.w
+        cost = np.array([sp * (len(r) - sp) if sp >= 0 else len(r) * (len(r) - 1) // 2 for r, sp in w.blocks])
+        owner = np.zeros(len(w.blocks), dtype=np.int64)
+        if self.world > 1:
+            load = np.zeros(self.world, dtype=np.int64)
+            for k in np.argsort(-cost, kind="stable"):
+                j = int(np.argmin(load))
+                owner[k] = j
+                load[j] += cost[k]
+        mine = [w.blocks[k] for k in np.flatnonzero(owner == self.rank)]
+        self.b_refs = pin_array(np.concatenate([r for r, _ in mine]).astype(np.int32)) if mine else np.zeros(0, np.int32)
+        self.b_offs = np.zeros(len(mine) + 1, dtype=np.int64)
+        np.cumsum([len(r) for r, _ in mine], out=self.b_offs[1:])
+        self.b_splits = np.array([sp for _, sp in mine], dtype=np.int64)
+        self.out = None
+
+    def step(self):
+        from paper_2410_04349_b200._lib import RB_SYMMETRIC
+
+        t0 = time.perf_counter()
+        (t, s, r, p), st = self.prog.run_batch(self.b_refs, self.b_offs, self.b_splits, RB_SYMMETRIC, out=self.out)
+        if self.out is None:  # later steps copy the rows into reusable pinned buffers
+            import torch
+
+            self.out = tuple(torch.empty(max(1, len(t)), dtype=torch.int32, pin_memory=True).numpy() for _ in range(4))
+        self.stage_ms = {"execute": 1e3 * (time.perf_counter() - t0)}
+        return (t, s, r), st
+
+    def e2e_step(self, host_enc):
+        from paper_2410_04349_b200.engine import DeviceRelation, PathProgram
+
+        drel = DeviceRelation(self.ctx, host_enc)
+        p2 = PathProgram(self.w.path, host_enc, compiled=self.prog.program, drel=drel)
+        saved, self.prog = self.prog, p2
+        try:
+            rows, _ = self.step()
+        finally:
+            self.prog = saved
+            p2.close()
+            drel.close()
+        self.d2h = 12 * len(rows[0])
+        return len(rows[0]), {}
+
+
+def make_workload(name, n, seed):
+    from paper_2410_04349_b200 import synth
+
+    if name == "person5_pipeline":
+        w = synth.person5(n, seed=seed)
+        w.name = "person5_pipeline"
+        return w
+    return synth.WORKLOADS[name](n, seed=seed)
+
+
+def job_for(args, w, rank, world, group, dev):
+    if args.workload == "person5_pipeline":
+        return PipelineJob(args, w, rank, world, group, dev)
+    if w.blocks is not None:
+        return BlocksJob(args, w, rank, world, group, dev)
+    return PartitionJob(args, w, rank, world, group, dev)
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle legs (test infrastructure: run after the timed regions)
 
 
 def sample_rows(n, budget_pairs, k=8):
-    """k disjoint row slices spread over the triangle whose pairs sum to
-    ~budget; the whole triangle when it is within budget."""
+    """k disjoint outer-row slices spread over the triangle whose pairs sum
+    to ~budget; the whole triangle when it is within budget."""
     if n * (n - 1) // 2 <= budget_pairs:
         return [(0, n)]
     per = max(1, budget_pairs // k)
@@ -195,65 +480,37 @@ def sample_rows(n, budget_pairs, k=8):
     return out
 
 
-def ncu_capture(w, pairs_step):
-    """(dram bytes per launch, pipe utilisation) of the committed ncu capture
-    of this workload at this size (profiles/traffic.json), or (None, None)."""
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "traffic.json")
-    pipe = None
-    if os.path.exists(tfile):
-        try:  # ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, same workload and size
-            entry = json.load(open(tfile)).get(w.name, {})
-            if entry.get("n") == w.n:
-                traffic = entry.get("bytes_per_launch")
-                m = entry.get("metrics", {})
-                pipe = {k: float(m[k]["value"]) for k in (
-                    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
-                    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
-                    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
-                    "smsp__issue_active.avg.pct_of_peak_sustained_active") if k in m}
-                if "smsp__inst_executed.sum" in m:  # the per-pair instruction cost of the capture
-                    pipe["warp_instructions_per_pair"] = float(m["smsp__inst_executed.sum"]["value"]) / pairs_step
-                pipe["source"] = entry.get("capture")
-                # the busiest issue pipe of the capture: the kernel's speed-of-light fraction
-                # (the inner tuples are reused from shared memory, so DRAM is not the bound)
-                names = {"sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "ALU",
-                         "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "XU",
-                         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "shared memory"}
-                busiest = max((k for k in names if k in pipe), key=lambda k: pipe[k], default=None)
-                if busiest:
-                    pipe["binding"] = {"pipe": names[busiest], "frac": pipe[busiest] / 100.0}
-        except Exception:
-            traffic = None
-    return traffic, pipe
+def unit_sample(units, budget, seed=0):
+    """Indices of whole units (refs, split) in seeded random order whose
+    pairs sum to <= budget, none above budget/4."""
+    rng = np.random.default_rng(seed)
+    chosen, pairs = [], 0
+    for k in rng.permutation(len(units)):
+        refs, sp = units[k]
+        c = sp * (len(refs) - sp) if sp >= 0 else len(refs) * (len(refs) - 1) // 2
+        if c == 0 or c > budget // 4 or pairs + c > budget:
+            continue
+        chosen.append(int(k))
+        pairs += c
+    return chosen
 
 
-def blocks_cpu_parity(w, prog, budget, kms, pairs_step, n_rows):
-    """Block workloads: oracle on a seeded sample of whole blocks (CPU
-    baseline), the same blocks re-run on the GPU for bit-exact parity."""
+def units_parity(job, units, budget, cores):
+    """Oracle on a sample of whole units (CPU baseline), the same units as
+    one GPU batch, rows compared per unit."""
     from oracle import oracle
     from paper_2410_04349_b200._lib import RB_SYMMETRIC
 
-    rng = np.random.default_rng(0)
-    order = rng.permutation(len(w.blocks))
-    chosen, pairs = [], 0
-    for k in order:
-        refs, sp = w.blocks[k]
-        c = sp * (len(refs) - sp) if sp >= 0 else len(refs) * (len(refs) - 1) // 2
-        if c > budget // 4 or pairs + c > budget:
-            continue
-        chosen.append(k)
-        pairs += c
-    cores = os.cpu_count() or 1
-    secs, cmp_total, ok = 0.0, 0, True
-    evals = np.zeros(prog.n_slots, dtype=np.int64)
-    sub = [w.blocks[k] for k in chosen]
+    w, prog = job.w, job.prog
+    chosen = unit_sample(units, budget)
+    sub = [units[k] for k in chosen]
     refs = np.concatenate([r for r, _ in sub]).astype(np.int32)
     offs = np.zeros(len(sub) + 1, dtype=np.int64)
     np.cumsum([len(r) for r, _ in sub], out=offs[1:])
     (gt, gs, gr, gp), _ = prog.run_batch(refs, offs, np.array([sp for _, sp in sub], dtype=np.int64), RB_SYMMETRIC)
     got = sorted(zip(gp.tolist(), gt.tolist(), gs.tolist(), gr.tolist()))
-    want = []
+    want, secs, cmp_total = [], 0.0, 0
+    evals = np.zeros(prog.n_slots, dtype=np.int64)
     for bi, (r, sp) in enumerate(sub):
         t0 = time.perf_counter()
         rows, cmp, ev = oracle.run(w.enc, prog.program, r, len(r), split=sp, flags=1, nthreads=cores)
@@ -261,113 +518,198 @@ def blocks_cpu_parity(w, prog, budget, kms, pairs_step, n_rows):
         cmp_total += cmp
         evals += ev
         want += [(bi, int(a), int(b), int(c)) for a, b, c in rows]
-    ok = sorted(want) == got
     cpu = {"value": cmp_total / secs, "unit": UNIT, "cores": cores, "kind": "port",
-           "sample": f"{len(sub)} whole cross blocks, {cmp_total} pairs (oracle/rb_oracle.c, OpenMP {cores} threads)"}
-    parity = {"blocks_checked": len(sub), "rows_checked": len(want), "pairs_checked": cmp_total, "bit_exact": ok}
-    peak, peak_kind = measured_peak()
-    bpp, terms = algorithmic_bytes_per_pair(w.enc, w.path, evals / max(1, cmp_total), n_rows / max(1, pairs_step))
-    k_ms = float(np.mean(kms))
-    achieved = bpp * pairs_step / (k_ms / 1e3) / 1e9
-    traffic, pipe = ncu_capture(w, pairs_step)
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "ncu_pipes": pipe, "peak_kind": peak_kind, "bytes_per_pair": bpp, "kernel_ms": k_ms, "terms": terms,
-            "model": "SURVEY 8d streaming bytes: sum_s E_s*b_s + 10 B per row; E_s from oracle first-touch counts"}
-    return cpu, parity, roof
+           "sample": f"{len(sub)} whole units (partitions / pulls) of the step, {cmp_total} pairs "
+                     f"(oracle/rb_oracle.c, OpenMP {cores} threads)"}
+    parity = {"units_checked": len(sub), "rows_checked": len(want), "pairs_checked": cmp_total,
+              "bit_exact": sorted(want) == got}
+    return cpu, parity, evals / max(1, cmp_total)
 
 
-def run_reference_blocks(args, w, prog, cores, world):
+def slices_parity(job, budget, cores):
+    """One partition: oracle on outer-row slices, the same slices on the GPU."""
     from oracle import oracle
+    from paper_2410_04349_b200._lib import RB_SYMMETRIC
 
-    rng = np.random.default_rng(0)
-    chosen, pairs = [], 0
-    for k in rng.permutation(len(w.blocks)):
-        refs, sp = w.blocks[k]
-        c = sp * (len(refs) - sp) if sp >= 0 else len(refs) * (len(refs) - 1) // 2
-        if c <= args.cpu_pairs // 4 and pairs + c <= args.cpu_pairs:
-            chosen.append(k)
-            pairs += c
+    w, prog = job.w, job.prog
+    srows = sample_rows(w.n, budget)
+    ok, secs, pairs, nrows = True, 0.0, 0, 0
+    evals = np.zeros(prog.n_slots, dtype=np.int64)
+    for lo, hi in srows:
+        t0 = time.perf_counter()
+        r, cmp, ev = oracle.run(w.enc, prog.program, None, w.n, row_lo=lo, row_hi=hi, flags=1, nthreads=cores)
+        secs += time.perf_counter() - t0
+        pairs += cmp
+        evals += ev
+        nrows += len(r)
+        (gt, gs, gr), _ = prog.run_raw(None, w.n, RB_SYMMETRIC, row_lo=lo, row_hi=hi)
+        ok &= sorted(map(tuple, r.tolist())) == sorted(zip(gt.tolist(), gs.tolist(), gr.tolist()))
+    cpu = {"value": pairs / secs, "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"{len(srows)} outer-row slices of the same relation, {pairs} pairs "
+                     f"(oracle/rb_oracle.c, OpenMP {cores} threads)"}
+    return cpu, {"slices_checked": len(srows), "rows_checked": nrows, "pairs_checked": pairs, "bit_exact": bool(ok)}, \
+        evals / max(1, pairs)
+
+
+def full_rows_checks(job, rows, cores, sample=4_000_000, collected=True):
+    """Size-independent checks over ALL rows of one full step: (t, s)
+    distinct, t < s, sorted when collected; every sampled row's rule is the
+    oracle's first witness of (t, s); recall: every injected duplicate pair
+    the step covers is emitted exactly when the oracle witnesses it."""
+    from oracle import oracle as orc
+
+    w, prog = job.w, job.prog
+    t, s, r = (np.asarray(x.cpu().numpy() if hasattr(x, "cpu") else x) for x in rows)
+    key = t.astype(np.int64) * w.n + s.astype(np.int64)
+    out = {"rows": int(len(t)), "t_lt_s": bool((t < s).all())}
+    if collected:
+        out["sorted_distinct"] = bool((np.diff(key) > 0).all())
+        sk = key
+    else:
+        sk = np.sort(key)
+        out["distinct"] = bool((np.diff(sk) > 0).all())
+    rng = np.random.default_rng(1)
+    pick = rng.choice(len(t), size=min(sample, len(t)), replace=False) if len(t) else np.zeros(0, np.int64)
+    wit = orc.witness(w.enc, prog.program, t[pick], s[pick], nthreads=cores)
+    out["witness_rows_checked"] = int(len(pick))
+    out["witness_exact"] = bool((wit == r[pick]).all())
+    inj = getattr(w, "injected", None)
+    if inj is not None and len(inj[0]):
+        a, b = np.minimum(inj[0], inj[1]).astype(np.int32), np.maximum(inj[0], inj[1]).astype(np.int32)
+        keep = a != b
+        a, b = a[keep], b[keep]
+        covered = np.ones(len(a), dtype=bool) if job.covers is None else job.covers(a, b)
+        wa = orc.witness(w.enc, prog.program, a, b, nthreads=cores)
+        expect = covered & (wa >= 0)
+        k = a.astype(np.int64) * w.n + b
+        pos = np.searchsorted(sk, k)
+        found = (pos < len(sk)) & (sk[np.minimum(pos, len(sk) - 1)] == k)
+        out["recall"] = {"injected_pairs": int(len(a)), "covered": int(covered.sum()), "witnessed": int(expect.sum()),
+                         "emitted": int(found.sum()), "exact": bool((found == expect).all()),
+                         "check": "each injected duplicate (t, s) the step covers is emitted iff "
+                                  "oracle.witness(t, s) >= 0"}
+    return out
+
+
+def covers_for(job):
+    """covers(a, b) -> bool array: does the step evaluate pair (a, b)?"""
+    w = job.w
+    if job.kind == "partition":
+        return None
+    if job.kind == "pipeline":  # pulls on: co-partitioned iff a root key is shared
+        cols = [w.enc.columns[c].data for c in job.cols]
+        return lambda a, b: np.logical_or.reduce([c[a] == c[b] for c in cols])
+    unit_of = np.full(w.n, -1, dtype=np.int64)
+    side = np.zeros(w.n, dtype=np.int8)
+    for k, (refs, sp) in enumerate(w.blocks):
+        unit_of[refs] = k
+        if sp >= 0:
+            side[refs[:sp]] = 1
+    cross = any(sp >= 0 for _, sp in w.blocks)
+    if cross:
+        return lambda a, b: (unit_of[a] == unit_of[b]) & (unit_of[a] >= 0) & (side[a] != side[b])
+    return lambda a, b: (unit_of[a] == unit_of[b]) & (unit_of[a] >= 0)
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU engine restated in C (the oracle
+    port; the reference is Python and has no compiled core to build), with
+    every host thread, on a bounded sample of this workload per step; rank 0."""
+    if rank != 0:
+        return
+    from oracle import oracle
+    from paper_2410_04349_b200.encode import compile_program
+
+    w = make_workload(args.workload, args.n, args.seed)
+    prog = compile_program(w.path, w.enc)
+    cores = os.cpu_count() or 1
+    if args.workload == "person5_pipeline":
+        from paper_2410_04349_b200 import synth
+
+        units = synth.plan_partitions(w.enc, w.path, PIPELINE_MAXP)
+    else:
+        units = w.blocks
+    if units is not None:
+        chosen = unit_sample(units, args.cpu_pairs)
+        total = int(sum(sp * (len(r) - sp) if sp >= 0 else len(r) * (len(r) - 1) // 2 for r, sp in units))
+        desc = "whole units (partitions / pulls)"
+
+        def one(it):
+            c_it = 0
+            for k in chosen[: (4 if it < args.warmup else None)]:
+                refs, sp = units[k]
+                _, c, _ = oracle.run(w.enc, prog, refs, len(refs), split=sp, flags=1, nthreads=cores)
+                c_it += c
+            return c_it
+        n_sample = len(chosen)
+    else:
+        rows = sample_rows(w.n, args.cpu_pairs)
+        total = w.n * (w.n - 1) // 2
+        desc = "outer-row slices"
+
+        def one(it):
+            c_it = 0
+            for lo, hi in rows[: (1 if it < args.warmup else None)]:
+                _, c, _ = oracle.run(w.enc, prog, None, w.n, row_lo=lo, row_hi=hi, flags=1, nthreads=cores)
+                c_it += c
+            return c_it
+        n_sample = len(rows)
     secs = cmp = 0
     for it in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        c_it = 0
-        for k in chosen[: (4 if it < args.warmup else None)]:
-            refs, sp = w.blocks[k]
-            _, c, _ = oracle.run(w.enc, prog, refs, len(refs), split=sp, flags=1, nthreads=cores)
-            c_it += c
+        c_it = one(it)
         if it >= args.warmup:
             secs += time.perf_counter() - t0
             cmp += c_it
     v = cmp / secs
-    total = w.pairs()
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{w.name} n={w.n} ({WORKLOAD_DESC.get(w.name, w.name)}), {len(w.blocks)} blocks",
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"{w.name} n={w.n} ({WORKLOAD_DESC.get(w.name, w.name)})",
                    "pairs_per_step_full": total, "sample_pairs_per_step": cmp // args.steps},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{len(chosen)} whole cross blocks, {cmp // args.steps} pairs per step"},
+                         "sample": f"{n_sample} {desc}, {cmp // args.steps} pairs per step; the full step "
+                                   f"extrapolates to {total / v:.0f} s"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "blocking_wall_s_full_extrapolated": total / v,
     }
     print(json.dumps(line), flush=True)
 
 
-def run_reference(args, rank, world):
-    """--impl reference: the reference CPU engine restated in C (oracle), all
-    host threads, bounded sample per step; rank 0 only."""
-    if rank != 0:
-        return
-    from paper_2410_04349_b200 import synth
-    from paper_2410_04349_b200.encode import compile_program
-
-    w = synth.WORKLOADS[args.workload](args.n, seed=args.seed)
-    prog = compile_program(w.path, w.enc)
-    cores = os.cpu_count() or 1
-    if w.blocks is not None:
-        return run_reference_blocks(args, w, prog, cores, world)
-    rows = sample_rows(w.n, args.cpu_pairs)
-    for _ in range(args.warmup):
-        cpu_sample(w, prog, rows[:1], cores)
-    pairs = secs = 0
-    for _ in range(args.steps):
-        _, p, s, _ = cpu_sample(w, prog, rows, cores)
-        pairs += p
-        secs += s
-    v = pairs / secs
-    total_pairs = w.n * (w.n - 1) // 2
-    line = {
-        "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{w.name} n={w.n} ({WORKLOAD_DESC.get(w.name, w.name)}), one symmetric partition",
-                   "pairs_per_step_full": total_pairs, "sample_pairs_per_step": pairs // args.steps},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{len(rows)} outer-row slices, {pairs // args.steps} pairs per step; "
-                                   f"full step extrapolates to {total_pairs / v:.0f} s"},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "blocking_wall_s_full_extrapolated": total_pairs / v,
-    }
-    print(json.dumps(line), flush=True)
+# ---------------------------------------------------------------------------
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="citation3")
-    ap.add_argument("--tuples", dest="n", type=int, default=1_000_000, help="tuples per GPU")
-    ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--workload", default="person5_pipeline", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--tuples", dest="n", type=int, default=None, help="tuples in the relation")
+    ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--cpu-pairs", type=int, default=120_000_000, help="oracle sample size (pairs)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the config 4 (ii) single-partition leg")
     args = ap.parse_args()
     rank, world, local = dist_env()
+    if args.gpus is not None and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args.gpus))
+    if args.gpus is not None and args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.warmup < 3:
         args.warmup = 3
+    if args.n is None:
+        args.n = DEFAULT_TUPLES.get(args.workload, 1_000_000)
+    if args.seed is None:
+        args.seed = {"person5_pipeline": 4, "person5": 4, "person5_parts": 4, "edit_heavy": 11,
+                     "linkage": 5}.get(args.workload, 2024)
 
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -379,25 +721,23 @@ def main():
     ndev = max(1, torch.cuda.device_count())
     dev = local % ndev
     torch.cuda.set_device(dev)
-    # one rank per GPU over NCCL; ranks sharing a GPU (functional tests on a
-    # 1-GPU box) reduce over gloo instead
+    # one rank per GPU over NCCL; ranks sharing a GPU (functional runs on a
+    # 1-GPU box) exchange over gloo on host copies instead
     backend = "nccl" if world <= ndev else "gloo"
-    red_dev = "cuda" if backend == "nccl" else "cpu"
+    group = None
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group("gloo")
+        group = dist.group.WORLD
+    red_dev = "cuda" if backend == "nccl" else "cpu"
 
-    from paper_2410_04349_b200 import synth
-    from paper_2410_04349_b200._lib import RB_SYMMETRIC
-    from paper_2410_04349_b200.engine import DeviceRelation, PathProgram, context
-
-    w = synth.WORKLOADS[args.workload](args.n, seed=args.seed + rank)
-    ctx = context(dev)
-    stream = torch.cuda.current_stream()
-    ctx.set_stream(stream.cuda_stream)
-    prog = PathProgram(w.path, w.enc, device=dev)
+    t_gen = time.perf_counter()
+    w = make_workload(args.workload, args.n, args.seed)  # the same relation on every rank
+    gen_s = time.perf_counter() - t_gen
+    job = job_for(args, w, rank, world, group, dev)
+    job.covers = covers_for(job)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -405,183 +745,153 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    if w.blocks is not None:  # many cross blocks / partitions: one batched launch per step
-        b_refs = pin_array(np.concatenate([r for r, _ in w.blocks]).astype(np.int32))  # the batch's input refs
-        b_offs = np.zeros(len(w.blocks) + 1, dtype=np.int64)
-        np.cumsum([len(r) for r, _ in w.blocks], out=b_offs[1:])
-        b_splits = np.array([sp for _, sp in w.blocks], dtype=np.int64)
-
-        def step(p, host=True):
-            (t, s, r, _), st_ = p.run_batch(b_refs, b_offs, b_splits, RB_SYMMETRIC,
-                                            out=None if host_rows is None else host_rows + (host_part,))
-            return (t, s, r), st_
-    elif world > 1 and backend == "nccl":
-        # N GPUs: each rank evaluates its partition, then the final collect is
-        # one NCCL all-gather of the row counts and of the rows themselves,
-        # straight from the device result buffers (distributed.gather_rows)
-        from paper_2410_04349_b200.distributed import gather_rows, run_rows_device
-
-        gathered = [0]
-
-        def step(p, host=False):
-            rows_d, st_ = run_rows_device(p, None, w.n, RB_SYMMETRIC, 0, w.n)
-            allrows = gather_rows(rows_d)
-            gathered[0] = int(allrows.shape[0])
-            if host:  # the e2e leg reads the collected rows back
-                allrows.cpu()
-            return (rows_d[:, 0], rows_d[:, 1], rows_d[:, 2]), st_
-    else:
-        def step(p, host=True):
-            return p.run_raw(None, w.n, RB_SYMMETRIC, out=host_rows)
-
-    # result rows land in reusable pinned host buffers (sized by the first run)
-    host_rows = None
-    rows, st = step(prog)
-    host_rows = pinned_rows(len(rows[0]))
-    host_part = pinned_rows(len(rows[0]))[0]
-    for _ in range(args.warmup - 1):
-        rows, st = step(prog)
-    n_rows = len(rows[0])
+    for _ in range(args.warmup):
+        rows, st = job.step()
     pairs_step = int(st.comparisons)
 
-    times, kms, vms = [], [], []
+    times, kms, stages = [], [], []
     sampler = ClockSampler(dev)
     with sampler:
-        for _ in range(args.steps):
+        for k in range(args.steps):
             flush.fill_(1)
             barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
-            h0 = time.perf_counter()
-            e0.record(stream)
-            rows, st = step(prog)
-            e1.record(stream)
+            e0.record(job.stream)
+            rows, st = job.step(keep_parts=True) if (job.kind == "pipeline" and k == args.steps - 1) else job.step()
+            e1.record(job.stream)
             torch.cuda.synchronize()
-            h1 = time.perf_counter()
             times.append(e0.elapsed_time(e1))
-            kms.append(st.pair_ms if st.pair_ms > 0 else st.kernel_ms)  # the dominant (pair) kernel
-            vms.append(st.kernel_ms - kms[-1])  # deferred verification kernel
-            print(f"step: events {times[-1]:.1f} ms, kernels {st.kernel_ms:.1f} ms (pair {kms[-1]:.1f}), "
-                  f"host {1e3 * (h1 - h0):.1f} ms, "
-                  f"survivors {st.survivors}, rows {len(rows[0])}, launches {st.launches}, retries {st.retries}",
+            kms.append(st.pair_ms if st.pair_ms > 0 else st.kernel_ms)
+            stages.append(dict(job.stage_ms))
+            print(f"step: {times[-1]:.1f} ms, pair kernel {kms[-1]:.1f} ms, stages "
+                  + ", ".join(f"{a} {b:.1f}" for a, b in job.stage_ms.items())
+                  + f", survivors {st.survivors}, rows {len(rows[0])}, launches {st.launches}, retries {st.retries}",
                   file=sys.stderr)
-            assert st.comparisons == pairs_step and len(rows[0]) == n_rows
+            assert int(st.comparisons) == pairs_step
+    clocks = sampler.summary()
     barrier()
     t_total = torch.tensor([sum(times)], dtype=torch.float64, device=red_dev)
-    counts = torch.tensor([pairs_step * args.steps, n_rows], dtype=torch.float64, device=red_dev)
+    counts = torch.tensor([pairs_step * args.steps, len(rows[0])], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t_total, op=dist.ReduceOp.MAX)
         dist.all_reduce(counts, op=dist.ReduceOp.SUM)
     ms_step = t_total.item() / args.steps
     value = counts[0].item() / (t_total.item() / 1e3)
+    pairs_total_step = int(counts[0].item()) // args.steps
+    stage_mean = {k: float(np.mean([s.get(k, 0.0) for s in stages])) for k in stages[-1]}
 
-    # ---- e2e: host buffers through the C ABI, copies inside the timed region.
-    # The step's inputs (the encoded columns) sit in pinned host memory, as a
-    # loader would leave them; pinning happens once, outside the timed region.
+    # ---- e2e through the public API from pinned host buffers
     e2e_steps = args.e2e_steps or max(1, min(args.steps, 3))
     host_enc = pinned_encoding(w.enc)
-    h2d = sum(c.data.nbytes + (0 if c.offsets is None else c.offsets.nbytes)
-              + (0 if c.missing is None else c.missing.nbytes) for c in w.enc.columns)
-    h2d += prog.program.tables.nbytes + prog.program.slots.nbytes + 4 * 4 * len(prog.program.ins_op)
-    # one untimed pass first: the stream-ordered pool grows to the e2e working set once
-    drel = DeviceRelation(ctx, host_enc)
-    p2 = PathProgram(w.path, host_enc, compiled=prog.program, drel=drel)
-    step(p2)
-    p2.close()
-    drel.close()
+    job.e2e_step(host_enc)  # untimed: the stream-ordered pool grows to the working set once
     barrier()
     t0 = time.perf_counter()
-    phase = {"upload": 0.0, "program": 0.0, "run": 0.0, "free": 0.0}
+    e2e_tm = []
     for _ in range(e2e_steps):
-        q0 = time.perf_counter()
-        drel = DeviceRelation(ctx, host_enc)  # H2D of every encoded column
-        q1 = time.perf_counter()
-        p2 = PathProgram(w.path, host_enc, compiled=prog.program, drel=drel)  # H2D of the program
-        q2 = time.perf_counter()
-        rows2, st2 = step(p2, host=True)  # evaluate + D2H of the rows
-        q3 = time.perf_counter()
-        print(f"e2e step: kernels {st2.kernel_ms:.1f} ms (pair {st2.pair_ms:.1f}), launches {st2.launches}, "
-              f"retries {st2.retries}", file=sys.stderr)
-        assert len(rows2[0]) == n_rows
-        p2.close()
-        drel.close()
-        q4 = time.perf_counter()
-        for k, v in zip(phase, (q1 - q0, q2 - q1, q3 - q2, q4 - q3)):
-            phase[k] += v / e2e_steps
-    print("e2e phases (s): " + ", ".join(f"{k} {v:.4f}" for k, v in phase.items()), file=sys.stderr)
+        _, tm = job.e2e_step(host_enc)
+        e2e_tm.append(tm)
     torch.cuda.synchronize()
     e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e_value = counts[0].item() / args.steps / e2e_s.item()
-    nccl_collect = world > 1 and backend == "nccl" and w.blocks is None
-    d2h = 12 * (gathered[0] if nccl_collect else n_rows) + 8 * 68
+    e2e_value = pairs_total_step / e2e_s.item()
+    e2e_phases = {k: float(np.mean([t[k] for t in e2e_tm])) for k in (e2e_tm[0] if e2e_tm and e2e_tm[0] else {})}
 
-    # ---- CPU oracle sample (rank 0, N = 1): baseline + parity on the same rows
-    cpu = None
-    parity = None
-    roof = None
-    peak, peak_kind = measured_peak()
-    if rank == 0 and world == 1 and not args.no_cpu and w.blocks is not None:
-        cpu, parity, roof = blocks_cpu_parity(w, prog, args.cpu_pairs, kms, pairs_step, n_rows)
-    elif rank == 0 and world == 1 and not args.no_cpu:
+    # ---- config 4 (ii): the same relation as one partition (strong-scaled rows)
+    secondary = None
+    if args.workload == "person5_pipeline" and not args.no_secondary:
+        pj = PartitionJob(args, w, rank, world, group, dev)
+        pj.prog = job.prog
+        pj.covers = None  # one partition covers every pair
+        pj.step(lo=pj.lo, hi=min(pj.hi, pj.lo + 2000))  # warm: the single-partition kernel variant
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(job.stream)
+        rows2, st2 = pj.step()
+        e1.record(job.stream)
+        torch.cuda.synchronize()
+        t2 = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=red_dev)
+        c2 = torch.tensor([float(st2.comparisons)], dtype=torch.float64, device=red_dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+            dist.all_reduce(c2, op=dist.ReduceOp.SUM)
+        secondary = {"workload": f"person5 n={w.n}: {WORKLOAD_DESC['person5']} (4.9999999e13 pairs at 10M)",
+                     "value": c2.item() / (t2.item() / 1e3), "unit": UNIT, "ms_per_step": t2.item(), "steps": 1,
+                     "pairs_per_step": int(c2.item()), "rows": int(len(rows2[0])),
+                     "pair_kernel_ms": float(st2.pair_ms), "stages_ms": pj.stage_ms,
+                     "parallelism": f"outer rows split by equal pair count x{world}, NCCL all-gather of rows"
+                                    if world > 1 else "one GPU"}
+        pj_rows = rows2
+        del rows2
+
+    # ---- CPU oracle: baseline + parity (rank 0 at N = 1)
+    cpu = parity = None
+    evals_frac = None
+    if rank == 0 and world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
-        srows = sample_rows(w.n, args.cpu_pairs)
-        orc_rows, orc_pairs, orc_s, orc_evals = cpu_sample(w, prog.program, srows, cores)
-        cpu = {"value": orc_pairs / orc_s, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{len(srows)} outer-row slices of the same relation, {orc_pairs} pairs "
-                         f"(oracle/rb_oracle.c, OpenMP {cores} threads)"}
-        ok = True
-        for lo, hi in srows:
-            (gt, gs, gr), gst = prog.run_raw(None, w.n, RB_SYMMETRIC, row_lo=lo, row_hi=hi)
-            sel = (orc_rows[:, 0] >= lo) & (orc_rows[:, 0] < hi)
-            want = sorted(map(tuple, orc_rows[sel].tolist()))
-            got = sorted(zip(gt.tolist(), gs.tolist(), gr.tolist()))
-            ok &= want == got
-        parity = {"rows_checked": int(len(orc_rows)), "pairs_checked": int(orc_pairs), "bit_exact": bool(ok)}
-        # every row of the last timed step: a true match (refs = identity, so t is the
-        # lower tid), carrying the oracle's first witness, no pair twice
-        from oracle import oracle as _orc
+        t_chk = time.perf_counter()
+        if job.kind == "pipeline":
+            refs, base, size, split, rbase, _, _ = job.rp.parts.host()
+            units = []
+            for k in range(len(base)):
+                if rbase[k] >= 0:  # a pull: left sibling then right sibling
+                    u = np.concatenate([refs[base[k]:base[k] + split[k]], refs[rbase[k]:rbase[k] + size[k] - split[k]]])
+                else:
+                    u = refs[base[k]:base[k] + size[k]]
+                units.append((u, int(split[k])))
+            cpu, parity, evals_frac = units_parity(job, units, args.cpu_pairs, cores)
+            parity["step_units"] = len(units)
+            parity["full_step"] = full_rows_checks(job, rows, cores, collected=True)
+            job.rp.parts.close()
+            if secondary is not None:  # 4 (ii): slices + full-row checks of its step
+                c2, p2, _ = slices_parity(pj, args.cpu_pairs // 2, cores)
+                p2["full_step"] = full_rows_checks(pj, pj_rows, cores, collected=False)
+                secondary["parity"] = p2
+                secondary["cpu_baseline"] = c2
+        elif job.kind == "blocks":
+            cpu, parity, evals_frac = units_parity(job, w.blocks, args.cpu_pairs, cores)
+            parity["full_step"] = full_rows_checks(job, rows, cores, collected=False)
+        else:
+            cpu, parity, evals_frac = slices_parity(job, args.cpu_pairs, cores)
+            parity["full_step"] = full_rows_checks(job, rows, cores, collected=False)
+        parity["check_s"] = time.perf_counter() - t_chk
 
-        at, as_, ar = (np.asarray(x) for x in rows)
-        wit = _orc.witness(w.enc, prog.program, at, as_, nthreads=cores)
-        key = at.astype(np.int64) * w.n + as_
-        parity["all_step_rows"] = {"rows": int(len(at)), "witness_exact": bool((wit == ar).all()),
-                                   "ordered": bool((at < as_).all()), "distinct": bool(len(np.unique(key)) == len(key)),
-                                   "check": "oracle.witness on every emitted (t, s): rule == oracle first witness"}
-        bpp, terms = algorithmic_bytes_per_pair(w.enc, w.path, orc_evals / max(1, orc_pairs), n_rows / pairs_step)
-        k_ms = float(np.mean(kms))
-        achieved = bpp * pairs_step / (k_ms / 1e3) / 1e9
-        traffic, pipe = ncu_capture(w, pairs_step)
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_kind": peak_kind,
-                "true_bound": "integer pipes: XU (POPC) and ALU issue (inner tuples are reused from shared "
-                              "memory, so DRAM is not the limit; see DESIGN.md 3.1)",
-                "ncu_pipes": pipe,
-                "model": "SURVEY 8d streaming bytes: sum_s E_s*b_s + 10 B per row; E_s from oracle first-touch counts",
-                "bytes_per_pair": bpp, "kernel_ms": k_ms, "verify_kernel_ms": float(np.mean(vms)),
-                "kernel": "rb_pair_kernel_spec (phase 1; CUDA events on the engine's stream)", "terms": terms}
+    k_ms = float(np.mean(kms))
+    bpp = terms = None
+    if evals_frac is not None:
+        bpp, terms = algorithmic_bytes_per_pair(w.enc, w.path, evals_frac, len(rows[0]) / max(1, pairs_step))
+    roof = roofline(w.name, w.n, pairs_step, k_ms, clocks, bpp, terms)
+    roof["kernel"] = "rb_pair_kernel_spec (NVRTC-specialised pair kernel; CUDA events on the engine's stream)"
+    roof["kernel_share_of_step"] = k_ms / (t_total.item() / args.steps) if world == 1 else None
 
-    clocks = sampler.summary()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": f"{w.name} n={w.n} per GPU ({WORKLOAD_DESC.get(w.name, w.name)}), "
-                                   + (f"{len(w.blocks)} blocks in one batched launch per GPU" if w.blocks is not None
-                                      else "one symmetric partition per GPU"),
-                       "pairs_per_step_per_gpu": pairs_step, "rows_per_step_per_gpu": n_rows,
-                       "l2": "flushed (512 MiB write) between timed steps", "parallelism": f"partition-per-gpu x{world}",
-                       "collective": (f"{backend}: all-gather of row counts and rows (final collect)"
-                                      if world > 1 and backend == "nccl" and w.blocks is None
-                                      else backend if world > 1 else None)},
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"{w.name} n={w.n} ({WORKLOAD_DESC.get(w.name, w.name)})",
+                       "pairs_per_step": pairs_total_step, "rows_per_step_rank0": int(len(rows[0])),
+                       "l2": "flushed (512 MiB write) between timed steps; relation > L2",
+                       "parallelism": (f"strong x{world}: " + {"pipeline": "LPT shares of the units, rows exchanged "
+                                                                          "by t range (NCCL all-to-all) + collect",
+                                                              "partition": "outer rows split by equal pair count, "
+                                                                           "NCCL all-gather of rows",
+                                                              "blocks": "LPT shares of the blocks"}[job.kind])
+                       if world > 1 else "one GPU",
+                       "collective": backend if world > 1 else None},
             "blocking_wall_s": ms_step / 1e3,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "blocking_wall_s": e2e_s.item()},
-            "roofline": roof, "cpu_baseline": cpu, "parity": parity,
+            "stages_ms": stage_mean,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(job.h2d),
+                    "d2h_bytes_per_step": int(job.d2h), "blocking_wall_s": e2e_s.item(),
+                    "api": {"pipeline": "pipeline.run_pipeline_encoded (host Encoded columns)",
+                            "partition": "DeviceRelation + PathProgram + run_rows_device",
+                            "blocks": "DeviceRelation + PathProgram + PathProgram.run_batch"}[job.kind],
+                    "phases_s": e2e_phases},
+            "roofline": roof, "cpu_baseline": cpu, "parity": parity, "secondary": secondary,
             "gpu_launches": int(st.launches) * args.steps,
-            "clocks": clocks,
+            "clocks": clocks, "workload_gen_s": gen_s,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

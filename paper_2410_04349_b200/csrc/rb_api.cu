@@ -62,6 +62,7 @@ int rb_ctx_create(int device, rb_ctx** out) {
     if (!c) return fail(RB_ERR_OOM, "host allocation failed");
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
+    c->mem_total = prop.totalGlobalMem;
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
@@ -105,6 +106,9 @@ int rb_ctx_destroy(rb_ctx* c) {
     c->scratch.release(c->stream);
     c->surv.release(c->stream);
     c->offs.release(c->stream);
+    for (DevBuf* b : {&c->col_k0, &c->col_k1, &c->col_flag, &c->col_temp, &c->col_r1, &c->col_r2, &c->col_cnt,
+                      &c->col_out[0], &c->col_out[1], &c->col_out[2]})
+        b->release(c->stream);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->ev_mid) cudaEventDestroy(c->ev_mid);
@@ -1049,7 +1053,10 @@ int rb::run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t tot
     // RB_SURV_LIMIT / RB_SURV_MIN override both bounds (tests drive the retry and fallback paths with them)
     const char* env_lim = std::getenv("RB_SURV_LIMIT");
     const char* env_min = std::getenv("RB_SURV_MIN");
-    const long long SURV_LIMIT = env_lim ? std::max(1ll, std::atoll(env_lim)) : 1ll << 28;
+    // survivor buffer limit: 16 B per entry; 2^30 entries (17 GB) on a GPU with
+    // HBM to spare (B200: 180 GB) so a pass with hundreds of millions of
+    // survivors streams in one range instead of several serialised ones
+    const long long SURV_LIMIT = env_lim ? std::max(1ll, std::atoll(env_lim)) : (c->mem_total >= (96ull << 30) ? 1ll << 30 : 1ll << 28);
     const long long SURV_MIN = env_min ? std::max(1ll, std::atoll(env_min)) : 1ll << 24;
     const bool defer = J.ok && J.defer;
     // capacity: the program's last survivor count, or whatever the context's
@@ -1067,7 +1074,12 @@ int rb::run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t tot
     const int grid_v = c->sm_count * (J.ok ? J.verify_blocks_per_sm : 1);  // deferred verification
     int64_t stride = 0;
     if (P->lmax_edit >= 0) {
-        stride = (P->lmax_edit + 2 + 31) & ~(int64_t)31;
+        // a slice holds the banded DP row, or Myers' pattern table for bounds
+        // above 31 (rb_device.cuh lev_myers: 2 x MYERS_HS slots + MYERS_DCAP x W
+        // 64-bit masks, W = ceil(min(L, MYERS_NMAX) / 64))
+        int64_t need = P->lmax_edit + 2;
+        if (P->lmax_edit > 31) need = std::max<int64_t>(need, 2 * 64 + 2 * 48 * ((std::min<int64_t>(P->lmax_edit, 1024) + 63) / 64));
+        stride = (need + 31) & ~(int64_t)31;
         const size_t slices = (size_t)std::max(grid, std::max(gridg, grid_v)) * BLOCK;
         if (cudaError_t e = c->scratch.grow(sizeof(int32_t) * stride * slices, c->stream))
             return cleanup(fail(RB_ERR_OOM, "edit scratch (%lld B): %s",

@@ -270,14 +270,98 @@ static __device__ __forceinline__ int slide(const DevColumn& cs, int64_t s0, int
     return i;
 }
 
+// Myers' bit-vector Levenshtein distance (Myers 1999, the block form with
+// the horizontal delta carried from word to word): the shorter string is the
+// pattern, 64 of its positions per machine word; every character of the other
+// string advances all W = ceil(n/64) words by ~15 integer ops, so a pair costs
+// O(ceil(n/64) m) word steps instead of the band's O(n k) cells.  The
+// pattern's match masks Peq[c] live in the thread's scratch slice: an
+// open-addressed table of its distinct characters (at most MYERS_DCAP) and
+// MYERS_DCAP x W masks.  Stops as soon as the last row's score minus the
+// columns left exceeds k (the final score cannot come back under k).
+// Returns the exact distance when <= k, k+1 when above, -1 when the pattern
+// does not fit (longer than MYERS_NMAX or more than MYERS_DCAP distinct
+// characters): the caller then runs the banded DP.
+#define MYERS_NMAX 1024
+#define MYERS_DCAP 48
+#define MYERS_HS 64  // hash slots (power of two > MYERS_DCAP)
+static __device__ __forceinline__ int myers_slot(const int32_t* hkey, uint32_t c) {
+    uint32_t h = (c * 0x9E3779B1u) >> 26;  // 6 bits: MYERS_HS slots
+    while (true) {
+        const int32_t k = hkey[h];
+        if (k == (int32_t)c || k == -1) return (int)h;
+        h = (h + 1) & (MYERS_HS - 1);
+    }
+}
+static __device__ int lev_myers(const DevColumn& cs, int64_t s0, int n, const DevColumn& cl, int64_t l0, int m,
+                                int k, int32_t* scr) {
+    if (n > MYERS_NMAX) return -1;
+    const int W = (n + 63) >> 6;
+    int32_t* hkey = scr;
+    int32_t* hidx = scr + MYERS_HS;
+    uint64_t* peq = (uint64_t*)(scr + 2 * MYERS_HS);  // 8-byte aligned: the slice is 128-byte aligned
+    for (int h = 0; h < MYERS_HS; h++) hkey[h] = -1;
+    int D = 0;
+    for (int i = 0; i < n; i++) {
+        const uint32_t c = char_at(cs, s0 + i);
+        const int h = myers_slot(hkey, c);
+        int idx = hidx[h];
+        if (hkey[h] == -1) {
+            if (D == MYERS_DCAP) return -1;
+            hkey[h] = (int32_t)c;
+            hidx[h] = idx = D++;
+            for (int w = 0; w < W; w++) peq[idx * W + w] = 0;
+        }
+        peq[idx * W + (i >> 6)] |= 1ull << (i & 63);
+    }
+    uint64_t Pv[MYERS_NMAX / 64], Mv[MYERS_NMAX / 64];
+    for (int w = 0; w < W; w++) {
+        Pv[w] = ~0ull;
+        Mv[w] = 0;
+    }
+    const int last = (n - 1) & 63;
+    int score = n;
+    for (int j = 0; j < m; j++) {
+        const uint32_t c = char_at(cl, l0 + j);
+        const int h = myers_slot(hkey, c);
+        const uint64_t* eqv = hkey[h] == -1 ? nullptr : peq + hidx[h] * W;
+        int hin = 1;  // the top row D[0][j] = j rises by one per column
+        for (int w = 0; w < W; w++) {
+            uint64_t Eq = eqv ? eqv[w] : 0ull;
+            const uint64_t pv = Pv[w], mv = Mv[w];
+            const uint64_t Xv = Eq | mv;
+            if (hin < 0) Eq |= 1ull;
+            const uint64_t Xh = (((Eq & pv) + pv) ^ pv) | Eq;
+            uint64_t Ph = mv | ~(Xh | pv);
+            uint64_t Mh = pv & Xh;
+            const int high = (w == W - 1) ? last : 63;
+            const int hout = (int)((Ph >> high) & 1ull) - (int)((Mh >> high) & 1ull);
+            Ph <<= 1;
+            Mh <<= 1;
+            if (hin < 0)
+                Mh |= 1ull;
+            else if (hin > 0)
+                Ph |= 1ull;
+            Pv[w] = Mh | ~(Xv | Ph);
+            Mv[w] = Ph & Xv;
+            hin = hout;
+        }
+        score += hin;
+        if (score - (m - 1 - j) > k) return k + 1;
+    }
+    return score <= k ? score : k + 1;
+}
+
 // Bounded Levenshtein: exact when the distance is <= k, otherwise k+1.
 // For k <= 31 (every threshold the configs use) it is Landau-Vishkin /
 // Ukkonen's diagonal algorithm: for e = 0..k edits keep, per diagonal
 // d = j - i, the furthest row reachable with e edits, then slide along
 // matching characters.  Cost O(k^2 + slide length) instead of the band's
 // O(n k) cells; near-duplicate strings slide almost all the way at e = 0.
-// Wider bounds run a banded DP over the thread's slice of the global
-// scratch row.
+// Wider bounds first try the same diagonal algorithm up to 31 edits (a
+// near duplicate is decided there), then Myers' bit-vector algorithm; a
+// pattern Myers cannot hold runs a banded DP over the thread's slice of
+// the global scratch.
 static __device__ int lev_bounded(const DevColumn& ca, int64_t a0, int la, const DevColumn& cb, int64_t b0, int lb, int k,
                            int32_t* row) {
     const DevColumn* cs = &ca;
@@ -295,7 +379,8 @@ static __device__ int lev_bounded(const DevColumn& ca, int64_t a0, int la, const
     const int INF = k + 1;
     if (m - n > k) return INF;
     if (n == 0) return m;
-    if (k <= 31) {
+    {
+        const int kd = min(k, 31);  // the diagonal algorithm's own bound
         constexpr int OFF = 32, NEG = -(1 << 30);
         int fr0[2 * OFF + 1], fr1[2 * OFF + 1];  // furthest row per diagonal, index OFF + d
         int* prev = fr0;
@@ -304,7 +389,7 @@ static __device__ int lev_bounded(const DevColumn& ca, int64_t a0, int la, const
         int i = slide(*cs, s0, n, *cl, l0, m, 0, 0);
         if (dfin == 0 && i >= n) return 0;
         prev[OFF] = i;
-        for (int e = 1; e <= k; e++) {
+        for (int e = 1; e <= kd; e++) {
             for (int d = -e; d <= e; d++) {
                 int best = NEG;
                 if (d >= -(e - 1) && d <= e - 1) best = prev[OFF + d] + 1;                      // substitution
@@ -323,8 +408,10 @@ static __device__ int lev_bounded(const DevColumn& ca, int64_t a0, int la, const
             prev = cur;
             cur = t;
         }
-        return INF;
+        if (k <= 31) return INF;
     }
+    const int dm = lev_myers(*cs, s0, n, *cl, l0, m, k, row);
+    if (dm >= 0) return dm;
     for (int j = 0; j <= m; j++) row[j] = min(j, INF);
     for (int i = 1; i <= n; i++) {
         const uint32_t ai = char_at(*cs, s0 + i - 1);

@@ -17,7 +17,9 @@
 // All of it is HBM streaming (sort passes): no tensor-core work here.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <numeric>
 #include <queue>
@@ -31,8 +33,13 @@ struct rb_parts {
     int64_t n = 0;            // tuples per branch
     int32_t n_branches = 0;
     int32_t* d_refs = nullptr;  // n_branches * n tuple ids, branch by branch
-    std::vector<Part> parts;    // partitions (in iter_partitions order), then pulls
+    // the partitions with more than one tuple (in iter_partitions order), then
+    // the pulls; every other position of a branch is a single-tuple partition
+    // (no pairs), implied by the gaps -- rb_parts_copy lists them too
+    std::vector<Part> parts;
     std::vector<int32_t> branch, sibling;
+    std::vector<int32_t> branch_ids;  // branch id of position range [b*n, (b+1)*n)
+    int64_t n_kept = 0;               // entries of parts that are partitions
     int64_t n_partitions = 0, n_pulls = 0, n_groups = 0;
 };
 
@@ -100,6 +107,24 @@ __global__ void deal_siblings(const Deal* __restrict__ deals, const int32_t* __r
         const int64_t sub = i % d.k, idx = i / d.k;
         const int64_t pos = sub * q + (sub < r ? sub : r) + idx;
         dst[d.start + pos] = src[d.start + i];
+    }
+}
+
+// groups of more than one tuple: (run index, start, size) of each, compacted
+// in order; the exclusive scan of the run lengths gives the starts
+__global__ void flag_multi(const int32_t* __restrict__ counts, const int64_t* __restrict__ runs,
+                           uint8_t* __restrict__ flag) {
+    const int64_t k = *runs;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = counts[i] > 1;
+}
+__global__ void gather_groups(const int32_t* __restrict__ sel, const int64_t* __restrict__ n_sel,
+                              const int32_t* __restrict__ counts, const int64_t* __restrict__ starts,
+                              longlong4* __restrict__ out) {
+    const int64_t k = *n_sel;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t g = sel[i];
+        out[i] = make_longlong4(g, starts[g], counts[g], 0);
     }
 }
 
@@ -186,8 +211,11 @@ struct Scratch {
     } while (0)
 
 // One branch: sort, run-length groups, deal oversize groups; appends the
-// branch's partitions to P (positions offset by `base`), returns the sibling
-// ranges of every oversize group for the pulls.
+// branch's partitions of more than one tuple to P (positions offset by
+// `base`), returns the sibling ranges of every oversize group for the pulls.
+// Only those groups come back to the host: the group sizes are scanned and
+// compacted on the device (a 10M-tuple branch of mostly unique keys has
+// millions of single-tuple groups, which evaluate no pairs).
 int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, int key_bits, int64_t base,
                      int32_t branch, int64_t maxp, int& sibling_counter,
                      std::vector<std::vector<std::pair<int64_t, int64_t>>>& sib_ranges) {
@@ -196,36 +224,60 @@ int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, i
     const int64_t n = P->n;
     Scratch S(st);
     uint64_t *key_out, *uniq;
-    int32_t *counts, *tid_out;
-    int64_t* d_runs;
+    int32_t *counts, *tid_out, *sel;
+    int64_t *d_runs, *starts, *d_sel;
+    uint8_t* flag;
+    longlong4* groups;
     CKS(S.get(&key_out, n));
     CKS(S.get(&tid_out, n));
     CKS(S.get(&uniq, n));
     CKS(S.get(&counts, n));
+    CKS(S.get(&starts, n));
+    CKS(S.get(&flag, n));
+    CKS(S.get(&sel, n));
     CKS(S.get(&d_runs, 1));
-    size_t tb1 = 0, tb2 = 0;
+    CKS(S.get(&d_sel, 1));
+    size_t tb1 = 0, tb2 = 0, tb3 = 0, tb4 = 0;
     CKS(cub::DeviceRadixSort::SortPairs(nullptr, tb1, d_key_in, key_out, d_tid_in, tid_out, n, 0,
                                         std::max(1, key_bits), st));
     CKS(cub::DeviceRunLengthEncode::Encode(nullptr, tb2, key_out, uniq, counts, d_runs, n, st));
+    CKS(cub::DeviceScan::ExclusiveSum(nullptr, tb3, counts, starts, n, st));
+    CKS(cub::DeviceSelect::Flagged(nullptr, tb4, thrust::counting_iterator<int32_t>(0), flag, sel, d_sel, n, st));
+    const size_t tbm = std::max(std::max(tb1, tb2), std::max(tb3, tb4));
     void* temp;
-    CKS(S.get((char**)&temp, std::max(tb1, tb2)));
-    size_t tb = std::max(tb1, tb2);
+    CKS(S.get((char**)&temp, tbm));
+    size_t tb = tbm;
     CKS(cub::DeviceRadixSort::SortPairs(temp, tb, d_key_in, key_out, d_tid_in, tid_out, n, 0,
                                         std::max(1, key_bits), st));
-    tb = std::max(tb1, tb2);
+    tb = tbm;
     CKS(cub::DeviceRunLengthEncode::Encode(temp, tb, key_out, uniq, counts, d_runs, n, st));
     int64_t runs = 0;
     CKS(cudaMemcpyAsync(&runs, d_runs, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CKS(cudaStreamSynchronize(st));
-    std::vector<int32_t> h_counts((size_t)runs);
-    if (runs) CKS(cudaMemcpyAsync(h_counts.data(), counts, sizeof(int32_t) * runs, cudaMemcpyDeviceToHost, st));
+    const int grid = grid_for(std::max<int64_t>(runs, 1), c->sm_count);
+    tb = tbm;
+    CKS(cub::DeviceScan::ExclusiveSum(temp, tb, counts, starts, runs, st));
+    flag_multi<<<grid, PB, 0, st>>>(counts, d_runs, flag);
+    CKS(cudaGetLastError());
+    tb = tbm;
+    CKS(cub::DeviceSelect::Flagged(temp, tb, thrust::counting_iterator<int32_t>(0), flag, sel, d_sel, runs, st));
+    int64_t n_multi = 0;
+    CKS(cudaMemcpyAsync(&n_multi, d_sel, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CKS(cudaStreamSynchronize(st));
+    CKS(S.get(&groups, n_multi));
+    std::vector<longlong4> h_groups((size_t)n_multi);
+    if (n_multi) {
+        gather_groups<<<grid_for(n_multi, c->sm_count), PB, 0, st>>>(sel, d_sel, counts, starts, groups);
+        CKS(cudaGetLastError());
+        CKS(cudaMemcpyAsync(h_groups.data(), groups, sizeof(longlong4) * n_multi, cudaMemcpyDeviceToHost, st));
+    }
     int32_t* dst = P->d_refs + base;
     CKS(cudaMemcpyAsync(dst, tid_out, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
     CKS(cudaStreamSynchronize(st));
     std::vector<Deal> deals;
-    int64_t start = 0;
-    for (int64_t g = 0; g < runs; g++) {
-        const int64_t m = h_counts[(size_t)g];
+    int64_t extra = 0;  // sibling sub-partitions beyond one per group: pids of the single-tuple gaps follow
+    for (int64_t g = 0; g < n_multi; g++) {
+        const int64_t start = h_groups[(size_t)g].y, m = h_groups[(size_t)g].z;
         if (m <= maxp) {
             P->parts.push_back(Part{base + start, m, -1, 0});
             P->branch.push_back(branch);
@@ -234,6 +286,7 @@ int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, i
             const int64_t k = (m + maxp - 1) / maxp, q = m / k, r = m % k;
             deals.push_back(Deal{start, m, k});  // positions relative to the branch
             sibling_counter++;
+            extra += k - 1;
             std::vector<std::pair<int64_t, int64_t>> ranges;
             int64_t at = base + start;
             for (int64_t sub = 0; sub < k; sub++) {
@@ -246,9 +299,9 @@ int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, i
             }
             sib_ranges.push_back(std::move(ranges));
         }
-        start += m;
     }
     P->n_groups += runs;
+    P->n_partitions += runs + extra;
     if (!deals.empty()) {
         // the deal reads the sorted ids (tid_out) and rewrites the oversize groups of dst
         Deal* d_deals;
@@ -263,7 +316,7 @@ int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, i
 
 int finish_pulls(rb_parts* P, bool pulls, const std::vector<std::vector<std::pair<int64_t, int64_t>>>& sib_ranges,
                  const std::vector<int32_t>& sib_branch) {
-    P->n_partitions = (int64_t)P->parts.size();
+    P->n_kept = (int64_t)P->parts.size();
     if (!pulls) return RB_OK;
     int gid = 0;
     for (size_t g = 0; g < sib_ranges.size(); g++) {
@@ -320,6 +373,7 @@ int partition_impl(rb_ctx* c, rb_rel* rel, const int32_t* cols, const int64_t* k
         const int grid = grid_for(n, c->sm_count);
         for (int b = 0; b < nb && n > 0; b++) {
             const int32_t bid = branch_ids ? branch_ids[b] : b;
+            P->branch_ids.push_back(bid);
             int key_bits;
             if (cols) {
                 keys_from_codes<<<grid, PB, 0, st>>>(rel->cols[cols[b]].codes, n, key, tid);
@@ -364,48 +418,52 @@ int collect_impl(rb_ctx* c, const int32_t* t, const int32_t* s, const int32_t* r
     const int sb = std::max(1, bits_for((uint64_t)std::max<int64_t>(1, n_tuples - 1)));
     const int rb = bits_for((uint64_t)std::max(0, n_rules - 1));
     const int grid = grid_for(k, c->sm_count);
-    Scratch S(st);
-    uint64_t *k0, *k1;
-    uint8_t* flag;
-    int64_t* d_cnt;
-    CKS(S.get(&k0, k));
-    CKS(S.get(&k1, k));
-    CKS(S.get(&flag, k));
-    CKS(S.get(&d_cnt, 1));
+    // the context's collect scratch (grow-only)
+    CKS(c->col_k0.grow(sizeof(uint64_t) * k, st));
+    CKS(c->col_k1.grow(sizeof(uint64_t) * k, st));
+    CKS(c->col_flag.grow(k, st));
+    CKS(c->col_cnt.grow(sizeof(int64_t), st));
+    uint64_t* k0 = (uint64_t*)c->col_k0.p;
+    uint64_t* k1 = (uint64_t*)c->col_k1.p;
+    uint8_t* flag = (uint8_t*)c->col_flag.p;
+    int64_t* d_cnt = (int64_t*)c->col_cnt.p;
     if (2 * sb + rb <= 64) {
         pack_rows<<<grid, PB, 0, st>>>(t, s, r, k, sb, rb, k0);
         CKS(cudaGetLastError());
         size_t tb1 = 0, tb2 = 0;
         CKS(cub::DeviceRadixSort::SortKeys(nullptr, tb1, k0, k1, k, 0, 2 * sb + rb, st));
         CKS(cub::DeviceSelect::Flagged(nullptr, tb2, k1, flag, k0, d_cnt, k, st));
-        void* temp;
-        CKS(S.get((char**)&temp, std::max(tb1, tb2)));
-        size_t tb = std::max(tb1, tb2);
+        const size_t tbm = std::max(tb1, tb2);
+        CKS(c->col_temp.grow(tbm, st));
+        void* temp = c->col_temp.p;
+        size_t tb = tbm;
         CKS(cub::DeviceRadixSort::SortKeys(temp, tb, k0, k1, k, 0, 2 * sb + rb, st));
         flag_firsts<<<grid, PB, 0, st>>>(k1, k, rb, flag);
         CKS(cudaGetLastError());
-        tb = std::max(tb1, tb2);
+        tb = tbm;
         CKS(cub::DeviceSelect::Flagged(temp, tb, k1, flag, k0, d_cnt, k, st));
         unpack_rows<<<grid, PB, 0, st>>>(k0, d_cnt, sb, rb, ot, os, orr);
         CKS(cudaGetLastError());
     } else {
-        int32_t *r1, *r2;
-        CKS(S.get(&r1, k));
-        CKS(S.get(&r2, k));
+        CKS(c->col_r1.grow(sizeof(int32_t) * k, st));
+        CKS(c->col_r2.grow(sizeof(int32_t) * k, st));
+        int32_t* r1 = (int32_t*)c->col_r1.p;
+        int32_t* r2 = (int32_t*)c->col_r2.p;
         pack_ts<<<grid, PB, 0, st>>>(t, s, k, k0);
         CKS(cudaGetLastError());
         size_t tb1 = 0, tb2 = 0;
         CKS(cub::DeviceRadixSort::SortPairs(nullptr, tb1, k0, k1, r, r1, k, 0, 64, st));
         CKS(cub::DeviceSelect::Flagged(nullptr, tb2, k0, flag, k1, d_cnt, k, st));
-        void* temp;
-        CKS(S.get((char**)&temp, std::max(tb1, tb2)));
-        size_t tb = std::max(tb1, tb2);
+        const size_t tbm = std::max(tb1, tb2);
+        CKS(c->col_temp.grow(tbm, st));
+        void* temp = c->col_temp.p;
+        size_t tb = tbm;
         CKS(cub::DeviceRadixSort::SortPairs(temp, tb, k0, k1, r, r1, k, 0, 64, st));
         min_rule_runs<<<grid, PB, 0, st>>>(k1, r1, k, k0, r2, flag);
         CKS(cudaGetLastError());
-        tb = std::max(tb1, tb2);
+        tb = tbm;
         CKS(cub::DeviceSelect::Flagged(temp, tb, k0, flag, k1, d_cnt, k, st));
-        tb = std::max(tb1, tb2);
+        tb = tbm;
         CKS(cub::DeviceSelect::Flagged(temp, tb, r2, flag, r1, d_cnt, k, st));
         unpack_ts<<<grid, PB, 0, st>>>(k1, r1, d_cnt, ot, os, orr);
         CKS(cudaGetLastError());
@@ -454,15 +512,40 @@ int rb_parts_copy(const rb_parts* p, int32_t* refs, int64_t* base, int64_t* size
         CKS(cudaMemcpyAsync(refs, p->d_refs, sizeof(int32_t) * p->n_branches * p->n, cudaMemcpyDeviceToHost, c->stream));
         CKS(cudaStreamSynchronize(c->stream));
     }
-    for (size_t k = 0; k < p->parts.size(); k++) {
-        const Part& q = p->parts[k];
-        if (base) base[k] = q.base;
-        if (size) size[k] = q.n;
-        if (split) split[k] = q.split;
-        if (rbase) rbase[k] = q.split >= 0 ? q.rbase : -1;
-        if (branch) branch[k] = p->branch[k];
-        if (sibling) sibling[k] = p->sibling[k];
+    int64_t out = 0;
+    auto put = [&](int64_t b0, int64_t sz, int64_t sp, int64_t rb, int32_t br, int32_t sib) {
+        if (base) base[out] = b0;
+        if (size) size[out] = sz;
+        if (split) split[out] = sp;
+        if (rbase) rbase[out] = rb;
+        if (branch) branch[out] = br;
+        if (sibling) sibling[out] = sib;
+        out++;
+    };
+    // partitions in pid order: the kept ones, every uncovered position of a
+    // branch in between as a single-tuple partition
+    size_t k = 0;
+    for (int32_t b = 0; b < (int32_t)p->branch_ids.size(); b++) {
+        const int64_t lo = (int64_t)b * p->n, hi = lo + p->n;
+        int64_t at = lo;
+        while (true) {
+            const bool more = k < (size_t)p->n_kept && p->parts[k].base < hi;
+            const int64_t next = more ? p->parts[k].base : hi;
+            for (; at < next; at++) put(at, 1, -1, -1, p->branch_ids[(size_t)b], 0);
+            if (!more) break;
+            const Part& q = p->parts[k];
+            put(q.base, q.n, -1, -1, p->branch[k], p->sibling[k]);
+            at = q.base + q.n;
+            k++;
+        }
     }
+    for (; k < p->parts.size(); k++) {
+        const Part& q = p->parts[k];
+        put(q.base, q.n, q.split, q.split >= 0 ? q.rbase : -1, p->branch[k], p->sibling[k]);
+    }
+    if (out != p->n_partitions + p->n_pulls)
+        return fail(RB_ERR_INTERNAL, "rb_parts_copy: %lld entries for %lld partitions + %lld pulls", (long long)out,
+                    (long long)p->n_partitions, (long long)p->n_pulls);
     return RB_OK;
 }
 
@@ -526,32 +609,29 @@ int rb_result_collect(rb_result* res, int64_t n_tuples, int32_t n_rules) {
     CKS(cudaSetDevice(c->device));
     std::lock_guard<std::mutex> lock(c->mu);
     const int64_t k = res->count;
-    int32_t *t = nullptr, *s = nullptr, *r = nullptr;
-    cudaError_t e = dev_alloc((void**)&t, sizeof(int32_t) * k, c->stream);
-    if (!e) e = dev_alloc((void**)&s, sizeof(int32_t) * k, c->stream);
-    if (!e) e = dev_alloc((void**)&r, sizeof(int32_t) * k, c->stream);
-    if (e) {
-        dev_free(t, c->stream);
-        dev_free(s, c->stream);
-        dev_free(r, c->stream);
-        return fail(RB_ERR_OOM, "collect output of %lld rows: %s", (long long)k, cudaGetErrorString(e));
-    }
+    // the collected rows go to the context's spare row buffers, which then
+    // swap owners with the result's (no allocation per collect)
+    for (int q = 0; q < 3; q++)
+        if (cudaError_t e = c->col_out[q].grow(sizeof(int32_t) * k, c->stream))
+            return fail(RB_ERR_OOM, "collect output of %lld rows: %s", (long long)k, cudaGetErrorString(e));
+    int32_t* t = (int32_t*)c->col_out[0].p;
+    int32_t* s = (int32_t*)c->col_out[1].p;
+    int32_t* r = (int32_t*)c->col_out[2].p;
     int64_t kept = 0;
-    if (int rc = collect_impl(c, res->d_t, res->d_s, res->d_r, k, n_tuples, n_rules, t, s, r, &kept)) {
-        dev_free(t, c->stream);
-        dev_free(s, c->stream);
-        dev_free(r, c->stream);
-        return rc;
-    }
-    dev_free(res->d_t, c->stream);
-    dev_free(res->d_s, c->stream);
-    dev_free(res->d_r, c->stream);
-    dev_free(res->d_p, c->stream);
+    if (int rc = collect_impl(c, res->d_t, res->d_s, res->d_r, k, n_tuples, n_rules, t, s, r, &kept)) return rc;
+    int32_t* old[3] = {res->d_t, res->d_s, res->d_r};
+    const long long old_cap = res->cap;
     res->d_t = t;
     res->d_s = s;
     res->d_r = r;
+    res->cap = (long long)(std::min(std::min(c->col_out[0].bytes, c->col_out[1].bytes), c->col_out[2].bytes) /
+                           sizeof(int32_t));
+    for (int q = 0; q < 3; q++) {
+        c->col_out[q].p = old[q];
+        c->col_out[q].bytes = old[q] ? sizeof(int32_t) * (size_t)old_cap : 0;
+    }
+    dev_free(res->d_p, c->stream);
     res->d_p = nullptr;
-    res->cap = k;
     res->count = kept;
     return RB_OK;
 }

@@ -115,7 +115,11 @@ struct rb_ctx {
     bool own_stream = false;
     int sm_count = 0;
     int blocks_per_sm = 1;
+    size_t mem_total = 0;
     DevBuf items, refs, counters, scratch, surv, offs;
+    // collect (rb_pipeline.cu): sort keys, flags, CUB temp and the collected
+    // rows -- grown once and reused, so a step allocates nothing from the pool
+    DevBuf col_k0, col_k1, col_flag, col_temp, col_r1, col_r2, col_cnt, col_out[3];
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr;
     // output buffers of the last destroyed result, reused by the next run
     int32_t* pool[3] = {nullptr, nullptr, nullptr};

@@ -58,6 +58,9 @@ def run_rows_device(prog: PathProgram, refs, n: int, flags: int, row_lo: int, ro
             check(L.rb_result_device(res, _lib.ctypes.byref(pt), _lib.ctypes.byref(ps), _lib.ctypes.byref(pr), None))
             for col, p in enumerate((pt, ps, pr)):  # the run has completed (its count is on the host)
                 out[:, col].copy_(torch.as_tensor(_DevRows(p.value, k), device=dev))
+            # the copies ran on torch's stream: finish them before the library
+            # frees or reuses the result buffers on its own stream
+            torch.cuda.current_stream(dev).synchronize()
         st = _lib.RbStats()
         check(L.rb_result_stats(res, _lib.ctypes.byref(st)))
     finally:
@@ -73,6 +76,8 @@ def gather_rows(rows, group=None):
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
+    if rows.is_cuda and dist.get_backend(group) == "gloo":  # ranks sharing one GPU (functional runs)
+        return gather_rows(rows.cpu(), group).to(rows.device)
     cnt = torch.tensor([rows.shape[0]], dtype=torch.int64, device=rows.device)
     counts = torch.empty(world, dtype=torch.int64, device=rows.device)
     dist.all_gather_into_tensor(counts, cnt, group=group)
@@ -94,7 +99,7 @@ def run_partition_distributed(partition, relation, path, cfg: Optional[EngineCon
     with the same arguments; every rank returns the whole CandidateSet."""
     import torch.distributed as dist
 
-    cfg = cfg or EngineConfig()
+    cfg = EngineConfig.of(cfg)
     if partition is None or len(partition.tuple_refs) == 0:
         return CandidateSet(pairs=[])
     if not dist.is_initialized():
@@ -120,3 +125,41 @@ def run_partition_distributed(partition, relation, path, cfg: Optional[EngineCon
                      kernel_ms=float(st.kernel_ms), launches=int(st.launches), specialized=bool(st.specialized),
                      jit_log=prog.jit_log)
     return CandidateSet(stats=stats, arrays=(allrows[:, 0], allrows[:, 1], allrows[:, 2]), rule_ids=prog.rule_ids)
+
+
+def t_bounds(n_tuples: int, world: int) -> list:
+    """Rank r owns the rows whose t lies in [bounds[r], bounds[r+1])."""
+    return [(n_tuples * r) // world for r in range(world + 1)]
+
+
+def exchange_rows(rows, n_tuples: int, group=None):
+    """The exchange step of the multi-GPU collect: (t, s, rule) int32 rows,
+    sorted by t (a rank's collected rows), are re-distributed so that rank r
+    receives every rank's rows with t in its tuple-id range (``t_bounds``).
+    One all-to-all of the per-destination counts, one of the rows packed
+    (k, 3).  Returns this rank's received (t, s, rule), the senders' runs
+    back to back in rank order.  Works on CUDA tensors over NCCL and on CPU
+    tensors over gloo."""
+    import torch
+    import torch.distributed as dist
+
+    t, s, r = rows
+    world = dist.get_world_size(group)
+    if world == 1:
+        return t, s, r
+    if t.is_cuda and dist.get_backend(group) == "gloo":  # ranks sharing one GPU (functional runs)
+        got = exchange_rows((t.cpu(), s.cpu(), r.cpu()), n_tuples, group)
+        return tuple(x.to(t.device) for x in got)
+    dev = t.device
+    inner = torch.tensor(t_bounds(n_tuples, world)[1:-1], dtype=t.dtype, device=dev)
+    cuts = torch.searchsorted(t, inner)  # t is sorted: each destination is a contiguous run
+    edges = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), cuts.to(torch.int64),
+                       torch.tensor([t.shape[0]], dtype=torch.int64, device=dev)])
+    send = edges[1:] - edges[:-1]
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    send_h, recv_h = send.tolist(), recv.tolist()
+    packed = torch.stack([t, s, r], dim=1)
+    out = torch.empty((sum(recv_h), 3), dtype=t.dtype, device=dev)
+    dist.all_to_all_single(out, packed, output_split_sizes=recv_h, input_split_sizes=send_h, group=group)
+    return out[:, 0].contiguous(), out[:, 1].contiguous(), out[:, 2].contiguous()

@@ -62,6 +62,27 @@ MAX_CHECKPOINTS = 64
 NEVER = 1 << 30  # table value that no count reaches
 
 
+BUILTIN_SCORERS = {"edit": "edit_score", "jaccard": "jaccard_score", "exact_token": "exact_token_score"}
+
+
+def _require_builtin_scorer(reg, p) -> None:
+    """Where the reference scores a predicate through the registry
+    (_fallback_slot -> eval_predicate, encode.py:281-288, measures.py:145-174)
+    the device evaluates the built-in measure.  A registry that maps the
+    measure to anything else (a custom scorer, fold=False) would change
+    results, so it is refused instead of silently replaced."""
+    if reg is None or not hasattr(reg, "get"):
+        return
+    m = reg.get(p.measure)
+    scorer = getattr(m, "scorer", None)
+    name = getattr(scorer, "__name__", None)
+    module = getattr(scorer, "__module__", "") or ""
+    if name != BUILTIN_SCORERS.get(p.measure) or not module.endswith("measures") or not getattr(m, "fold", True):
+        raise ConfigError(f"measure {p.measure!r} is registered with a custom scorer ({module}.{name}, "
+                          f"fold={getattr(m, 'fold', True)}); {p.describe()} is scored through the registry by the "
+                          f"reference and has no device kernel for a custom scorer")
+
+
 @dataclass
 class Column:
     kind: int
@@ -206,9 +227,12 @@ class Encoded:
             a = self.get(("chars", p.lhs_attr))
             b = self.get(("chars", rhs))
             same_width = self.columns[a].width == self.columns[b].width
+            if not same_width:  # the reference's _fallback_slot: scored by the registry (encode.py:307-308)
+                _require_builtin_scorer(reg, p)
             return SLOT_EDIT, a, b, SLOT_FLAG_PREFILTER if same_width else 0
         kind = SLOT_JACCARD if p.measure == "jaccard" else SLOT_EXACT
         if p.is_cross_attr:
+            _require_builtin_scorer(reg, p)  # _fallback_slot (encode.py:310-317)
             a = self.get(("xtokens", p.lhs_attr, rhs, 0))
             b = self.get(("xtokens", p.lhs_attr, rhs, 1))
             return kind, a, b, 0

@@ -59,6 +59,19 @@ class EngineConfig:
         if self.buffer_half_capacity < 1 or self.chunk_size < 1:
             raise ConfigError("buffer_half_capacity and chunk_size must be >= 1")
 
+    @classmethod
+    def of(cls, cfg) -> "EngineConfig":
+        """This package's EngineConfig for ``cfg``: None -> defaults, ours as
+        is, any object with the reference's EngineConfig fields (engine.py:41-62,
+        e.g. the reference's own, passed by its pipeline or CLI) converted
+        field by field -- so the reference's call sites work unchanged."""
+        if cfg is None:
+            return cls()
+        if isinstance(cfg, cls):
+            return cfg
+        names = [f for f in cls.__dataclass_fields__ if f != "device_stats"]
+        return cls(**{f: getattr(cfg, f) for f in names if hasattr(cfg, f)})
+
     def resolved_blocks(self) -> int:
         return self.num_blocks if self.num_blocks else (os.cpu_count() or 1)
 
@@ -115,7 +128,7 @@ class CandidateSet:
     def __init__(self, pairs=None, stats: Optional[RunStats] = None, *, arrays=None, rule_ids=None):
         self.stats = stats if stats is not None else RunStats()
         self._pairs = list(pairs) if pairs is not None else None
-        self._arrays = arrays  # (t int64[k], s int64[k], rule_index int64[k])
+        self._arrays = arrays  # (t, s, rule_index) integer arrays of k rows (int64, or int32 as copied back)
         self._rule_ids = list(rule_ids) if rule_ids is not None else []
 
     @property
@@ -128,7 +141,7 @@ class CandidateSet:
 
     @property
     def arrays(self):
-        """(t, s, rule_index) int64 arrays."""
+        """(t, s, rule_index) integer arrays."""
         if self._arrays is None:
             idx = {rid: k for k, rid in enumerate(self._rule_ids)}
             p = self._pairs or []
@@ -403,6 +416,37 @@ class DeviceResult:
             check(lib().rb_result_copy(self.handle, ptr(t), ptr(s), ptr(r)))
         return t, s, r
 
+    def torch_rows(self):
+        """(t, s, rule) int32 torch tensors on the result's device: copies
+        that stay valid after close().  The copies run on torch's current
+        stream and are complete on return, so the library may free or reuse
+        its buffers (rb_result_destroy, next run) right after."""
+        import torch
+
+        dev = torch.device("cuda", self.ctx.device)
+        k = self.count
+        out = [torch.empty(k, dtype=torch.int32, device=dev) for _ in range(3)]
+        if k:
+            from .distributed import _DevRows
+
+            for o, p in zip(out, self.device_pointers()):  # the rows are final: rb_* returned after a sync
+                o.copy_(torch.as_tensor(_DevRows(p, k), device=dev))
+            torch.cuda.current_stream(dev).synchronize()
+        return tuple(out)
+
+    def torch_views(self):
+        """(t, s, rule) int32 torch tensors viewing the result's device
+        buffers (no copy): valid until close()."""
+        import torch
+
+        from .distributed import _DevRows
+
+        dev = torch.device("cuda", self.ctx.device)
+        k = self.count
+        if k == 0:
+            return tuple(torch.empty(0, dtype=torch.int32, device=dev) for _ in range(3))
+        return tuple(torch.as_tensor(_DevRows(p, k), device=dev) for p in self.device_pointers())
+
     def device_pointers(self):
         """(t, s, rule) device addresses, valid until close()."""
         pt, ps, pr = _lib.c_vp(), _lib.c_vp(), _lib.c_vp()
@@ -545,7 +589,7 @@ def _candidates(prog: PathProgram, rows, st, cfg: EngineConfig, n_outer: int, wa
 def run_partition(partition, relation, path, cfg=None, reg=None, encoded=None, program=None) -> CandidateSet:
     """All pairs of one partition (engine.py:619-646): symmetric i<j with
     t = the lower position, or every ordered i != j."""
-    cfg = cfg or EngineConfig()
+    cfg = EngineConfig.of(cfg)
     if partition is None or len(partition.tuple_refs) == 0:
         return CandidateSet(pairs=[])
     started = time.perf_counter()
@@ -589,7 +633,7 @@ def run_partition_rows(partition, relation, path, row_lo: int, row_hi: int, cfg=
     """The pairs of `partition` whose outer (t) position lies in [row_lo,
     row_hi): one shard of run_partition.  The union over a split of [0, n)
     equals run_partition exactly."""
-    cfg = cfg or EngineConfig()
+    cfg = EngineConfig.of(cfg)
     if partition is None or len(partition.tuple_refs) == 0:
         return CandidateSet(pairs=[])
     started = time.perf_counter()
@@ -638,7 +682,7 @@ def run_partitions(partitions, relation, path, cfg=None, reg=None, encoded=None,
     """run_partition over many partitions in ONE device launch (the
     pipeline's per-task loop, pipeline.py:177-209, batched).  Returns one
     CandidateSet per partition, each identical to run_partition's."""
-    cfg = cfg or EngineConfig()
+    cfg = EngineConfig.of(cfg)
     live = [p for p in partitions if p is not None and len(p.tuple_refs)]
     prog = _program_for(path, relation, reg, encoded, program)
     res = iter(_batch(prog, [(_refs_array(p), -1) for p in live], cfg)) if live else iter(())
@@ -648,7 +692,7 @@ def run_partitions(partitions, relation, path, cfg=None, reg=None, encoded=None,
 def run_crosses(pairs, relation, path, cfg=None, reg=None, encoded=None, program=None) -> list:
     """run_cross over many (left, right) partition pairs in one launch --
     e.g. the per-block record-linkage runs of BASELINE config 5."""
-    cfg = cfg or EngineConfig()
+    cfg = EngineConfig.of(cfg)
     prog = _program_for(path, relation, reg, encoded, program)
     blocks = []
     for left, right in pairs:
@@ -663,7 +707,7 @@ def run_crosses(pairs, relation, path, cfg=None, reg=None, encoded=None, program
 def run_cross(left, right, relation, path, cfg=None, reg=None, encoded=None, program=None) -> CandidateSet:
     """Every (t in left, s in right) pair, t always the left tuple
     (engine.py:649-681 with _bipartite_patch 684-719)."""
-    cfg = cfg or EngineConfig()
+    cfg = EngineConfig.of(cfg)
     started = time.perf_counter()
     prog = _program_for(path, relation, reg, encoded, program)
     lrefs = _refs_array(left)

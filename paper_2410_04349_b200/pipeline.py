@@ -352,25 +352,123 @@ def _cuda_devices(devices, pipe_cfg) -> list:
     return out
 
 
-def _device_stage(dev: int, enc, path, compiled, keys, code_cols, branch_ids, maxp: int, pulls: bool, cfg,
-                  rank: int, world: int, n_tuples: int, key_groups, timings: dict):
-    """One device: upload, partition, run its share, collect."""
-    from .engine import Context, DeviceRelation, PathProgram
+class ResidentPipeline:
+    """pipeline_run's device stages over a relation already resident on one
+    GPU (a ``PathProgram`` and its ``DeviceRelation``): partition, execute
+    this rank's LPT share of the units, collect; with ``world > 1`` the
+    collected rows are then exchanged by tuple-id range between the ranks
+    (``distributed.exchange_rows``, one NCCL all-to-all) and collected once
+    more, so rank r ends with the final candidate rows whose t lies in its
+    range -- the ranks' shards in rank order are the collected set.
 
-    ctx = Context(dev)
-    drel = DeviceRelation(ctx, enc)
-    prog = PathProgram(path, enc, compiled=compiled, drel=drel)
-    t0 = time.perf_counter()
-    parts = partition_on_device(prog, keys=keys, code_cols=code_cols, branch_ids=branch_ids, max_partition_size=maxp,
-                                pulls=pulls, key_groups=key_groups)
-    t1 = time.perf_counter()
-    res = prog.run_parts(parts, cfg.flags(), rank, world)
-    st = res.stats()
-    t2 = time.perf_counter()
-    res.collect(n_tuples, max(1, len(path.rule_ids)))
-    t3 = time.perf_counter()
-    timings.update(partition_s=t1 - t0, execute_s=t2 - t1, collect_s=t3 - t2)
-    return prog, parts, res, st
+    ``step()`` is one pass of the hot path (BASELINE config 4 (i)); every
+    stage is timed with CUDA events on the context's stream (the bench binds
+    the context to torch's current stream)."""
+
+    def __init__(self, prog, *, keys=None, code_cols=None, branch_ids, max_partition_size: int, pulls: bool,
+                 flags: int, key_groups=None):
+        self.prog = prog
+        self.keys = keys
+        self.code_cols = code_cols
+        self.branch_ids = list(branch_ids)
+        self.maxp = int(max_partition_size)
+        self.pulls = bool(pulls)
+        self.flags = int(flags)
+        self.key_groups = key_groups
+        self.n_tuples = prog.enc.n
+        self.n_rules = max(1, len(prog.rule_ids))
+        self.res = None  # the last single-rank step's DeviceResult (its rows are views)
+        self.parts = None
+
+    def close(self) -> None:
+        if self.res is not None:
+            self.res.close()
+            self.res = None
+        if self.parts is not None:
+            self.parts.close()
+            self.parts = None
+
+    def step(self, rank: int = 0, world: int = 1, group=None, events: bool = False, keep_parts: bool = False):
+        """-> (rows, stats, stage_ms).  ``rows``: (t, s, rule) int32 device
+        tensors of this rank's collected shard (at world 1: views of the
+        result buffers, valid until the next step() or close()); the rows
+        are exchanged between the ranks only when ``group`` is given (one
+        process per GPU); without it the caller merges the ranks' rows
+        (several devices driven from one process); ``stats``: the run's rb_stats
+        (this rank's units); ``stage_ms``: partition / execute / collect /
+        exchange milliseconds (CUDA events when ``events``, else host clock
+        around the stage; every stage ends on a host sync).  ``keep_parts``:
+        the partition set stays alive as ``self.parts`` (DeviceParts)."""
+        import torch
+
+        dev = torch.device("cuda", self.prog.ctx.device)
+        marks = []
+
+        def mark():
+            if events:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(torch.cuda.current_stream(dev))
+                marks.append(e)
+            else:
+                marks.append(time.perf_counter())
+
+        mark()
+        parts = partition_on_device(self.prog, keys=self.keys, code_cols=self.code_cols, branch_ids=self.branch_ids,
+                                    max_partition_size=self.maxp, pulls=self.pulls, key_groups=self.key_groups)
+        mark()
+        res = self.prog.run_parts(parts, self.flags, rank, world)
+        st = res.stats()
+        if self.parts is not None:
+            self.parts.close()
+            self.parts = None
+        if keep_parts:
+            self.parts = parts
+        else:
+            parts.close()
+        mark()
+        res.collect(self.n_tuples, self.n_rules)
+        if self.res is not None:
+            self.res.close()
+        self.res = None
+        exchange = group is not None and world > 1
+        rows = res.torch_views()
+        if not exchange:  # the rows stay in the result's buffers: views, valid until the next step / close()
+            self.res = res
+        mark()
+        if exchange:
+            from .distributed import exchange_rows
+
+            rows = exchange_rows(rows, self.n_tuples, group)  # packed copies of the views
+            torch.cuda.current_stream(dev).synchronize()  # before the library frees the viewed buffers
+            res.close()
+            rows = collect_device_rows(rows, self.n_tuples, self.n_rules, self.prog.ctx)
+        mark()
+        if events:
+            torch.cuda.current_stream(dev).synchronize()
+            ms = [marks[k].elapsed_time(marks[k + 1]) for k in range(len(marks) - 1)]
+        else:
+            ms = [1e3 * (marks[k + 1] - marks[k]) for k in range(len(marks) - 1)]
+        stage_ms = dict(zip(("partition", "execute", "collect", "exchange"), ms))
+        return rows, st, stage_ms
+
+
+def collect_device_rows(rows, n_tuples: int, n_rules: int, ctx):
+    """rb_collect_device over (t, s, rule) int32 device tensors -> new
+    tensors (sorted by (t, s), smallest rule per (t, s))."""
+    import torch
+
+    from . import _lib
+
+    k = int(rows[0].shape[0])
+    dev = rows[0].device
+    out = [torch.empty(max(1, k), dtype=torch.int32, device=dev) for _ in range(3)]
+    if k == 0:
+        return tuple(x[:0] for x in out)
+    torch.cuda.current_stream(dev).synchronize()  # the inputs precede the library's stream
+    cnt = _lib.ctypes.c_int64(0)
+    _lib.check(_lib.lib().rb_collect_device(ctx.handle, *[_lib.c_vp(x.data_ptr()) for x in rows], k, n_tuples,
+                                            n_rules, *[_lib.c_vp(x.data_ptr()) for x in out], _lib.ctypes.byref(cnt)))
+    return tuple(x[: cnt.value] for x in out)
 
 
 def _merge_runs(runs: list, n_tuples: int, n_rules: int, device: int):
@@ -388,28 +486,71 @@ def _merge_runs(runs: list, n_tuples: int, n_rules: int, device: int):
         return tuple(np.zeros(0, np.int32) for _ in range(3))
     dev = torch.device("cuda", device)
     cols = [torch.from_numpy(np.concatenate([r[c] for r in runs])).to(dev) for c in range(3)]
-    out = [torch.empty(total, dtype=torch.int32, device=dev) for _ in range(3)]
-    ctx = context(device)
-    torch.cuda.current_stream(dev).synchronize()  # the uploads precede the library's stream
-    cnt = _lib.ctypes.c_int64(0)
-    _lib.check(_lib.lib().rb_collect_device(ctx.handle, *[_lib.c_vp(x.data_ptr()) for x in cols], total, n_tuples,
-                                            n_rules, *[_lib.c_vp(x.data_ptr()) for x in out], _lib.ctypes.byref(cnt)))
-    return tuple(x[: cnt.value].cpu().numpy() for x in out)
+    out = collect_device_rows(cols, n_tuples, n_rules, context(device))
+    return tuple(x.cpu().numpy() for x in out)
+
+
+def _device_stage(dev: int, enc, path, compiled, keys, code_cols, branch_ids, maxp: int, pulls: bool, cfg,
+                  rank: int, world: int, key_groups, timings: dict, group=None, out=None):
+    """One device: upload, then ResidentPipeline.step (partition, this
+    rank's share, collect; exchange when ``group`` spans several ranks).
+    Returns (host rows of the rank, rb_stats, DeviceParts)."""
+    from .engine import DeviceRelation, PathProgram, context
+
+    t0 = time.perf_counter()
+    ctx = context(dev)
+    drel = DeviceRelation(ctx, enc)
+    prog = PathProgram(path, enc, compiled=compiled, drel=drel)
+    t1 = time.perf_counter()
+    rp = ResidentPipeline(prog, keys=keys, code_cols=code_cols, branch_ids=branch_ids, max_partition_size=maxp,
+                          pulls=pulls, flags=cfg.flags(), key_groups=key_groups)
+    rows, st, ms = rp.step(rank, world, group, keep_parts=True)
+    t2 = time.perf_counter()
+    k = int(rows[0].shape[0])
+    if out is not None and all(len(a) >= k and a.dtype == np.int32 and a.flags["C_CONTIGUOUS"] for a in out):
+        import torch
+
+        host = tuple(a[:k] for a in out)  # caller's (pinned) host buffers: D2H at link speed
+        for h, x in zip(host, rows):
+            if k:
+                torch.from_numpy(h).copy_(x)
+    else:
+        host = tuple(x.cpu().numpy() for x in rows)
+    if rp.res is not None:  # the rows were views of it
+        rp.res.close()
+        rp.res = None
+    t3 = time.perf_counter()
+    prog.close()
+    drel.close()
+    timings.update(upload_s=t1 - t0, partition_s=ms["partition"] / 1e3, execute_s=ms["execute"] / 1e3,
+                   collect_s=ms["collect"] / 1e3, exchange_s=ms["exchange"] / 1e3, d2h_s=t3 - t2)
+    return host, st, rp.parts
 
 
 def run_pipeline_encoded(enc, path, pipe_cfg: Optional[PipelineConfig] = None,
                          engine_cfg: Optional[EngineConfig] = None, *, keys=None, code_cols=None, branch_ids=None,
-                         devices=None, reg=None, key_groups=None) -> PipelineResult:
+                         devices=None, reg=None, key_groups=None, group=None, compiled=None,
+                         out=None) -> PipelineResult:
     """The device pipeline over an encoded relation: partition (``keys``
-    int64 (branches, n) or eq-root ``code_cols``), execute on every device
-    in ``devices`` (LPT share of the units each), collect."""
+    int64 (branches, n) or eq-root ``code_cols``), execute, collect.
+
+    * ``group`` None: every device in ``devices`` runs its LPT share of the
+      units from a host thread of this process; the rows are merged and
+      collected once more on the first device.
+    * ``group`` a torch.distributed process group (one process per GPU, this
+      process on ``torch.cuda.current_device()``): this rank runs its share,
+      the rows are exchanged by tuple-id range over the group (NCCL
+      all-to-all) and collected; the result holds this rank's shard (t in
+      ``distributed.t_bounds(n, world)[rank:rank + 2]``).  Collective.
+    ``out``: optional (t, s, rule) int32 host arrays (e.g. pinned) the rows
+    are copied into when they fit (one device only)."""
     from .encode import compile_program
 
     pipe_cfg = pipe_cfg or PipelineConfig()
     engine_cfg = engine_cfg or EngineConfig(num_blocks=1)
-    devs = _cuda_devices(devices, pipe_cfg)
     n = enc.n
-    compiled = compile_program(path, enc, reg)
+    if compiled is None:
+        compiled = compile_program(path, enc, reg)
     threshold = pipe_cfg.single_partition_threshold
     if threshold is None:
         threshold = pipe_cfg.max_partition_size
@@ -419,17 +560,30 @@ def run_pipeline_encoded(enc, path, pipe_cfg: Optional[PipelineConfig] = None,
         maxp = max(1, n)
     if branch_ids is None:
         branch_ids = branch_order(path)
+    n_rules = max(1, len(path.rule_ids))
     wall0 = time.perf_counter()
+    if group is not None:
+        import torch
+        import torch.distributed as dist
+
+        devs = [torch.cuda.current_device()]
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+    else:
+        devs = _cuda_devices(devices, pipe_cfg)
+        rank, world = 0, len(devs)
     per_dev: list = [None] * len(devs)
     errors: list = []
 
     def work(k: int):
         try:
             tm: dict = {}
-            out = _device_stage(devs[k], enc, path, compiled, keys, code_cols, branch_ids, maxp,
-                                pipe_cfg.enable_pulls, engine_cfg, k, len(devs), n, key_groups, tm)
-            rows = out[2].copy()
-            per_dev[k] = (out, rows, tm)
+            rows, st, parts = _device_stage(devs[k], enc, path, compiled, keys, code_cols, branch_ids, maxp,
+                                            pipe_cfg.enable_pulls, engine_cfg, rank + k, world, key_groups, tm, group,
+                                            out if len(devs) == 1 else None)
+            if k:
+                parts.close()
+                parts = None
+            per_dev[k] = (rows, st, tm, parts)
         except BaseException as exc:  # surfaced below
             errors.append(exc)
 
@@ -444,28 +598,30 @@ def run_pipeline_encoded(enc, path, pipe_cfg: Optional[PipelineConfig] = None,
     if errors:
         raise errors[0]
     t0 = time.perf_counter()
-    t, s, r = _merge_runs([x[1] for x in per_dev], n, max(1, len(path.rule_ids)), devs[0])
+    if group is None:
+        t, s, r = _merge_runs([x[0] for x in per_dev], n, n_rules, devs[0])
+    else:
+        t, s, r = per_dev[0][0]
     merge_s = time.perf_counter() - t0
-    timings = {k: max(x[2][k] for x in per_dev) for k in ("partition_s", "execute_s", "collect_s")}
+    keys_t = ("upload_s", "partition_s", "execute_s", "collect_s", "exchange_s", "d2h_s")
+    timings = {k: max(x[2][k] for x in per_dev) for k in keys_t}
     timings["collect_s"] += merge_s
     timings["total_s"] = time.perf_counter() - wall0
-    stats = [x[0][3] for x in per_dev]
+    stats = [x[1] for x in per_dev]
     from .engine import BlockStats
 
-    blocks = [BlockStats(block_id=k, comparisons=int(st.comparisons), survivors=int(st.survivors),
+    blocks = [BlockStats(block_id=rank + k, comparisons=int(st.comparisons), survivors=int(st.survivors),
                          emitted=int(st.emitted), busy_s=st.kernel_ms / 1e3,
                          slot_evals=np.array(st.slot_evals[: len(path.predicate_table)], dtype=np.int64))
               for k, st in enumerate(stats)]
-    cand = CandidateSet(arrays=(t.astype(np.int64), s.astype(np.int64), r.astype(np.int64)),
+    cand = CandidateSet(arrays=(t, s, r),  # int32 as copied back (no host widening pass)
                         rule_ids=list(path.rule_ids),
                         stats=RunStats(blocks=blocks, wall_s=timings["total_s"],
                                        kernel_ms=sum(st.kernel_ms for st in stats),
                                        launches=sum(int(st.launches) for st in stats)))
-    parts = per_dev[0][0][1]
-    for x in per_dev[1:]:
-        x[0][2].close()
+    parts = per_dev[0][3]
     return PipelineResult(candidates=cand, timings=timings, assignment={}, n_partitions=int(parts.n_partitions),
-                          device_busy_s={devs[k]: per_dev[k][0][3].kernel_ms / 1e3 for k in range(len(devs))},
+                          device_busy_s={devs[k]: per_dev[k][1].kernel_ms / 1e3 for k in range(len(devs))},
                           plan=None, parts=parts)
 
 

@@ -154,7 +154,7 @@ class MultiDeviceEngine:
         """blocks: [(refs, split)] with split = -1 for a partition, else the
         size of the left side of a cross block.  Returns a CandidateSet per
         block."""
-        cfg = cfg or EngineConfig()
+        cfg = EngineConfig.of(cfg)
         units = make_units(blocks, cfg.symmetric_mode, self.batch_pairs, self.shard_pairs)
         queues = StealingQueues(units, len(self.devices))
         results: dict = {}

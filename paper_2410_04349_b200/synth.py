@@ -53,6 +53,7 @@ class Workload:
     path: object
     n: int
     blocks: object = None  # [(refs int32, split)]: cross blocks / partitions instead of one partition
+    injected: object = None  # (a, b) int arrays: the generator's duplicate pairs (recall checks)
 
     def pairs(self, symmetric: bool = True) -> int:
         if self.blocks is None:
@@ -145,7 +146,7 @@ def citation3(n: int = 1_000_000, seed: int = 2024, plan_sample: int = 200_000) 
 
     rules = parse_ruleset(json.dumps(CITATION3_RULES))
     path = data_aware_plan(enc, rules, sample=plan_sample, seed=seed)
-    return Workload("citation3", enc, rules, path, n)
+    return Workload("citation3", enc, rules, path, n, injected=(a, b))
 
 
 def sampled_selectivity(enc: Encoded, predicates, sample: int, seed: int) -> dict:
@@ -227,7 +228,7 @@ def _perturb(rng, base: bytes, k: int) -> bytes:
 
 
 def _chars_column(strs: list) -> Column:
-    lens = np.fromiter((len(x) for x in strs), dtype=np.int64, count=len(strs))
+    lens = np.fromiter(map(len, strs), dtype=np.int64, count=len(strs))
     off = np.zeros(len(strs) + 1, dtype=np.int64)
     np.cumsum(lens, out=off[1:])
     data = np.frombuffer(b"".join(strs), dtype=np.uint8).copy()
@@ -246,14 +247,16 @@ def edit_heavy(n: int = 1_000_000, seed: int = 11, plan_sample: int = 200_000) -
     zipf_p = 1.0 / np.arange(1, 100_001) ** 1.1
     zip_draws = nrng.choice(100_000, size=2 * n, p=zipf_p / zipf_p.sum()).astype(np.int32).tolist()
     zd = 0
-    texts, names, zips = [], [], []
+    texts, names, zips, gid = [], [], [], []
     while len(texts) < n:
         g = rng.randint(2, 50)
         base = bytes(ALPHA[rng.randrange(27)] for _ in range(rng.randint(64, 256)))
         nb = f"{rng.choice(FIRST)} {rng.choice(LAST)}".encode()
         z = zip_draws[zd]
         zd += 1
+        g_id = len(texts)  # the group's first position: a unique group id
         for _ in range(min(g, n - len(texts))):
+            gid.append(g_id)
             texts.append(_perturb(rng, base, rng.randint(0, 3)))
             names.append(nb if rng.random() < 0.8 else _perturb(rng, nb, 1))
             if rng.random() < 0.9:
@@ -262,6 +265,11 @@ def edit_heavy(n: int = 1_000_000, seed: int = 11, plan_sample: int = 200_000) -
                 zips.append(zip_draws[zd])
                 zd += 1
     order = nrng.permutation(n)
+    gid = np.asarray(gid, dtype=np.int64)
+    inv = np.empty(n, dtype=np.int64)
+    inv[order] = np.arange(n)
+    same = np.flatnonzero(gid[1:] == gid[:-1])  # consecutive members of one near-duplicate group
+    injected = (inv[same], inv[same + 1])
     texts = [texts[k] for k in order]
     names = [names[k] for k in order]
     zips = np.asarray(zips, dtype=np.int32)[order]
@@ -273,7 +281,7 @@ def edit_heavy(n: int = 1_000_000, seed: int = 11, plan_sample: int = 200_000) -
 
     rules = parse_ruleset(json.dumps(EDIT_HEAVY_RULES))
     path = data_aware_plan(enc, rules, sample=plan_sample, seed=seed)
-    return Workload("edit_heavy", enc, rules, path, n)
+    return Workload("edit_heavy", enc, rules, path, n, injected=injected)
 
 
 SYL = ["ka", "ri", "mo", "ta", "le", "sa", "no", "vi", "de", "ru", "mi", "ko", "na", "el", "an", "to", "be", "ga",
@@ -345,7 +353,7 @@ def linkage(n: int = 1_000_000, seed: int = 5, zipf_s: float = 1.3, n_blocks: in
 
     rules = parse_ruleset(json.dumps(LINKAGE_RULES))
     path = data_aware_plan(enc, rules, sample=plan_sample, seed=seed)
-    return Workload("linkage", enc, rules, path, n, blocks=blocks)
+    return Workload("linkage", enc, rules, path, n, blocks=blocks, injected=(src, dup))
 
 
 PERSON5_RULES = [
@@ -407,13 +415,32 @@ def person5(n: int = 10_000_000, seed: int = 4, plan_sample: int = 100_000) -> W
             k //= S
         return "".join(out).encode()
 
-    firsts = [name_of(int(k), 3) for k in first_id]
-    lasts = [name_of(int(k) * 7919 + 13, 4) for k in last_id]
-    for j in dup[rng.random(len(dup)) < 0.5]:
+    # names from per-id tables (each distinct id spelled once), then the
+    # perturbed first names; codes = rank among the sorted distinct strings
+    # (np.unique's inverse), computed per table entry
+    def spelled(ids, parts, mul=1, add=0):
+        uniq, inv = np.unique(ids, return_inverse=True)
+        table = np.array([name_of(int(k) * mul + add, parts) for k in uniq], dtype=object)
+        return table, inv
+
+    f_table, f_inv = spelled(first_id, 3)
+    l_table, l_inv = spelled(last_id, 4, 7919, 13)
+    firsts = f_table[f_inv].tolist()
+    lasts = l_table[l_inv].tolist()
+    pert = dup[rng.random(len(dup)) < 0.5]
+    for j in pert:
         firsts[j] = _perturb(prng, firsts[j], 1)
-    # equality codes of the same attribute values the edit predicates read
-    first_codes = np.unique(np.array(firsts, dtype=object), return_inverse=True)[1].astype(np.int32)
-    last_codes = np.unique(np.array(lasts, dtype=object), return_inverse=True)[1].astype(np.int32)
+
+    def codes_of(table, inv, extra_idx, strs):
+        distinct = sorted(set(table.tolist()) | {strs[j] for j in extra_idx})
+        rank = {x: i for i, x in enumerate(distinct)}
+        codes = np.array([rank[x] for x in table.tolist()], dtype=np.int32)[inv]
+        for j in extra_idx:
+            codes[j] = rank[strs[j]]
+        return codes
+
+    first_codes = codes_of(f_table, f_inv, pert, firsts)
+    last_codes = codes_of(l_table, l_inv, [], lasts)
     t_off, t_ids = _csr_from_padded(addr, n_tok, sort_rows=True)
     enc = Encoded(n)
     enc.add(("codes", "zip"), Column(COL_CODES, zipc))
@@ -428,7 +455,7 @@ def person5(n: int = 10_000_000, seed: int = 4, plan_sample: int = 100_000) -> W
 
     rules = parse_ruleset(json.dumps(PERSON5_RULES))
     path = data_aware_plan(enc, rules, sample=plan_sample, seed=seed)
-    return Workload("person5", enc, rules, path, n)
+    return Workload("person5", enc, rules, path, n, injected=(src, dup))
 
 
 def citation3_parts(n: int = 1_000_000, seed: int = 2024, part: int = 512) -> Workload:

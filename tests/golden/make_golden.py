@@ -304,7 +304,12 @@ def pipelines(tmp):
 
 
 def main():
-    seeds = range(int(os.environ.get("RB_GOLDEN_SEEDS", "60")))
+    # the suite_oracle rotation covers seeds 0..99 (bench.py:77-119)
+    seeds = range(int(os.environ.get("RB_GOLDEN_SEED_LO", "0")), int(os.environ.get("RB_GOLDEN_SEEDS", "100")))
+    if os.environ.get("RB_GOLDEN_ONLY") == "randoms":
+        with tempfile.TemporaryDirectory() as tmp:
+            randoms(tmp, seeds)
+        return
     if os.environ.get("RB_GOLDEN_ONLY") == "pipelines":
         with tempfile.TemporaryDirectory() as tmp:
             pipelines(tmp)

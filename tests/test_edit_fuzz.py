@@ -82,3 +82,51 @@ def test_fuzz_relation_has_matches():
     case = {"symmetric": True, "enumerate": True, "refs": None, "left": None, "right": None}
     want, _ = goldens.oracle_rows(rel, path, case)
     assert len(want) > 50
+
+
+def make_long(seed, n=70):
+    """Long strings with low thresholds: maxd[L] far above 31, so the
+    device runs Myers' bit-vector algorithm (and its fallbacks: patterns
+    over 1024 characters or with more than 48 distinct characters)."""
+    rng = random.Random(seed)
+    alpha = ["abcdefghij ", "abcdefghijklmnopqrstuvwxyz ", "abcdefghijklmnopqrstuvwxyzABCDEFGHIJKLMNOPQRSTUVWXYZ0123456789",
+             "abcdeéßΩжйк "][seed % 4]
+    rows = []
+    while len(rows) < n:
+        L = rng.choice([40, 150, 300, 700, 1100]) + rng.randint(0, 40)
+        base = "".join(rng.choice(alpha) for _ in range(L))
+        for _ in range(rng.randint(1, 6)):
+            rows.append([_perturb(rng, base, rng.choice([0, 3, 30, 120, 400]), alpha)])
+    rel = relation_from_rows(["s"], ["long_text"], rows[:n])
+    doc = [{"id": f"e{k}", "when": [{"t_attr": "s", "op": "sim", "s_attr": "s", "measure": "edit", "threshold": th}]}
+           for k, th in enumerate(rng.sample([0.3, 0.45, 0.55, 0.7, 0.8, 0.9], 3))]
+    rules = parse_ruleset(json.dumps(doc))
+    uni = predicate_universe(rules)
+    return rel, plan_from_stats(rules, {p: 1.0 for p in uni}, {p: 0.5 for p in uni})
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(8))
+def test_long_strings_large_bounds_gpu_vs_oracle(seed):
+    rel, path = make_long(seed)
+    refs = list(range(len(rel)))
+    for sym in (True, False):
+        cfg = EngineConfig(symmetric_mode=sym, enumerate_witnesses=True)
+        cs = run_partition(DataPartition(0, tuple(refs)), rel, path, cfg)
+        case = {"symmetric": sym, "enumerate": True, "refs": None, "left": None, "right": None}
+        want, cmp = goldens.oracle_rows(rel, path, case)
+        assert sorted(cs.pairs) == want
+        assert cs.stats.total_comparisons() == cmp
+
+
+def test_long_fuzz_has_large_bounds_and_matches():
+    from paper_2410_04349_b200.encode import RelationEncoding, compile_program
+
+    for seed in range(4):
+        rel, path = make_long(seed)
+        case = {"symmetric": True, "enumerate": True, "refs": None, "left": None, "right": None}
+        want, _ = goldens.oracle_rows(rel, path, case)
+        assert len(want) > 0
+        enc = RelationEncoding(rel).prepare(path.predicate_table)
+        prog = compile_program(path, enc)
+        assert prog.tables.max() > 300  # some maxd[L] far above the diagonal algorithm's 31

@@ -209,3 +209,63 @@ def test_encoding_accepts_reference_objects_and_matches_encoded_relation():
                 cc = ours.columns[ours.get(("chars", attr))]
                 assert np.array_equal(ch.offsets, cc.offsets) and np.array_equal(ch.flat, cc.data)
                 assert ch.flat.dtype == cc.data.dtype
+
+
+class _Measure:
+    def __init__(self, scorer, fold=True):
+        self.scorer, self.fold = scorer, fold
+
+
+class _Registry:
+    def __init__(self, **entries):
+        self.entries = entries
+
+    def get(self, mid):
+        if mid not in self.entries:
+            raise ConfigError(f"unregistered measure {mid!r}")
+        return self.entries[mid]
+
+
+def _builtin(name):
+    def f(a, b, fold=True):
+        return 0.0
+    f.__name__, f.__module__ = name, "ruleblock.measures"
+    return f
+
+
+def test_registry_scored_slots_refuse_custom_scorers():
+    """The reference scores cross-attribute jaccard / exact_token and
+    mixed-width edit through the registry (encode.py:281-324 ->
+    measures.py:145-174): a custom scorer there raises ConfigError instead
+    of being replaced by the built-in device measure."""
+    rel, path, _ = goldens.load("edge_cross_attr")
+    builtin = _Registry(edit=_Measure(_builtin("edit_score")), jaccard=_Measure(_builtin("jaccard_score")),
+                        exact_token=_Measure(_builtin("exact_token_score")))
+    enc = RelationEncoding(rel).prepare(path.predicate_table)
+    compile_program(path, enc, builtin)  # built-in scorers: accepted
+    for mid in ("jaccard", "exact_token"):
+        custom = dict(builtin.entries)
+        custom[mid] = _Measure(lambda a, b, fold=True: 1.0)
+        with pytest.raises(ConfigError, match="custom scorer"):
+            compile_program(path, RelationEncoding(rel).prepare(path.predicate_table), _Registry(**custom))
+        custom[mid] = _Measure(_builtin(f"{mid}_score"), fold=False)
+        with pytest.raises(ConfigError, match="custom scorer"):
+            compile_program(path, RelationEncoding(rel).prepare(path.predicate_table), _Registry(**custom))
+    # a same-attribute jaccard slot never consults the scorer (the reference's _jaccard_slot)
+    rel2, path2, _ = goldens.load("products")
+    custom = dict(builtin.entries, jaccard=_Measure(lambda a, b, fold=True: 1.0),
+                  edit=_Measure(lambda a, b, fold=True: 1.0))
+    compile_program(path2, RelationEncoding(rel2).prepare(path2.predicate_table), _Registry(**custom))
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="reference package not present")
+def test_reference_default_registry_is_builtin():
+    sys.path.insert(0, REF)
+    from ruleblock.measures import Measure, default_registry
+
+    rel, path, _ = goldens.load("edge_cross_attr")
+    reg = default_registry()
+    compile_program(path, RelationEncoding(rel).prepare(path.predicate_table), reg)
+    reg.register(Measure("jaccard", lambda a, b, fold=True: 1.0))
+    with pytest.raises(ConfigError):
+        compile_program(path, RelationEncoding(rel).prepare(path.predicate_table), reg)
