@@ -59,6 +59,11 @@ extern "C" {
 #define RB_SYMMETRIC 1u
 #define RB_ENUMERATE 2u
 #define RB_STATS 4u /* count per-slot exact evaluations */
+/* slot_evals = first-touch evaluations of every slot over EVERY pair of the
+ * run under evaluate_pair semantics (engine.py:93-132, 122-128; the counts
+ * SURVEY 8d's E_s names), from a separate exact pass over all pairs -- not
+ * only the survivors of the pair filter.  Slower: opt-in. */
+#define RB_EXACT_STATS 8u
 
 #define RB_MAX_SLOTS 64
 #define RB_MAX_CHECKPOINTS 64

@@ -22,7 +22,7 @@ HEADERS = [HEADER, os.path.join(os.path.dirname(HERE), "include", "rbencode.h")]
 
 RB_OK = 0
 RB_ERR_INVALID, RB_ERR_CUDA, RB_ERR_OOM, RB_ERR_LIMIT, RB_ERR_INTERNAL = -1, -2, -3, -4, -5
-RB_SYMMETRIC, RB_ENUMERATE, RB_STATS = 1, 2, 4
+RB_SYMMETRIC, RB_ENUMERATE, RB_STATS, RB_EXACT_STATS = 1, 2, 4, 8
 RB_PART_PULLS, RB_PART_KEYS_DEVICE = 1, 2
 MAX_SLOTS = 64
 

@@ -793,6 +793,36 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
     P->V.n_slots = n_slots;
     if ((e = cudaStreamSynchronize(c->stream))) return bail(e);
     P->jit = jit_pair_kernel(P->F, c->device);
+    {  // the program's shape key, and what earlier programs of this shape learned
+        uint64_t h = 1469598103934665603ull;
+        auto mix = [&](const void* p, size_t bytes) {
+            const unsigned char* b = (const unsigned char*)p;
+            for (size_t k = 0; k < bytes; k++) h = (h ^ b[k]) * 1099511628211ull;
+        };
+        mix(op, sizeof(int32_t) * n_ins);
+        mix(slot, sizeof(int32_t) * n_ins);
+        mix(failj, sizeof(int32_t) * n_ins);
+        mix(rule, sizeof(int32_t) * n_ins);
+        mix(slots, sizeof(rb_slot) * n_slots);
+        if (n_tables) mix(tables, sizeof(int32_t) * n_tables);
+        mix(&rel->n, sizeof rel->n);
+        for (size_t k = 0; k < rel->cols.size(); k++) {
+            mix(&rel->cols[k].kind, sizeof rel->cols[k].kind);
+            mix(&rel->max_len[k], sizeof rel->max_len[k]);
+        }
+        P->shape_key = h;
+        std::lock_guard<std::mutex> lock(c->mu);
+        auto it = c->learned.find(h);
+        if (it != c->learned.end()) {
+            const Learned& L = it->second;
+            P->gate_off = L.gate_off;
+            P->last_rows = L.last_rows;
+            P->last_surv = L.last_surv;
+            P->surv_rate = L.surv_rate;
+            P->last_ranges = L.last_ranges;
+            P->last_n_items = L.last_n_items;
+        }
+    }
     *out = P;
     return RB_OK;
 }
@@ -824,8 +854,79 @@ static double host_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+namespace {
+int edit_stride(const rb_prog* P) {
+    if (P->lmax_edit < 0) return 0;
+    // a slice holds the banded DP row, or Myers' pattern table for bounds
+    // above 31 (rb_device.cuh lev_myers: 2 x MYERS_HS slots + MYERS_DCAP x W
+    // 64-bit masks, W = ceil(min(L, MYERS_NMAX) / 64))
+    int64_t need = P->lmax_edit + 2;
+    if (P->lmax_edit > 31) need = std::max<int64_t>(need, 2 * 64 + 2 * 48 * ((std::min<int64_t>(P->lmax_edit, 1024) + 63) / 64));
+    return (int)((need + 31) & ~(int64_t)31);
+}
+
+int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
+             int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device);
+
+// RB_EXACT_STATS: after the run, one pass of the exact interpreter over
+// every pair of its parts counts each slot's first touches; they replace
+// the run's survivor-only counts.
+int exact_stats(rb_ctx* c, rb_prog* P, const int32_t* d_refs, const std::vector<Part>& parts, int64_t row_lo,
+                int64_t row_hi, uint32_t flags, int64_t* slot_evals) {
+    std::lock_guard<std::mutex> lock(c->mu);
+    cudaStream_t st = c->stream;
+    std::vector<StatPart> sp(parts.size());
+    for (size_t k = 0; k < parts.size(); k++) sp[k] = StatPart{parts[k].base, parts[k].n, parts[k].split, parts[k].rbase};
+    const int block = 256, grid = std::max(1, std::min<int>((int)sp.size(), c->sm_count * 4));
+    const int64_t stride = std::max(1, edit_stride(P));
+    if (cudaError_t e = c->scratch.grow(sizeof(int32_t) * (size_t)stride * grid * block, st))
+        return fail(RB_ERR_OOM, "exact stats scratch: %s", cudaGetErrorString(e));
+    StatPart* d_parts = nullptr;
+    unsigned long long* d_ev = nullptr;
+    cudaError_t e = dev_alloc((void**)&d_parts, sizeof(StatPart) * std::max<size_t>(1, sp.size()), st);
+    if (!e) e = dev_alloc((void**)&d_ev, sizeof(unsigned long long) * RB_MAX_SLOTS, st);
+    unsigned long long h_ev[RB_MAX_SLOTS];
+    if (!e && !sp.empty()) e = cudaMemcpyAsync(d_parts, sp.data(), sizeof(StatPart) * sp.size(), cudaMemcpyHostToDevice, st);
+    if (!e) e = cudaMemsetAsync(d_ev, 0, sizeof(unsigned long long) * RB_MAX_SLOTS, st);
+    if (!e) e = launch_exact_stats(P->V, d_refs, d_parts, (int)sp.size(), row_lo, row_hi, flags, (int32_t*)c->scratch.p,
+                                   stride, d_ev, grid, block, st);
+    if (!e) e = cudaMemcpyAsync(h_ev, d_ev, sizeof h_ev, cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    dev_free(d_parts, st);
+    dev_free(d_ev, st);
+    if (e) return fail(RB_ERR_CUDA, "exact stats: %s", cudaGetErrorString(e));
+    for (int s = 0; s < RB_MAX_SLOTS; s++) slot_evals[s] = (int64_t)h_ev[s];
+    return RB_OK;
+}
+}  // namespace
+
 int rb::run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
             int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device) {
+    int rc = run_impl(c, rel, P, refs, total, parts, row_lo, row_hi, flags, want_parts, out, refs_on_device);
+    if (rc == RB_OK) {  // keep what this run taught the program for later programs of its shape
+        std::lock_guard<std::mutex> lock(c->mu);
+        std::lock_guard<std::mutex> lock2(P->ranges_mu);
+        Learned& L = c->learned[P->shape_key];
+        L.gate_off = P->gate_off;
+        L.last_rows = P->last_rows;
+        L.last_surv = P->last_surv;
+        L.surv_rate = P->surv_rate;
+        L.last_ranges = P->last_ranges;
+        L.last_n_items = P->last_n_items;
+    }
+    if (rc != RB_OK || !(flags & RB_EXACT_STATS)) return rc;
+    const int32_t* d_refs = refs ? (refs_on_device ? refs : (const int32_t*)c->refs.p) : nullptr;
+    rc = exact_stats(c, P, d_refs, parts, row_lo, row_hi, flags, (*out)->stats.slot_evals);
+    if (rc != RB_OK) {
+        rb_result_destroy(*out);
+        *out = nullptr;
+    }
+    return rc;
+}
+
+namespace {
+int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
+             int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device) {
     if (!c || !rel || !P || !out) return fail(RB_ERR_INVALID, "run: null argument");
     // every run on a context shares its scratch (items, counters, survivor
     // buffer, output pool) and its program's adaptive state: one at a time
@@ -1074,12 +1175,7 @@ int rb::run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t tot
     const int grid_v = c->sm_count * (J.ok ? J.verify_blocks_per_sm : 1);  // deferred verification
     int64_t stride = 0;
     if (P->lmax_edit >= 0) {
-        // a slice holds the banded DP row, or Myers' pattern table for bounds
-        // above 31 (rb_device.cuh lev_myers: 2 x MYERS_HS slots + MYERS_DCAP x W
-        // 64-bit masks, W = ceil(min(L, MYERS_NMAX) / 64))
-        int64_t need = P->lmax_edit + 2;
-        if (P->lmax_edit > 31) need = std::max<int64_t>(need, 2 * 64 + 2 * 48 * ((std::min<int64_t>(P->lmax_edit, 1024) + 63) / 64));
-        stride = (need + 31) & ~(int64_t)31;
+        stride = edit_stride(P);
         const size_t slices = (size_t)std::max(grid, std::max(gridg, grid_v)) * BLOCK;
         if (cudaError_t e = c->scratch.grow(sizeof(int32_t) * stride * slices, c->stream))
             return cleanup(fail(RB_ERR_OOM, "edit scratch (%lld B): %s",
@@ -1428,6 +1524,7 @@ int rb::run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t tot
     *out = res;
     return RB_OK;
 }
+}  // namespace
 
 extern "C" {
 

@@ -30,6 +30,13 @@ cudaError_t launch_composite_key(int64_t n, const CompositeSpec& spec, int32_t* 
 cudaError_t launch_pair_kernel(const FilterPlan& F, const VerifyProg& V, const RunParams& R, int grid,
                                cudaStream_t st);
 int pair_kernel_blocks_per_sm();
+// RB_EXACT_STATS: first-touch slot evaluations over every pair of `parts`
+struct StatPart {
+    int64_t base, n, split, rbase;
+};
+cudaError_t launch_exact_stats(const VerifyProg& V, const int32_t* refs, const StatPart* parts, int n_parts,
+                               int64_t row_lo, int64_t row_hi, uint32_t flags, int32_t* scratch, int64_t stride,
+                               unsigned long long* evals, int grid, int block, cudaStream_t st);
 
 // NVRTC specialisation (rb_jit.cu).  A JitKernel is looked up (or compiled
 // once per process) from the program's shape; `ok` false means the generic

@@ -121,6 +121,52 @@ cudaError_t launch_composite_key(int64_t n, const CompositeSpec& spec, int32_t* 
     return cudaGetLastError();
 }
 
+// RB_EXACT_STATS: every pair of every part through the exact interpreter,
+// counting each slot's first touch per pair (evaluate_pair, engine.py:93-132)
+// into shared counters; one global add per slot and block.
+__global__ void exact_stats_kernel(VerifyProg V, const int32_t* __restrict__ refs, const StatPart* __restrict__ parts,
+                                   int n_parts, int64_t row_lo, int64_t row_hi, uint32_t flags, int32_t* scratch,
+                                   int64_t stride, unsigned long long* evals) {
+    __shared__ unsigned long long cnt[RB_MAX_SLOTS];
+    for (int k = threadIdx.x; k < RB_MAX_SLOTS; k += blockDim.x) cnt[k] = 0;
+    __syncthreads();
+    int32_t* scr = scratch + (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) * stride;
+    const bool sym = (flags & RB_SYMMETRIC) != 0, enumerate = (flags & RB_ENUMERATE) != 0;
+    for (int p = blockIdx.x; p < n_parts; p += gridDim.x) {
+        const StatPart P = parts[p];
+        const bool cross = P.split >= 0;
+        const int64_t rlo = max((int64_t)0, row_lo), rhi = min(row_hi, cross ? P.split : P.n);
+        for (int64_t i = rlo; i < rhi; i++) {
+            const int64_t pi = P.base + i;
+            const int32_t ti = refs ? __ldg(refs + pi) : (int32_t)pi;
+            int64_t jlo, jhi;
+            if (cross) {
+                jlo = P.rbase;
+                jhi = P.rbase + (P.n - P.split);
+            } else {
+                jlo = P.base + (sym ? i + 1 : 0);
+                jhi = P.base + P.n;
+            }
+            for (int64_t pj = jlo + threadIdx.x; pj < jhi; pj += blockDim.x) {
+                if (!cross && pj == pi) continue;
+                const int32_t si = refs ? __ldg(refs + pj) : (int32_t)pj;
+                interpret(V, ti, si, enumerate, scr, cnt);
+            }
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < V.n_slots && k < RB_MAX_SLOTS; k += blockDim.x)
+        if (cnt[k]) atomicAdd(evals + k, cnt[k]);
+}
+
+cudaError_t launch_exact_stats(const VerifyProg& V, const int32_t* refs, const StatPart* parts, int n_parts,
+                               int64_t row_lo, int64_t row_hi, uint32_t flags, int32_t* scratch, int64_t stride,
+                               unsigned long long* evals, int grid, int block, cudaStream_t st) {
+    if (n_parts <= 0) return cudaSuccess;
+    exact_stats_kernel<<<grid, block, 0, st>>>(V, refs, parts, n_parts, row_lo, row_hi, flags, scratch, stride, evals);
+    return cudaGetLastError();
+}
+
 // Range check of a run's tuple refs (replaces a host scan of every ref).
 __global__ void refs_check_kernel(const int32_t* __restrict__ refs, int64_t n, int64_t limit,
                                   unsigned long long* bad) {

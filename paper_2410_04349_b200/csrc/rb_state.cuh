@@ -2,6 +2,7 @@
 // rb_prog, rb_result) shared by rb_api.cu (relations, programs, runs) and
 // rb_pipeline.cu (device partitioning and collect).  Not part of the ABI.
 #pragma once
+#include <unordered_map>
 
 #include <cuda_runtime.h>
 
@@ -109,6 +110,19 @@ using rb::FilterPlan;
 using rb::VerifyProg;
 using rb::JitKernel;
 
+// What runs taught a program (variant, buffer sizes, survivor ranges), kept
+// per context under the program's shape key: a new rb_prog for the same
+// program over a relation of the same shape (the public API building its
+// objects afresh on every call) starts from it instead of probing again.
+// Only sizing hints: overflow handling keeps every run exact.
+struct Learned {
+    bool gate_off = false;
+    long long last_rows = 0, last_surv = 0;
+    double surv_rate = -1.0;
+    std::vector<std::pair<int, int>> last_ranges;
+    int last_n_items = -1;
+};
+
 struct rb_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -128,6 +142,7 @@ struct rb_ctx {
     PinnedVec<Item> host_items;              // the last run's work items
     PinnedVec<int32_t> host_offs;            // the last run's part starts / ends (packed items)
     std::mutex mu;                           // runs on one context are serialised (shared scratch)
+    std::unordered_map<uint64_t, Learned> learned;  // by rb_prog::shape_key, guarded by mu
 };
 
 struct rb_rel {
@@ -168,7 +183,10 @@ struct rb_prog {
     std::vector<std::pair<int, int>> last_ranges;
     int last_n_items = -1;
     std::mutex ranges_mu;  // guards last_ranges / last_n_items (a program may be run from several threads)
+    uint64_t shape_key = 0;  // hash of the program arrays + relation shape (rb_ctx::learned)
 };
+
+
 
 struct rb_result {
     rb_ctx* ctx = nullptr;

@@ -31,7 +31,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._lib import RB_ENUMERATE, RB_STATS, RB_SYMMETRIC, check, i32, lib, ptr
+from ._lib import RB_ENUMERATE, RB_EXACT_STATS, RB_STATS, RB_SYMMETRIC, check, i32, lib, ptr
 from .encode import COL_CHARS, COL_CODES, COL_MASK, COL_TOKENS, Encoded, RelationEncoding, compile_program
 from .errors import ConfigError, SchemaError
 
@@ -50,6 +50,10 @@ class EngineConfig:
     chunk_size: int = 4096
     enumerate_witnesses: bool = False
     device_stats: bool = True  # per-slot exact-evaluation counters (RB_STATS)
+    # slot_evals = first-touch evaluations over EVERY pair (evaluate_pair,
+    # engine.py:122-128; SURVEY 8d's E_s) from an extra exact pass
+    # (RB_EXACT_STATS); off: the counts of the pairs the filter passed on
+    exact_slot_evals: bool = False
 
     def __post_init__(self) -> None:
         if self.n_t < 1 or self.n_w < 1 or self.lanes_per_block < 1:
@@ -69,7 +73,7 @@ class EngineConfig:
             return cls()
         if isinstance(cfg, cls):
             return cfg
-        names = [f for f in cls.__dataclass_fields__ if f != "device_stats"]
+        names = [f for f in cls.__dataclass_fields__ if f not in ("device_stats", "exact_slot_evals")]
         return cls(**{f: getattr(cfg, f) for f in names if hasattr(cfg, f)})
 
     def resolved_blocks(self) -> int:
@@ -81,6 +85,8 @@ class EngineConfig:
             f |= RB_ENUMERATE
         if self.device_stats:
             f |= RB_STATS
+        if self.exact_slot_evals:
+            f |= RB_EXACT_STATS
         return f
 
 

@@ -487,10 +487,12 @@ def plan_partitions(enc: Encoded, path, max_partition_size: int = 65536) -> list
         if pred.comparator != "eq" or pred.is_cross_attr:
             raise ValueError(f"plan_partitions handles equality roots only, not {pred.describe()}")
         codes = enc.columns[enc.get(("codes", pred.lhs_attr))].data
-        order = np.argsort(codes, kind="stable")  # tids ascending inside each key
+        order = np.argsort(codes, kind="stable").astype(np.int32)  # tids ascending inside each key
         sc = codes[order]
-        cuts = np.flatnonzero(sc[1:] != sc[:-1]) + 1
-        for g in np.split(order.astype(np.int32), cuts):
+        starts = np.flatnonzero(np.r_[True, sc[1:] != sc[:-1]])
+        sizes = np.diff(np.r_[starts, len(sc)])
+        for a, m in zip(starts[sizes > 1].tolist(), sizes[sizes > 1].tolist()):  # single tuples: no pairs
+            g = order[a:a + m]
             if len(g) <= max_partition_size:
                 if len(g) > 1:
                     blocks.append((g, -1))

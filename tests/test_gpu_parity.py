@@ -147,3 +147,33 @@ def test_evaluate_pair_known_answers():
     bm.reset()
     evaluate_pair(path, T[0], T[4], bm, None, rel.schema)
     assert bm.scorer_calls.max() <= 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", [n for n in goldens.names() if n.startswith(("random_0", "products", "edge", "grouped"))][:40])
+def test_exact_slot_evals_equal_oracle_first_touch(name):
+    """RB_EXACT_STATS: the device's per-slot first-touch counts over every
+    pair equal the oracle's (evaluate_pair semantics, engine.py:122-128;
+    SURVEY 8d E_s) -- for partitions, shuffled refs and cross runs."""
+    from oracle import oracle
+    from paper_2410_04349_b200.encode import RelationEncoding, compile_program
+
+    rel, path, cases = goldens.load(name)
+    enc = RelationEncoding(rel).prepare(path.predicate_table)
+    prog = compile_program(path, enc)
+    for case in cases:
+        cfg = EngineConfig(symmetric_mode=case["symmetric"], enumerate_witnesses=case["enumerate"],
+                           exact_slot_evals=True)
+        flags = (1 if case["symmetric"] else 0) | (2 if case["enumerate"] else 0)
+        if case["left"] is not None:
+            left, right = DataPartition(0, tuple(case["left"])), DataPartition(1, tuple(case["right"]))
+            cs = run_cross(left, right, rel, path, cfg)
+            refs = np.array(case["left"] + case["right"], dtype=np.int32)
+            _, cmp, ev = oracle.run(enc, prog, refs, len(refs), split=len(case["left"]), flags=flags)
+        else:
+            refs = tuple(range(len(rel))) if case["refs"] is None else tuple(case["refs"])
+            cs = run_partition(DataPartition(0, refs), rel, path, cfg)
+            _, cmp, ev = oracle.run(enc, prog, np.array(refs, dtype=np.int32), len(refs), flags=flags)
+        got = np.sum([b.slot_evals for b in cs.stats.blocks], axis=0)
+        assert cs.stats.total_comparisons() == cmp
+        assert got.tolist() == np.asarray(ev).tolist(), (name, case["name"])

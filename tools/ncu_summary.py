@@ -1,33 +1,38 @@
 """Summarise one `ncu --set full` capture of the pair kernel into
-profiles/traffic.json (read by bench.py for roofline.traffic and the pipe
-utilisation):  python tools/ncu_summary.py REP.ncu-rep WORKLOAD N DETAILS_CSV"""
+profiles/traffic.json (read by bench.py for roofline.traffic and the binding
+pipe):  python tools/ncu_summary.py REP.ncu-rep WORKLOAD N DETAILS_CSV [PAIRS_PER_LAUNCH]
+
+Keeps the DRAM bytes, duration, SM clock, issue / pipe utilisations and
+instruction counts of the captured launch, plus the hash of the device
+source it was built from (bench.py attributes a capture only to a run of the
+same kernel source)."""
 import csv
+import hashlib
 import io
 import json
 import os
 import subprocess
 import sys
 
-METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-           "smsp__issue_active.avg.pct_of_peak_sustained_active",
-           "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
-           "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-           "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
-           "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
-           "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
-           "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-           "smsp__inst_executed.sum"]
+KEEP_PREFIX = ("gpu__time_duration", "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__issue_active",
+               "sm__pipe_", "sm__inst_executed_pipe_", "smsp__inst_executed.sum", "sm__cycles_elapsed.avg",
+               "l1tex__data_pipe_lsu_wavefronts_mem_shared", "sm__warps_active", "launch__registers_per_thread",
+               "launch__occupancy_limit", "sm__throughput", "smsp__average_warps_issue_stalled")
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 rep, wl, n, details = sys.argv[1], sys.argv[2], int(sys.argv[3]), sys.argv[4]
+pairs = int(sys.argv[5]) if len(sys.argv) > 5 else None
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, units, v = rows[0], rows[1], rows[2]
-m = {k: {"value": v[h.index(k)], "unit": units[h.index(k)]} for k in METRICS if k in h}
-tb = sum(float(m[k]["value"]) * SCALE[m[k]["unit"]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
+m = {k: {"value": v[i], "unit": units[i]} for i, k in enumerate(h) if k.startswith(KEEP_PREFIX)}
+tb = sum(float(m[k]["value"].replace(",", "")) * SCALE[m[k]["unit"]]
+         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in m)
+sha = hashlib.sha1(open(os.path.join(ROOT, "paper_2410_04349_b200", "csrc", "rb_device.cuh"), "rb").read()).hexdigest()[:12]
+path = os.path.join(ROOT, "profiles", "traffic.json")
 doc = json.load(open(path)) if os.path.exists(path) else {}
 doc[wl] = {"n": n, "capture": details, "kernel": v[h.index("Kernel Name")] if "Kernel Name" in h else "",
-           "bytes_per_launch": tb, "metrics": m}
+           "kernel_sha": sha, "pairs": pairs, "bytes_per_launch": tb, "metrics": m}
 json.dump(doc, open(path, "w"), indent=1)
-print(wl, tb, {k: m[k]["value"] for k in m})
+print(wl, tb, len(m), "metrics kept")
