@@ -114,7 +114,9 @@ int rb_ctx_set_stream(rb_ctx* ctx, void* cuda_stream);
 int rb_ctx_destroy(rb_ctx* ctx);
 
 /* relation: uploaded once, shared by every program/partition over it
- * (the role of EncodedRelation shared copy-on-write, pipeline.py:273-307) */
+ * (the role of EncodedRelation shared copy-on-write, pipeline.py:273-307),
+ * from any context of the same device (programs and partition sets of a
+ * sibling context wait for its uploads; add no columns while they run) */
 int rb_relation_create(rb_ctx* ctx, int64_t n_tuples, rb_rel** out);
 int rb_relation_add_codes(rb_rel* rel, const int32_t* codes, int32_t* col);
 int rb_relation_add_mask(rb_rel* rel, const uint8_t* mask, int32_t* col);

@@ -15,6 +15,7 @@ from .engine import (
     PairBitmaps,
     PathProgram,
     evaluate_pair,
+    evaluate_pairs,
     RunStats,
     context,
     run_cross,
@@ -35,6 +36,7 @@ from .rules import MDRule, Predicate, RuleSet, parse_ruleset, predicate_universe
 __version__ = "0.1.0"
 
 __all__ = [
+    "evaluate_pairs",
     "BandingConfig", "BlockStats", "ColumnarRelation", "load_relation", "CandidateSet", "MultiDeviceEngine", "PipelineConfig", "PipelineResult",
     "iter_partitions", "pipeline_run", "Checkpoint", "ConfigError", "DataParseError", "DataPartition", "Encoded",
     "EngineConfig", "PairBitmaps", "evaluate_pair", "EvalPredicate", "ExecutionPath", "Kind", "MDRule", "MISSING", "PathProgram", "Predicate",

@@ -266,7 +266,10 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                       const int32_t* tables, int64_t n_tables, rb_prog** out) {
     if (!c || !rel || !out || (n_ins && (!op || !slot || !failj || !rule)) || (n_slots && !slots))
         return fail(RB_ERR_INVALID, "rb_program_create: null argument");
-    if (rel->ctx != c) return fail(RB_ERR_INVALID, "relation belongs to another context");
+    // a relation is shared by every context of its device (e.g. one per
+    // worker stream): its uploads, ordered on the owner's stream, finish first
+    if (rel->ctx->device != c->device) return fail(RB_ERR_INVALID, "relation lives on another device");
+    if (rel->ctx != c) CK(cudaStreamSynchronize(rel->ctx->stream));
     if (n_slots > RB_MAX_SLOTS) return fail(RB_ERR_LIMIT, "%d slots exceed the limit of %d", n_slots, RB_MAX_SLOTS);
     if (n_tables < 0 || (n_tables && !tables)) return fail(RB_ERR_INVALID, "bad table buffer");
     const int ncols = (int)rel->cols.size();
@@ -812,15 +815,15 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
         }
         P->shape_key = h;
         std::lock_guard<std::mutex> lock(c->mu);
-        auto it = c->learned.find(h);
+        const char* learn = std::getenv("RB_LEARN");  // RB_LEARN=0: every program starts cold (tests)
+        auto it = (learn && std::atoi(learn) == 0) ? c->learned.end() : c->learned.find(h);
         if (it != c->learned.end()) {
             const Learned& L = it->second;
             P->gate_off = L.gate_off;
             P->last_rows = L.last_rows;
             P->last_surv = L.last_surv;
             P->surv_rate = L.surv_rate;
-            P->last_ranges = L.last_ranges;
-            P->last_n_items = L.last_n_items;
+            P->range_plans = L.range_plans;
         }
     }
     *out = P;
@@ -911,8 +914,7 @@ int rb::run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t tot
         L.last_rows = P->last_rows;
         L.last_surv = P->last_surv;
         L.surv_rate = P->surv_rate;
-        L.last_ranges = P->last_ranges;
-        L.last_n_items = P->last_n_items;
+        L.range_plans = P->range_plans;
     }
     if (rc != RB_OK || !(flags & RB_EXACT_STATS)) return rc;
     const int32_t* d_refs = refs ? (refs_on_device ? refs : (const int32_t*)c->refs.p) : nullptr;
@@ -925,13 +927,119 @@ int rb::run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t tot
 }
 
 namespace {
+__global__ void remap_parts_kernel(int32_t* __restrict__ p, int64_t k, const int32_t* __restrict__ map) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = map[p[i]];
+}
+}  // namespace
+
+int rb::run_mixed(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total,
+                  const std::vector<Part>& parts, uint32_t flags, bool want_parts, rb_result** out,
+                  bool refs_on_device) {
+    // size classes: a "large" unit fills at least one 3-row item (768 outer
+    // rows) and one column chunk's worth of inner tuples
+    const int64_t big = 3 * (int64_t)BLOCK;
+    std::vector<int32_t> ia, ib;
+    for (size_t k = 0; k < parts.size(); k++) {
+        const Part& q = parts[k];
+        const int64_t rows = q.split >= 0 ? q.split : q.n, cols = q.split >= 0 ? q.n - q.split : q.n;
+        (rows >= big && cols >= big ? ib : ia).push_back((int32_t)k);
+    }
+    static const bool off = std::getenv("RB_MIXED") && std::atoi(std::getenv("RB_MIXED")) == 0;
+    if (off || ia.empty() || ib.empty())
+        return run(c, rel, P, refs, total, parts, 0, INT64_MAX, flags, want_parts, out, refs_on_device);
+    std::vector<Part> pa, pb;
+    for (int32_t k : ia) pa.push_back(parts[(size_t)k]);
+    for (int32_t k : ib) pb.push_back(parts[(size_t)k]);
+    rb_result *ra = nullptr, *rbg = nullptr;
+    int rc = run(c, rel, P, refs, total, pb, 0, INT64_MAX, flags, want_parts, &rbg, refs_on_device);
+    if (rc != RB_OK) return rc;
+    rc = run(c, rel, P, refs, total, pa, 0, INT64_MAX, flags, want_parts, &ra, refs_on_device);
+    if (rc != RB_OK) {
+        rb_result_destroy(rbg);
+        return rc;
+    }
+    std::lock_guard<std::mutex> lock(c->mu);
+    cudaStream_t st = c->stream;
+    rb_result* res = new (std::nothrow) rb_result();
+    if (!res) {
+        rb_result_destroy(ra);
+        rb_result_destroy(rbg);
+        return fail(RB_ERR_OOM, "host allocation failed");
+    }
+    res->ctx = c;
+    res->stream = st;
+    const int64_t k = ra->count + rbg->count;
+    res->cap = std::max<int64_t>(k, 1);
+    res->count = k;
+    cudaError_t e = cudaSuccess;
+    int32_t** dst[4] = {&res->d_t, &res->d_s, &res->d_r, &res->d_p};
+    int32_t* srca[4] = {ra->d_t, ra->d_s, ra->d_r, ra->d_p};
+    int32_t* srcb[4] = {rbg->d_t, rbg->d_s, rbg->d_r, rbg->d_p};
+    for (int q = 0; q < 4 && !e; q++) {
+        if (q == 3 && !want_parts) break;
+        e = dev_alloc((void**)dst[q], sizeof(int32_t) * (size_t)res->cap, st);
+        if (!e && ra->count) e = cudaMemcpyAsync(*dst[q], srca[q], sizeof(int32_t) * ra->count, cudaMemcpyDeviceToDevice, st);
+        if (!e && rbg->count)
+            e = cudaMemcpyAsync(*dst[q] + ra->count, srcb[q], sizeof(int32_t) * rbg->count, cudaMemcpyDeviceToDevice, st);
+    }
+    int32_t* d_map = nullptr;
+    if (!e && want_parts && k) {  // sub-run part indices -> the batch's
+        std::vector<int32_t> map(ia);
+        map.insert(map.end(), ib.begin(), ib.end());
+        e = dev_alloc((void**)&d_map, sizeof(int32_t) * map.size(), st);
+        if (!e) e = cudaMemcpyAsync(d_map, map.data(), sizeof(int32_t) * map.size(), cudaMemcpyHostToDevice, st);
+        // rows of ra index ia (map[0..|ia|)), rows of rbg index ib (map[|ia|..))
+        const int grid = (int)std::min<int64_t>((k + 255) / 256, (int64_t)c->sm_count * 8);
+        if (!e && ra->count) {
+            remap_parts_kernel<<<grid, 256, 0, st>>>(res->d_p, ra->count, d_map);
+            e = cudaGetLastError();
+        }
+        if (!e && rbg->count) {
+            remap_parts_kernel<<<grid, 256, 0, st>>>(res->d_p + ra->count, rbg->count, d_map + ia.size());
+            e = cudaGetLastError();
+        }
+    }
+    if (!e) e = cudaStreamSynchronize(st);
+    dev_free(d_map, st);
+    res->stats = rbg->stats;
+    rb_stats& S = res->stats;
+    const rb_stats& A = ra->stats;
+    S.comparisons += A.comparisons;
+    S.survivors += A.survivors;
+    S.emitted += A.emitted;
+    S.kernel_ms += A.kernel_ms;
+    S.pair_ms += A.pair_ms;
+    S.launches += A.launches;
+    S.retries += A.retries;
+    S.jit_compile_ms += A.jit_compile_ms;
+    S.specialized = std::min(S.specialized, A.specialized);
+    for (int s = 0; s < RB_MAX_SLOTS; s++) S.slot_evals[s] += A.slot_evals[s];
+    {
+        // the sub-results go back to the context (their buffers feed the pool)
+        c->mu.unlock();
+        rb_result_destroy(ra);
+        rb_result_destroy(rbg);
+        c->mu.lock();
+    }
+    if (e) {
+        for (int q = 0; q < 4; q++) dev_free(*dst[q], st);
+        delete res;
+        return fail(RB_ERR_CUDA, "merging the size classes of a batch: %s", cudaGetErrorString(e));
+    }
+    *out = res;
+    return RB_OK;
+}
+
+namespace {
 int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
              int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device) {
     if (!c || !rel || !P || !out) return fail(RB_ERR_INVALID, "run: null argument");
     // every run on a context shares its scratch (items, counters, survivor
     // buffer, output pool) and its program's adaptive state: one at a time
     std::lock_guard<std::mutex> ctx_lock(c->mu);
-    if (P->rel != rel || rel->ctx != c) return fail(RB_ERR_INVALID, "run: program/relation/context mismatch");
+    if (P->rel != rel || P->ctx != c || rel->ctx->device != c->device)
+        return fail(RB_ERR_INVALID, "run: program/relation/context mismatch");
     if (total < 0 || total > INT32_MAX) return fail(RB_ERR_INVALID, "run: partition size out of range");
     // tuple refs are range-checked on the device (refs_check_kernel, ahead of
     // the pair kernel, which then does nothing); the host scans only to name
@@ -1272,7 +1380,8 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
         size_t replay = 0;
         {
             std::lock_guard<std::mutex> lock(P->ranges_mu);
-            if (P->last_n_items == n_items) plan = P->last_ranges;
+            auto it = P->range_plans.find(n_items);
+            if (it != P->range_plans.end()) plan = it->second;
         }
         if (!plan.empty() && P->last_surv > scap) {  // replayed ranges: the buffer the last run ended with
             scap = P->last_surv;
@@ -1415,8 +1524,9 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
         P->last_surv = std::max(P->last_surv, widest);
         {
             std::lock_guard<std::mutex> lock(P->ranges_mu);
-            P->last_ranges.swap(merged);
-            P->last_n_items = n_items;
+            if (P->range_plans.size() >= 8 && !P->range_plans.count(n_items))
+                P->range_plans.erase(P->range_plans.begin());
+            P->range_plans[n_items].swap(merged);
         }
         // a gate that nearly every warp iteration passes only costs its vote:
         // later runs of this program use the ungated kernel
@@ -1561,7 +1671,7 @@ int rb_run_batch(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, const 
         parts.push_back(Part{offsets[k], len, sp, sp >= 0 ? offsets[k] + sp : 0});
     }
     const int64_t total = n_parts ? offsets[n_parts] : 0;
-    return run(c, rel, P, refs, total, parts, 0, INT64_MAX, flags, true, out);
+    return run_mixed(c, rel, P, refs, total, parts, flags, true, out);
 }
 
 int rb_result_copy_parts(const rb_result* r, int32_t* part) {

@@ -336,7 +336,8 @@ int finish_pulls(rb_parts* P, bool pulls, const std::vector<std::vector<std::pai
 int partition_impl(rb_ctx* c, rb_rel* rel, const int32_t* cols, const int64_t* keys, const int32_t* branch_ids,
                    int32_t nb, int64_t maxp, uint32_t flags, rb_parts** out) {
     if (!c || !rel || !out || nb < 1 || (!cols && !keys)) return fail(RB_ERR_INVALID, "rb_partition: bad arguments");
-    if (rel->ctx != c) return fail(RB_ERR_INVALID, "rb_partition: relation belongs to another context");
+    if (rel->ctx->device != c->device) return fail(RB_ERR_INVALID, "rb_partition: relation lives on another device");
+    if (rel->ctx != c) CKS(cudaStreamSynchronize(rel->ctx->stream));
     if (maxp < 1) return fail(RB_ERR_INVALID, "max_partition_size must be >= 1");
     const int64_t n = rel->n;
     if ((int64_t)nb * n > INT32_MAX) return fail(RB_ERR_LIMIT, "%d branches x %lld tuples exceed the run's position range", nb, (long long)n);
@@ -597,8 +598,7 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
         for (int64_t k : units)
             if (take[(size_t)k]) mine.push_back(parts->parts[(size_t)k]);
     }
-    return run(c, rel, P, parts->d_refs, (int64_t)parts->n_branches * parts->n, mine, 0, INT64_MAX, flags, false, out,
-               true);
+    return run_mixed(c, rel, P, parts->d_refs, (int64_t)parts->n_branches * parts->n, mine, flags, false, out, true);
 }
 
 int rb_result_collect(rb_result* res, int64_t n_tuples, int32_t n_rules) {

@@ -2,6 +2,7 @@
 // rb_prog, rb_result) shared by rb_api.cu (relations, programs, runs) and
 // rb_pipeline.cu (device partitioning and collect).  Not part of the ABI.
 #pragma once
+#include <map>
 #include <unordered_map>
 
 #include <cuda_runtime.h>
@@ -119,8 +120,7 @@ struct Learned {
     bool gate_off = false;
     long long last_rows = 0, last_surv = 0;
     double surv_rate = -1.0;
-    std::vector<std::pair<int, int>> last_ranges;
-    int last_n_items = -1;
+    std::map<int, std::vector<std::pair<int, int>>> range_plans;
 };
 
 struct rb_ctx {
@@ -177,12 +177,12 @@ struct rb_prog {
     long long last_rows = 0;  // output size of the previous run: sizes the next buffer
     long long last_surv = 0;  // survivors of the previous run: sizes the deferred-verification buffer
     double surv_rate = -1.0;  // survivors per work item in the previous run (-1: none yet)
-    // item ranges that fit the survivor buffer in the previous run, and its item count: a
-    // run over the same items (a repeated batch) replays them instead of re-learning where
-    // the survivors concentrate (each range that overflows is re-run)
-    std::vector<std::pair<int, int>> last_ranges;
-    int last_n_items = -1;
-    std::mutex ranges_mu;  // guards last_ranges / last_n_items (a program may be run from several threads)
+    // item ranges that fit the survivor buffer in earlier runs, by the run's item count: a
+    // run over the same items (a repeated batch, or one of the size classes of a mixed
+    // batch) replays them instead of re-learning where the survivors concentrate (each
+    // range that overflows is re-run).  At most 8 item counts are kept.
+    std::map<int, std::vector<std::pair<int, int>>> range_plans;
+    std::mutex ranges_mu;  // guards range_plans (a program may be run from several threads)
     uint64_t shape_key = 0;  // hash of the program arrays + relation shape (rb_ctx::learned)
 };
 
@@ -215,5 +215,10 @@ struct Part {
 int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
         int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out,
         bool refs_on_device = false);
+// a batch mixing large and small units runs as two runs -- the units with a
+// full item of rows on both sides on the large-partition kernel, the rest on
+// the small / packed variant -- and one merged result (part indices global)
+int run_mixed(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
+              uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device = false);
 
 }  // namespace rb

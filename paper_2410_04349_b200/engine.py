@@ -272,13 +272,15 @@ class PathProgram:
     (the reference's PathProgram, engine.py:342-368)."""
 
     def __init__(self, path, enc: Encoded, reg=None, device: Optional[int] = None, *, compiled=None,
-                 drel: Optional[DeviceRelation] = None):
+                 drel: Optional[DeviceRelation] = None, ctx: Optional[Context] = None):
         self.path = path
         self.enc = enc
         self.n_slots = len(path.predicate_table)
         self.program = compiled if compiled is not None else compile_program(path, enc, reg)
         self.rule_ids = list(path.rule_ids)
-        self.ctx = context(device) if drel is None else drel.ctx
+        # ctx: the context (stream) the program runs on; a relation uploaded
+        # through another context of the same device is shared, not copied
+        self.ctx = ctx if ctx is not None else (context(device) if drel is None else drel.ctx)
         self.drel = drel if drel is not None else device_relation(self.ctx, enc)
         h = _lib.c_vp()
         p = self.program
@@ -488,9 +490,10 @@ def evaluate_pair(path, t, s, bitmaps: PairBitmaps, reg=None, schema=None, all_w
     """The sequential per-pair interpreter (engine.py:93-132), evaluated on
     the device: a two-tuple relation (t, s) run as one ordered cross pair.
     Returns the first witness rule id (or None), or every witness when
-    ``all_witnesses``.  ``bitmaps.scorer_calls`` receives the exact device
-    evaluations per slot; predicates the phase-1 filter settles are not
-    counted, so counts never exceed the reference's."""
+    ``all_witnesses``.  ``bitmaps.scorer_calls`` receives the first-touch
+    evaluations per slot of the pair (RB_EXACT_STATS: the reference's own
+    counts).  One call is one small launch; ``evaluate_pairs`` decides many
+    pairs of a relation in one."""
     from .relation import Relation as _Relation
     from .relation import Schema as _Schema
     from .relation import TupleRecord as _TR
@@ -501,7 +504,7 @@ def evaluate_pair(path, t, s, bitmaps: PairBitmaps, reg=None, schema=None, all_w
     rel = _Relation(schema=sch, tuples=(_TR(0, t.eid, tuple(t.values)), _TR(1, s.eid, tuple(s.values))))
     enc = RelationEncoding(rel).prepare(list(path.predicate_table))
     prog = PathProgram(path, enc, reg)
-    flags = RB_STATS | (RB_ENUMERATE if all_witnesses else 0)
+    flags = RB_STATS | RB_EXACT_STATS | (RB_ENUMERATE if all_witnesses else 0)
     (tt, ss, rr), st = prog.run_raw(np.array([0, 1], dtype=np.int32), 2, flags, split=1)
     bitmaps.scorer_calls += np.array(st.slot_evals[: prog.n_slots], dtype=np.int64)
     bitmaps.reuse |= bitmaps.scorer_calls > 0
@@ -510,6 +513,31 @@ def evaluate_pair(path, t, s, bitmaps: PairBitmaps, reg=None, schema=None, all_w
     if all_witnesses:
         return hits
     return hits[0] if hits else None
+
+
+def evaluate_pairs(path, relation, pairs, reg=None, encoded=None, program=None, all_witnesses: bool = False) -> list:
+    """evaluate_pair for many (t_tid, s_tid) pairs of one relation in one
+    device launch (each pair an ordered 1 x 1 cross block: t is the left
+    tuple).  Returns, per pair, the first witness rule id (or None), or the
+    list of every witness in path order when ``all_witnesses``."""
+    prog = _program_for(path, relation, reg, encoded, program)
+    pairs = np.asarray(pairs, dtype=np.int32).reshape(-1, 2)
+    k = len(pairs)
+    if k == 0:
+        return []
+    refs = np.ascontiguousarray(pairs.reshape(-1))
+    offs = np.arange(0, 2 * k + 1, 2, dtype=np.int64)
+    flags = RB_ENUMERATE if all_witnesses else 0
+    (tt, ss, rr, pp), _ = prog.run_batch(refs, offs, np.ones(k, dtype=np.int64), flags)
+    order = {rid: j for j, rid in enumerate(path.checkpoint_order())}
+    hits: list = [[] for _ in range(k)]
+    for p, r in zip(pp.tolist(), rr.tolist()):
+        hits[p].append(prog.rule_ids[r])
+    out = []
+    for h in hits:
+        h.sort(key=lambda rid: order[rid])
+        out.append(h if all_witnesses else (h[0] if h else None))
+    return out
 
 
 def _dedup(t, s, r, symmetric: bool, enumerate_all: bool):

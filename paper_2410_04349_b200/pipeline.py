@@ -658,25 +658,176 @@ def pipeline_run(relation, rules, pipe_cfg: Optional[PipelineConfig] = None,
     if isinstance(enc, RelationEncoding):
         enc.prepare(list(path.predicate_table))
     encode_s = time.perf_counter() - t0
-    t0 = time.perf_counter()
     threshold = pipe_cfg.single_partition_threshold
     if threshold is None:
         threshold = pipe_cfg.max_partition_size
     if len(relation) <= threshold:
-        keys, bids, groups = None, None, None
+        res = run_pipeline_encoded(enc, path, pipe_cfg, engine_cfg, devices=devices, reg=reg)
+        res.timings.update(keys_s=0.0)
     else:
-        kb = partition_keys(relation, path, pipe_cfg.banding)
-        bids = [b for b, _, _ in kb]
-        keys = np.stack([k for _, k, _ in kb]) if kb else None
-        groups = {b: g for b, _, g in kb}
-    keys_s = time.perf_counter() - t0
-    res = run_pipeline_encoded(enc, path, pipe_cfg, engine_cfg, keys=keys, branch_ids=bids, devices=devices, reg=reg,
-                               key_groups=groups)
-    res.timings.update(plan_s=plan_s, encode_s=encode_s, keys_s=keys_s)
-    res.timings["partition_s"] += keys_s
-    res.timings["total_s"] += plan_s + encode_s + keys_s
+        res = _streamed_pipeline(relation, enc, path, pipe_cfg, engine_cfg, devices, reg)
+    res.timings.update(plan_s=plan_s, encode_s=encode_s)
+    res.timings["total_s"] += plan_s + encode_s
     res.plan = plan
     return res
+
+
+class _BranchParts:
+    """The partition set of a streamed pipeline run: one DeviceParts per
+    branch (each numbered from 0), read back as the reference's single pid /
+    sibling-group sequence (iter_partitions order across branches)."""
+
+    def __init__(self, parts: list):
+        self.parts = parts
+        self.n_partitions = sum(int(p.n_partitions) for p in parts)
+        self.n_pulls = sum(int(p.n_pulls) for p in parts)
+
+    def close(self) -> None:
+        for p in self.parts:
+            p.close()
+
+    def partitions(self) -> list:
+        out, pid0, sib0 = [], 0, 0
+        for dp in self.parts:
+            got = dp.partitions()
+            for p in got:
+                out.append(DataPartition(pid=p.pid + pid0, tuple_refs=p.tuple_refs, branch_id=p.branch_id,
+                                         key_group=p.key_group,
+                                         sibling_group=None if p.sibling_group is None else p.sibling_group + sib0))
+            pid0 += len(got)
+            sib0 += max([p.sibling_group or 0 for p in got], default=0)
+        return out
+
+    def pulls(self) -> list:
+        out, pid0 = [], 0
+        for dp in self.parts:
+            out += [(a + pid0, b + pid0) for a, b in dp.pulls()]
+            pid0 += int(dp.n_partitions)
+        return out
+
+
+def _streamed_pipeline(relation, enc, path, pipe_cfg, engine_cfg, devices, reg) -> PipelineResult:
+    """pipeline_run over hash partitions, branch by branch: the host computes
+    the next branch's partition keys (key strings, minhash bands) while every
+    device partitions and evaluates its LPT share of the previous branch --
+    the reference's overlapped partition / execute stages (pipeline.py:
+    282-283, 352-386).  Each device then collects its rows once; the devices'
+    collected runs are merged and collected on the first."""
+    import queue
+
+    from .encode import compile_program
+
+    devs = _cuda_devices(devices, pipe_cfg)
+    compiled = compile_program(path, enc, reg)
+    roots = root_predicates(path)
+    n, n_rules = enc.n, max(1, len(path.rule_ids))
+    flags = engine_cfg.flags()
+    wall0 = time.perf_counter()
+    queues = [queue.Queue() for _ in devs]
+    per_dev = [{"host": None, "stats": [], "parts": [], "tm": dict(partition_s=0.0, execute_s=0.0, collect_s=0.0,
+                                                                  upload_s=0.0, d2h_s=0.0, exchange_s=0.0)}
+               for _ in devs]
+    errors: list = []
+
+    def worker(k: int):
+        import torch
+
+        from .engine import DeviceRelation, PathProgram, context
+
+        d = per_dev[k]
+        results = []
+        try:
+            t0 = time.perf_counter()
+            ctx = context(devs[k])
+            drel = DeviceRelation(ctx, enc)
+            prog = PathProgram(path, enc, compiled=compiled, drel=drel)
+            d["tm"]["upload_s"] += time.perf_counter() - t0
+            while True:
+                item = queues[k].get()
+                if item is None:
+                    break
+                b, keys_b, groups_b = item
+                t0 = time.perf_counter()
+                parts = partition_on_device(prog, keys=keys_b[None, :], branch_ids=[b],
+                                            max_partition_size=pipe_cfg.max_partition_size,
+                                            pulls=pipe_cfg.enable_pulls, key_groups={b: groups_b} if k == 0 else None)
+                t1 = time.perf_counter()
+                res = prog.run_parts(parts, flags, k, len(devs))
+                d["stats"].append(res.stats())
+                results.append(res)
+                if k == 0:
+                    d["parts"].append(parts)
+                else:
+                    parts.close()
+                d["tm"]["partition_s"] += t1 - t0
+                d["tm"]["execute_s"] += time.perf_counter() - t1
+            t0 = time.perf_counter()
+            views = [r.torch_views() for r in results]
+            rows = tuple(torch.cat([v[c] for v in views]) if views else torch.empty(0, dtype=torch.int32,
+                                                                                    device=f"cuda:{devs[k]}")
+                         for c in range(3))
+            rows = collect_device_rows(rows, n, n_rules, ctx)
+            d["tm"]["collect_s"] += time.perf_counter() - t0
+            t0 = time.perf_counter()
+            d["host"] = tuple(x.cpu().numpy() for x in rows)
+            d["tm"]["d2h_s"] += time.perf_counter() - t0
+            prog.close()
+            drel.close()
+        except BaseException as exc:  # surfaced below
+            errors.append(exc)
+            while queues[k].get() is not None:  # drain: the producer must not block
+                pass
+        finally:
+            for r in results:
+                r.close()
+
+    threads = [threading.Thread(target=worker, args=(k,), name=f"rb-pipeline-gpu{devs[k]}") for k in range(len(devs))]
+    for t in threads:
+        t.start()
+    keys_s = 0.0
+    try:
+        for b in branch_order(path):  # host keys of branch b overlap the devices' work on branch b - 1
+            t0 = time.perf_counter()
+            ranks, distinct = rank_keys(branch_keys(relation, roots[b], pipe_cfg.banding))
+            keys_s += time.perf_counter() - t0
+            for q in queues:
+                q.put((b, ranks, distinct))
+    finally:
+        for q in queues:
+            q.put(None)
+        for t in threads:
+            t.join()
+    if errors:
+        for p in per_dev[0]["parts"]:
+            p.close()
+        raise errors[0]
+    t0 = time.perf_counter()
+    t, s, r = _merge_runs([d["host"] for d in per_dev], n, n_rules, devs[0])
+    merge_s = time.perf_counter() - t0
+    timings = {key: max(d["tm"][key] for d in per_dev) for key in per_dev[0]["tm"]}
+    timings["collect_s"] += merge_s
+    timings["keys_s"] = keys_s
+    timings["total_s"] = time.perf_counter() - wall0
+    from .engine import BlockStats
+
+    blocks, kernel_ms, launches = [], 0.0, 0
+    for k, d in enumerate(per_dev):
+        st = d["stats"]
+        blocks.append(BlockStats(block_id=k, comparisons=sum(int(x.comparisons) for x in st),
+                                 survivors=sum(int(x.survivors) for x in st), emitted=sum(int(x.emitted) for x in st),
+                                 busy_s=sum(x.kernel_ms for x in st) / 1e3,
+                                 slot_evals=np.sum([np.array(x.slot_evals[: len(path.predicate_table)], dtype=np.int64)
+                                                    for x in st], axis=0) if st else
+                                 np.zeros(len(path.predicate_table), dtype=np.int64)))
+        kernel_ms += sum(x.kernel_ms for x in st)
+        launches += sum(int(x.launches) for x in st)
+    cand = CandidateSet(arrays=(t, s, r), rule_ids=list(path.rule_ids),
+                        stats=RunStats(blocks=blocks, wall_s=timings["total_s"], kernel_ms=kernel_ms,
+                                       launches=launches))
+    parts = _BranchParts(per_dev[0]["parts"])
+    return PipelineResult(candidates=cand, timings=timings, assignment={}, n_partitions=parts.n_partitions,
+                          device_busy_s={devs[k]: per_dev[k]["tm"]["execute_s"] for k in range(len(devs))},
+                          plan=None, parts=parts)
 
 
 def _universe(rules):

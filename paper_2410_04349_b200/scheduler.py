@@ -120,8 +120,10 @@ class MultiDeviceEngine:
     """Evaluate one path over many partitions on several GPUs.
 
     ``devices`` lists CUDA device ordinals (repeat one to test on a single
-    GPU).  The encoded relation and the program are uploaded once per
-    worker thread, in that thread, so no CUDA state crosses threads."""
+    GPU).  The encoded relation is uploaded once per device and shared by
+    that device's worker threads; each worker runs its own program on its
+    own context (stream), so the H2D and launch of one unit overlap the
+    kernel of another."""
 
     def __init__(self, relation, path, devices=(0,), reg=None, encoded=None, workers_per_device: int = 2,
                  batch_pairs: int = 1 << 30, shard_pairs: int = 1 << 34):
@@ -140,14 +142,26 @@ class MultiDeviceEngine:
         self.compiled = compile_program(path, enc, reg)
         self.last_steals: list = []
         self.last_busy_s: list = []
+        self._rels: dict = {}  # device -> (owning context, DeviceRelation)
+        self._rel_lock = threading.Lock()
+
+    def _relation(self, device: int):
+        """One uploaded relation per device, shared by its workers' contexts."""
+        with self._rel_lock:
+            if device not in self._rels:
+                from .engine import Context, DeviceRelation
+
+                owner = Context(device)
+                self._rels[device] = (owner, DeviceRelation(owner, self.enc))
+            return self._rels[device][1]
 
     def _program(self, device: int, cache: dict) -> PathProgram:
         if "prog" not in cache:
-            from .engine import Context, DeviceRelation
+            from .engine import Context
 
             ctx = Context(device)  # a private context (stream) for this worker thread
-            drel = DeviceRelation(ctx, self.enc)
-            cache["prog"] = PathProgram(self.path, self.enc, compiled=self.compiled, drel=drel)
+            cache["prog"] = PathProgram(self.path, self.enc, compiled=self.compiled, drel=self._relation(device),
+                                        ctx=ctx)
         return cache["prog"]
 
     def run(self, blocks, cfg: Optional[EngineConfig] = None) -> list:

@@ -7,6 +7,13 @@ with RB_SURV_MIN / RB_SURV_LIMIT and compared with the reference goldens."""
 import pytest
 
 import goldens
+
+
+@pytest.fixture(autouse=True)
+def _cold_programs(monkeypatch):
+    """These tests drive the first-run streaming paths: programs must not
+    start from the sizes an earlier program of the same shape learned."""
+    monkeypatch.setenv("RB_LEARN", "0")
 from paper_2410_04349_b200 import DataPartition, EngineConfig, run_cross, run_partition
 
 CASES = ["citation", "products", "grouped", "edit_low", "skewed", "random_007", "random_031"]

@@ -177,3 +177,68 @@ def test_exact_slot_evals_equal_oracle_first_touch(name):
         got = np.sum([b.slot_evals for b in cs.stats.blocks], axis=0)
         assert cs.stats.total_comparisons() == cmp
         assert got.tolist() == np.asarray(ev).tolist(), (name, case["name"])
+
+
+@pytest.mark.parametrize("name", ["products", "edge_direction", "edge_cross_attr", "random_007", "random_031",
+                                  "random_064", "grouped"])
+def test_evaluate_pairs_batch_equals_oracle_witness(name):
+    """evaluate_pairs: many ordered pairs in one launch, each == the
+    oracle's first witness evaluated t-then-s (evaluate_pair semantics)."""
+    from oracle import oracle
+    from paper_2410_04349_b200 import evaluate_pairs
+    from paper_2410_04349_b200.encode import RelationEncoding, compile_program
+
+    rel, path, _ = goldens.load(name)
+    n = len(rel)
+    rng = np.random.default_rng(3)
+    pairs = rng.integers(0, n, size=(min(4000, n * n), 2)).astype(np.int32)
+    pairs = pairs[pairs[:, 0] != pairs[:, 1]]
+    got = evaluate_pairs(path, rel, pairs)
+    enc = RelationEncoding(rel).prepare(path.predicate_table)
+    prog = compile_program(path, enc)
+    want = oracle.witness(enc, prog, pairs[:, 0], pairs[:, 1])
+    assert got == [None if w < 0 else path.rule_ids[w] for w in want.tolist()]
+
+
+@pytest.mark.parametrize("symmetric", [True, False])
+def test_mixed_size_batch_runs_in_two_classes(symmetric):
+    """A batch of large (>= 768-tuple) and tiny units runs as two size
+    classes (rb::run_mixed): every unit's rows -- recovered through the
+    merged result's part indices -- equal its own run."""
+    from paper_2410_04349_b200 import run_partitions
+
+    rel, path, _ = goldens.load("citation")
+    n = len(rel)
+    rng = np.random.default_rng(5)
+    perm = rng.permutation(n)
+    parts, at = [], 0
+    for size in [900, 3, 1200, 2, 17, 5, 800, 40, 2, 9]:
+        parts.append(DataPartition(len(parts), tuple(int(x) for x in perm[at:at + size])))
+        at += size
+    cfg = EngineConfig(symmetric_mode=symmetric)
+    got = run_partitions(parts, rel, path, cfg)
+    for p, cs in zip(parts, got):
+        one = run_partition(p, rel, path, cfg)
+        assert sorted(cs.pairs) == sorted(one.pairs)
+        assert cs.stats.total_comparisons() == one.stats.total_comparisons()
+
+
+def test_learned_shape_replays_without_retries(monkeypatch):
+    """A new program of an already-run shape (the public API builds its
+    objects afresh each call) starts from what the first one learned: its
+    first run replays the survivor ranges with no overflow re-run."""
+    from paper_2410_04349_b200.encode import RelationEncoding
+
+    monkeypatch.setenv("RB_SURV_MIN", "64")
+    monkeypatch.delenv("RB_LEARN", raising=False)
+    rel, path, cases = goldens.load("citation")
+    enc = RelationEncoding(rel).prepare(path.predicate_table)
+    p1 = PathProgram(path, enc)
+    from paper_2410_04349_b200._lib import RB_SYMMETRIC
+
+    rows1, st1 = p1.run_raw(None, len(rel), RB_SYMMETRIC)
+    p2 = PathProgram(path, enc)
+    rows2, st2 = p2.run_raw(None, len(rel), RB_SYMMETRIC)
+    assert sorted(zip(*rows1)) == sorted(zip(*rows2))
+    assert st1.survivors > 64
+    assert st2.retries == 0

@@ -18,7 +18,7 @@ KEEP_PREFIX = ("gpu__time_duration", "dram__bytes_read.sum", "dram__bytes_write.
                "sm__pipe_", "sm__inst_executed_pipe_", "smsp__inst_executed.sum", "sm__cycles_elapsed.avg",
                "l1tex__data_pipe_lsu_wavefronts_mem_shared", "sm__warps_active", "launch__registers_per_thread",
                "launch__occupancy_limit", "sm__throughput", "smsp__average_warps_issue_stalled")
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 rep, wl, n, details = sys.argv[1], sys.argv[2], int(sys.argv[3]), sys.argv[4]

@@ -96,16 +96,66 @@ def scaling(args, tmp):
     return line
 
 
+def async_suite(args, tmp):
+    """suite_async (bench.py:314-372): grouped_workload(600 x 40, 150-char
+    texts), pipeline_run async vs sync on 4 simulated devices in the
+    reference; ours: pipeline_run on the GPU (one device)."""
+    rows, doc = grouped_workload(n_groups=600, group_size=40, text_len=150, seed=5, edit_threshold=0.8,
+                                 perturb_divisor=3)
+    relation, rules = rbench._load_instance(rows, doc, tmp, header=["group", "text"])
+    bundle = generate_plan(relation, rules, rbench.FAST_PLANNER)
+    cfg = ours.PipelineConfig(async_mode=True)
+    ours.pipeline_run(relation, rules, cfg, plan=bundle)
+    res, wall = timed(lambda: ours.pipeline_run(relation, rules, cfg, plan=bundle), 3)
+    line = {"suite": "suite_async", "n_tuples": len(relation), "partitions": res.n_partitions,
+            "pairs_evaluated": res.candidates.stats.total_comparisons(), "candidates": len(res.candidates),
+            "gpu_wall_s": wall, "gpu_timings_s": res.timings}
+    if args.reference:
+        want, rwall = timed(lambda: rpipeline.pipeline_run(relation, rules, rpipeline.PipelineConfig(async_mode=True),
+                                                           rengine.EngineConfig(num_blocks=1),
+                                                           rpipeline.make_devices(4), plan=bundle), 1)
+        line.update(reference_wall_s_async_4_devices=rwall, reference_cores=os.cpu_count(),
+                    identical=sorted(res.candidates.pairs) == sorted(want.candidates.pairs), speedup=rwall / wall)
+    return line
+
+
+def overlap_suite(args, tmp):
+    """grouped_workload(with_title_rule=True): a second rule rooted at a
+    title jaccard, so partitioning has a minhash-keyed branch with real
+    host hashing cost -- the reference's 'exercises stage overlap' case
+    (datasets.py:271-283).  Reports the host key time beside the wall: the
+    GPU work on the equality branch runs while the minhash keys are built."""
+    rows, doc = grouped_workload(n_groups=2000, group_size=50, seed=3, edit_threshold=0.8, perturb_divisor=3,
+                                 with_title_rule=True)
+    relation, rules = rbench._load_instance(rows, doc, tmp, header=["group", "text", "title"])
+    bundle = generate_plan(relation, rules, rbench.FAST_PLANNER)
+    cfg = ours.PipelineConfig(async_mode=True)
+    ours.pipeline_run(relation, rules, cfg, plan=bundle)
+    res, wall = timed(lambda: ours.pipeline_run(relation, rules, cfg, plan=bundle), 3)
+    line = {"suite": "overlap_title_minhash", "n_tuples": len(relation), "partitions": res.n_partitions,
+            "pairs_evaluated": res.candidates.stats.total_comparisons(), "candidates": len(res.candidates),
+            "gpu_wall_s": wall, "gpu_timings_s": res.timings,
+            "overlap": "wall < keys_s + partition_s + execute_s + collect_s when the stages overlap"}
+    if args.reference:
+        want, rwall = timed(lambda: rpipeline.pipeline_run(relation, rules, rpipeline.PipelineConfig(async_mode=True),
+                                                           rengine.EngineConfig(num_blocks=1),
+                                                           rpipeline.make_devices(1), plan=bundle), 1)
+        line.update(reference_wall_s_1_device=rwall, reference_cores=os.cpu_count(),
+                    identical=sorted(res.candidates.pairs) == sorted(want.candidates.pairs), speedup=rwall / wall)
+    return line
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reference", action="store_true", help="also run the reference engine (parity + its time)")
     ap.add_argument("--out", default=None)
-    ap.add_argument("--suites", default="stealing,scaling")
+    ap.add_argument("--suites", default="stealing,scaling,async,overlap")
     args = ap.parse_args()
     out = open(args.out, "w") if args.out else sys.stdout
     with tempfile.TemporaryDirectory() as tmp:
         for name in args.suites.split(","):
-            line = {"stealing": stealing, "scaling": scaling}[name](args, tmp)
+            line = {"stealing": stealing, "scaling": scaling, "async": async_suite, "overlap": overlap_suite}[name](args,
+                                                                                                           tmp)
             print(json.dumps(line), file=out, flush=True)
 
 
