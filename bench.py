@@ -245,10 +245,9 @@ def roofline(w_name, n, pairs_step, kernel_ms, clocks, bytes_per_pair=None, term
         return out
     bind = max(have, key=have.get)
     cap_ns = val.get("gpu__time_duration.sum")
-    if cap_ns is not None and m["gpu__time_duration.sum"].get("unit") == "msecond":
-        cap_ns *= 1e6
-    elif cap_ns is not None and m["gpu__time_duration.sum"].get("unit") == "usecond":
-        cap_ns *= 1e3
+    if cap_ns is not None:
+        cap_ns *= {"s": 1e9, "second": 1e9, "msecond": 1e6, "ms": 1e6, "usecond": 1e3, "us": 1e3}.get(
+            m["gpu__time_duration.sum"].get("unit", "nsecond"), 1.0)
     cap_mhz = val.get("sm__cycles_elapsed.avg.per_second")
     if cap_mhz is not None:
         unit = m["sm__cycles_elapsed.avg.per_second"].get("unit", "")

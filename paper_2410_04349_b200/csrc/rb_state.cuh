@@ -215,9 +215,10 @@ struct Part {
 int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
         int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out,
         bool refs_on_device = false);
-// a batch mixing large and small units runs as two runs -- the units with a
-// full item of rows on both sides on the large-partition kernel, the rest on
-// the small / packed variant -- and one merged result (part indices global)
+// with RB_MIXED=1, a batch mixing large and small units runs as two runs --
+// the units with a full item of rows on both sides on the large-partition
+// kernel, the rest on the small / packed variant -- and one merged result
+// (part indices global); otherwise one run
 int run_mixed(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
               uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device = false);
 

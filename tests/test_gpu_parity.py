@@ -201,12 +201,14 @@ def test_evaluate_pairs_batch_equals_oracle_witness(name):
 
 
 @pytest.mark.parametrize("symmetric", [True, False])
-def test_mixed_size_batch_runs_in_two_classes(symmetric):
+@pytest.mark.parametrize("mixed", ["1", "0"])
+def test_mixed_size_batch_runs_in_two_classes(symmetric, mixed, monkeypatch):
     """A batch of large (>= 768-tuple) and tiny units runs as two size
     classes (rb::run_mixed): every unit's rows -- recovered through the
     merged result's part indices -- equal its own run."""
     from paper_2410_04349_b200 import run_partitions
 
+    monkeypatch.setenv("RB_MIXED", mixed)
     rel, path, _ = goldens.load("citation")
     n = len(rel)
     rng = np.random.default_rng(5)
