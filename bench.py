@@ -313,16 +313,18 @@ class PipelineJob(Job):
         self.host_out = None
         from paper_2410_04349_b200.pipeline import ResidentPipeline, branch_order, root_predicates
 
-        from paper_2410_04349_b200._lib import RB_SYMMETRIC
-
         w = self.w
         roots = root_predicates(w.path)
         if any(p.comparator != "eq" or p.is_cross_attr for p in roots):
             raise SystemExit("pipeline workloads key equality roots on the code columns")
         self.bids = branch_order(w.path)
         self.cols = [w.enc.get(("codes", roots[b].lhs_attr)) for b in self.bids]
+        from paper_2410_04349_b200.engine import EngineConfig
+
+        # the product's default flags (symmetric, per-slot survivor counts): the e2e leg runs the same
         self.rp = ResidentPipeline(self.prog, code_cols=self.cols, branch_ids=self.bids,
-                                   max_partition_size=PIPELINE_MAXP, pulls=True, flags=RB_SYMMETRIC)
+                                   max_partition_size=PIPELINE_MAXP, pulls=True,
+                                   flags=EngineConfig(num_blocks=1).flags())
 
     def step(self, keep_parts=False):
         rows, st, ms = self.rp.step(self.rank, self.world, self.group, keep_parts=keep_parts)

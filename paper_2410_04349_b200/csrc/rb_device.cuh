@@ -495,7 +495,7 @@ static __device__ bool exact_slot(const VerifyProg& V, int s, int32_t ti, int32_
 // Returns the mask of checkpoint ordinals reached (first one only unless
 // enumerating).  engine.py:531-559.
 static __device__ uint64_t interpret(const VerifyProg& V, int32_t ti, int32_t si, bool enumerate, int32_t* scratch,
-                              unsigned long long* slot_evals) {
+                              unsigned long long* slot_evals, uint64_t* touched = nullptr) {
     uint64_t reuse = 0, value = 0, hit = 0;
     int ip = 0;
     while (ip < V.n_ins) {
@@ -518,19 +518,44 @@ static __device__ uint64_t interpret(const VerifyProg& V, int32_t ti, int32_t si
         }
         ip = truth ? ip + 1 : ins.z;
     }
+    if (touched) *touched = reuse;
     return hit;
+}
+
+// Per-slot first-touch counts of a warp's pairs, added with one shared-memory
+// atomic per touched slot (a ballot per slot instead of one global atomic per
+// evaluation: 538M survivors x a few slots contended on 64 global counters).
+static __device__ __forceinline__ void count_touched(uint64_t touched, unsigned long long* evals) {
+    const unsigned FULL = 0xffffffffu;
+    uint64_t any = ((uint64_t)__reduce_or_sync(FULL, (unsigned)(touched >> 32)) << 32) |
+                   (uint64_t)__reduce_or_sync(FULL, (unsigned)touched);
+    while (any) {
+        const int s = __ffsll((long long)any) - 1;
+        any &= any - 1;
+        const unsigned n = __popc(__ballot_sync(FULL, (touched >> s) & 1ull));
+        if ((threadIdx.x & 31) == 0) atomicAdd(evals + s, (unsigned long long)n);
+    }
 }
 
 // Warp-collective: every lane decides one pair (valid lanes only) with the
 // exact interpreter and the warp appends the reached checkpoints' rows with
 // one atomicAdd.  engine.py:531-559 + CandidateSink.reserve (214-246).
+// evals: per-slot counters the warp adds its first touches to (RB_STATS):
+// shared-memory counters of the block in the verify kernel, else null
 static __device__ __forceinline__ void verify_emit(const VerifyProg& V, const RunParams& R, bool valid, int32_t ti,
-                                                   int32_t si, int part, const int* cp_rule, int32_t* scratch) {
+                                                   int32_t si, int part, const int* cp_rule, int32_t* scratch,
+                                                   unsigned long long* evals = nullptr) {
     const int lane = threadIdx.x & 31;
     const bool enumerate = (R.flags & RB_ENUMERATE) != 0;
     const bool sym = (R.flags & RB_SYMMETRIC) != 0;
     uint64_t hit = 0;
-    if (valid) hit = interpret(V, ti, si, enumerate, scratch, (R.flags & RB_STATS) ? R.slot_evals : nullptr);
+    if (evals) {
+        uint64_t touched = 0;
+        if (valid) hit = interpret(V, ti, si, enumerate, scratch, nullptr, &touched);
+        count_touched(touched, evals);
+    } else if (valid) {
+        hit = interpret(V, ti, si, enumerate, scratch, (R.flags & RB_STATS) ? R.slot_evals : nullptr);
+    }
     const int cnt = __popcll(hit);
     int incl = cnt;
 #pragma unroll
@@ -597,8 +622,11 @@ static __device__ __forceinline__ void flush_survivors(const RunParams& R, const
 // keeps no interpreter state.
 __device__ __forceinline__ void verify_body(const VerifyProg& V, const RunParams& R) {
     __shared__ int cp_rule[RB_MAX_CHECKPOINTS];
+    __shared__ unsigned long long evals[RB_MAX_SLOTS];
     for (int k = threadIdx.x; k < RB_MAX_CHECKPOINTS; k += blockDim.x) cp_rule[k] = V.cp_rule[k];
+    for (int k = threadIdx.x; k < RB_MAX_SLOTS; k += blockDim.x) evals[k] = 0;
     __syncthreads();
+    const bool stats = (R.flags & RB_STATS) != 0;
     const unsigned long long cnt = *R.surv_count;
     const long long n = (long long)(cnt < (unsigned long long)R.surv_cap ? cnt : (unsigned long long)R.surv_cap);
     int32_t* scratch = R.scratch + (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) * R.scratch_stride;
@@ -607,7 +635,12 @@ __device__ __forceinline__ void verify_body(const VerifyProg& V, const RunParams
     for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
         const long long k = base + (threadIdx.x & 31);
         const int4 e = k < n ? R.surv[k] : make_int4(0, 0, 0, 0);
-        verify_emit(V, R, k < n, e.x, e.y, e.z, cp_rule, scratch);
+        verify_emit(V, R, k < n, e.x, e.y, e.z, cp_rule, scratch, stats ? evals : nullptr);
+    }
+    if (stats) {
+        __syncthreads();
+        for (int k = threadIdx.x; k < V.n_slots && k < RB_MAX_SLOTS; k += blockDim.x)
+            if (evals[k]) atomicAdd(R.slot_evals + k, evals[k]);
     }
 }
 
