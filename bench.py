@@ -866,7 +866,10 @@ def main():
     if evals_frac is not None:
         bpp, terms = algorithmic_bytes_per_pair(w.enc, w.path, evals_frac, len(rows[0]) / max(1, pairs_step))
     roof = roofline(w.name, w.n, pairs_step, k_ms, clocks, bpp, terms)
-    roof["kernel"] = "rb_pair_kernel_spec (NVRTC-specialised pair kernel; CUDA events on the engine's stream)"
+    roof["kernel"] = ("rb_pair_kernel_spec (NVRTC-specialised pair kernel; CUDA events on the engine's stream)"
+                      if st.specialized else "pair_kernel (GENERIC build: the NVRTC specialisation failed)")
+    if not st.specialized:
+        print("WARNING: the pair kernel ran the generic build: " + job.prog.jit_log[:400], file=sys.stderr)
     roof["kernel_share_of_step"] = k_ms / (t_total.item() / args.steps) if world == 1 else None
 
     if rank == 0:
@@ -893,7 +896,7 @@ def main():
                             "blocks": "DeviceRelation + PathProgram + PathProgram.run_batch"}[job.kind],
                     "phases_s": e2e_phases},
             "roofline": roof, "cpu_baseline": cpu, "parity": parity, "secondary": secondary,
-            "gpu_launches": int(st.launches) * args.steps,
+            "gpu_launches": int(st.launches) * args.steps, "kernel_specialized": bool(st.specialized),
             "clocks": clocks, "workload_gen_s": gen_s,
         }
         print(json.dumps(line), flush=True)

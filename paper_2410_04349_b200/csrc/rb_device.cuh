@@ -51,6 +51,7 @@ typedef unsigned long long uintptr_t;
 #define RB_SYMMETRIC 1u
 #define RB_ENUMERATE 2u
 #define RB_STATS 4u
+#define RB_MAX_SLOTS 64
 #define RB_MAX_CHECKPOINTS 64
 #endif
 
