@@ -43,6 +43,73 @@ int fail(int code, const char* fmt, ...) {
 
 using rb::g_err;
 
+// Stage-1 gate (specialised kernel): for each rule, in checkpoint order, not
+// yet ruled out by a chosen test, choose the equality key or always-evaluated
+// token slot holding its earliest path slot.  If every rule is covered, the
+// other equality / token tests run only for warps with a live pair after
+// stage 1.  `implied`: path slots known to hold for every pair of the run
+// (the equality root of the branch whose partitions are being evaluated:
+// every pair of a non-missing group shares the key).  An equality feature
+// testing only implied slots can never fail: it kills nothing, is never
+// chosen for stage 1 and is compiled out, so a rule it guarded is gated by
+// its next test (e.g. the Jaccard of `zip = ∧ address jaccard` inside a zip
+// partition).  Exactness is unaffected: the filter only prunes, the
+// interpreter re-decides every survivor.
+void rb::choose_gate(FilterPlan& F, const std::vector<uint64_t>& need, const std::vector<int>& first_pos, int n_slots,
+                     uint64_t implied) {
+    if (implied)
+        for (int f = 0; f < F.n_eq; f++)
+            if (F.eq_slots[f] && (F.eq_slots[f] & ~implied) == 0) F.eq_kill[f] = 0;
+    const char* env_gate = std::getenv("RB_GATE");
+    bool covered_all = !(env_gate && env_gate[0] == '0');
+    uint64_t covered = 0;
+    std::vector<char> eq_chosen(F.n_eq, 0);
+    std::vector<std::vector<char>> tok_chosen(F.n_tok, std::vector<char>(MAX_FSLOTS, 0));
+    for (size_t r = 0; r < need.size() && covered_all; r++) {
+        if ((covered >> r) & 1) continue;
+        int best_pos = INT32_MAX, bf = -1, bz = -1;  // bz < 0: equality key bf
+        for (int f = 0; f < F.n_eq; f++) {
+            if (!((F.eq_kill[f] >> r) & 1) || !(F.eq_slots[f] & need[r])) continue;
+            for (int sl2 = 0; sl2 < n_slots; sl2++)
+                if (((F.eq_slots[f] & need[r] & ~implied) >> sl2) & 1 && first_pos[sl2] < best_pos) {
+                    best_pos = first_pos[sl2];
+                    bf = f;
+                    bz = -1;
+                }
+        }
+        for (int f = 0; f < F.n_tok; f++) {
+            if (!F.tok_always[f]) continue;
+            for (int z = 0; z < F.tok_nslots[f]; z++) {
+                const FSlot& fs = F.tok_slot[f][z];
+                if (((fs.kill >> r) & 1) && ((need[r] >> fs.slot) & 1) && first_pos[fs.slot] < best_pos) {
+                    best_pos = first_pos[fs.slot];
+                    bf = f;
+                    bz = z;
+                }
+            }
+        }
+        if (bf < 0) {
+            covered_all = false;
+            break;
+        }
+        if (bz < 0) {
+            eq_chosen[bf] = 1;
+            covered |= F.eq_kill[bf];
+        } else {
+            tok_chosen[bf][bz] = 1;
+            covered |= F.tok_slot[bf][bz].kill;
+        }
+    }
+    F.gate = covered_all && F.n_rules > 0 ? 1 : 0;
+    for (int f = 0; f < F.n_eq; f++) F.eq_stage2[f] = F.gate && !eq_chosen[f] && F.eq_kill[f];
+    for (int f = 0; f < F.n_tok; f++)
+        for (int z = 0; z < F.tok_nslots[f]; z++) F.tok_slot[f][z].stage2 = F.gate && F.tok_always[f] && !tok_chosen[f][z];
+    // Even with nothing deferred the gate pays when stage 1 is selective:
+    // one vote then replaces the token / string feature votes (config 4:
+    // 9.3e11 with, 7.9e11 without); it costs one vote per inner tuple when
+    // stage 1 never fails inside the partitions (config 5: 7.0e11 vs 7.4e11).
+}
+
 extern "C" {
 
 const char* rb_last_error(void) { return g_err.c_str(); }
@@ -625,71 +692,14 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
                 for (int b = 0; b < F.n_eq; b++)
                     if ((F.eq_slots[b] >> F.tok_slot[f][z].slot) & 1) F.tok_slot[f][z].kill |= ek[b];
     }
-    // ---- stage-1 gate (specialised kernel): for each rule, in checkpoint
-    // order, not yet ruled out by a chosen test, choose the equality key or
-    // always-evaluated token slot holding its earliest path slot.  If every
-    // rule is covered, the other equality / token tests run only for warps
-    // with a live pair after stage 1.
+    // ---- stage-1 gate (specialised kernel): see choose_gate
     {
-        const char* env_gate = std::getenv("RB_GATE");
-        bool covered_all = !(env_gate && env_gate[0] == '0');
-        uint64_t covered = 0;
         std::vector<int> first_pos(n_slots, INT32_MAX);  // earliest instruction of each slot
         for (int k = 0; k < n_ins; k++)
             if (op[k] == 0 && first_pos[slot[k]] == INT32_MAX) first_pos[slot[k]] = k;
-        std::vector<char> eq_chosen(F.n_eq, 0);
-        std::vector<std::vector<char>> tok_chosen(F.n_tok, std::vector<char>(MAX_FSLOTS, 0));
-        for (size_t r = 0; r < need.size() && covered_all; r++) {
-            if ((covered >> r) & 1) continue;
-            int best_pos = INT32_MAX, bf = -1, bz = -1;  // bz < 0: equality key bf
-            for (int f = 0; f < F.n_eq; f++) {
-                if (!((F.eq_kill[f] >> r) & 1) || !(F.eq_slots[f] & need[r])) continue;
-                for (int sl2 = 0; sl2 < n_slots; sl2++)
-                    if (((F.eq_slots[f] & need[r]) >> sl2) & 1 && first_pos[sl2] < best_pos) {
-                        best_pos = first_pos[sl2];
-                        bf = f;
-                        bz = -1;
-                    }
-            }
-            for (int f = 0; f < F.n_tok; f++) {
-                if (!F.tok_always[f]) continue;
-                for (int z = 0; z < F.tok_nslots[f]; z++) {
-                    const FSlot& fs = F.tok_slot[f][z];
-                    if (((fs.kill >> r) & 1) && ((need[r] >> fs.slot) & 1) && first_pos[fs.slot] < best_pos) {
-                        best_pos = first_pos[fs.slot];
-                        bf = f;
-                        bz = z;
-                    }
-                }
-            }
-            if (bf < 0) {
-                covered_all = false;
-                break;
-            }
-            if (bz < 0) {
-                eq_chosen[bf] = 1;
-                covered |= F.eq_kill[bf];
-            } else {
-                tok_chosen[bf][bz] = 1;
-                covered |= F.tok_slot[bf][bz].kill;
-            }
-        }
-        F.gate = covered_all && F.n_rules > 0 ? 1 : 0;
-        bool deferred = false;  // a gate with nothing behind it is only a vote per inner tuple
-        for (int f = 0; f < F.n_eq; f++) {
-            F.eq_stage2[f] = F.gate && !eq_chosen[f];
-            deferred |= F.eq_stage2[f] != 0;
-        }
-        for (int f = 0; f < F.n_tok; f++)
-            for (int z = 0; z < F.tok_nslots[f]; z++) {
-                F.tok_slot[f][z].stage2 = F.gate && F.tok_always[f] && !tok_chosen[f][z];
-                deferred |= F.tok_slot[f][z].stage2 != 0;
-            }
-        // Even with nothing deferred the gate pays when stage 1 is selective:
-        // one vote then replaces the token / string feature votes (config 4:
-        // 9.3e11 with, 7.9e11 without); it costs one vote per inner tuple when
-        // stage 1 never fails inside the partitions (config 5: 7.0e11 vs 7.4e11).
-        (void)deferred;
+        P->gate_need = need;
+        P->gate_first_pos = first_pos;
+        choose_gate(F, need, first_pos, n_slots, 0);
     }
     std::vector<int32_t> stab(TAB_BASE, 0);  // guard entries: lookups of missing (-1) lengths land here
     {
@@ -869,7 +879,8 @@ int edit_stride(const rb_prog* P) {
 }
 
 int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
-             int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device);
+             int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device,
+             uint64_t implied);
 
 // RB_EXACT_STATS: after the run, one pass of the exact interpreter over
 // every pair of its parts counts each slot's first touches; they replace
@@ -904,8 +915,9 @@ int exact_stats(rb_ctx* c, rb_prog* P, const int32_t* d_refs, const std::vector<
 }  // namespace
 
 int rb::run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
-            int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device) {
-    int rc = run_impl(c, rel, P, refs, total, parts, row_lo, row_hi, flags, want_parts, out, refs_on_device);
+            int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device,
+            uint64_t implied) {
+    int rc = run_impl(c, rel, P, refs, total, parts, row_lo, row_hi, flags, want_parts, out, refs_on_device, implied);
     if (rc == RB_OK) {  // keep what this run taught the program for later programs of its shape
         std::lock_guard<std::mutex> lock(c->mu);
         std::lock_guard<std::mutex> lock2(P->ranges_mu);
@@ -963,6 +975,11 @@ int rb::run_mixed(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64
         rb_result_destroy(rbg);
         return rc;
     }
+    return merge_results(c, ra, rbg, want_parts, ia, ib, out);
+}
+
+int rb::merge_results(rb_ctx* c, rb_result* ra, rb_result* rbg, bool want_parts, const std::vector<int32_t>& ia,
+                      const std::vector<int32_t>& ib, rb_result** out) {
     std::lock_guard<std::mutex> lock(c->mu);
     cudaStream_t st = c->stream;
     rb_result* res = new (std::nothrow) rb_result();
@@ -1037,7 +1054,8 @@ int rb::run_mixed(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64
 
 namespace {
 int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
-             int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device) {
+             int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device,
+             uint64_t implied) {
     if (!c || !rel || !P || !out) return fail(RB_ERR_INVALID, "run: null argument");
     // every run on a context shares its scratch (items, counters, survivor
     // buffer, output pool) and its program's adaptive state: one at a time
@@ -1197,7 +1215,27 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
     // default; 0 disables) run the packed variant: whole partitions of up to
     // that size go back to back into one item, so every warp of a CTA has rows.
     const JitKernel* jp = &P->jit;
-    if (P->jit.ok && P->jit.defer && parts.size() > 1 && pack_max >= 2 &&
+    // a run whose pairs all satisfy some slots (`implied`) uses a filter plan
+    // regated without them (rb::choose_gate), compiled per variant on first
+    // use (the process-wide NVRTC cache keys on the plan)
+    FilterPlan Fi;
+    JitKernel Ji;
+    const FilterPlan* Fp = &P->F;
+    if (implied && P->jit.ok && !P->gate_need.empty()) {
+        Fi = P->F;
+        choose_gate(Fi, P->gate_need, P->gate_first_pos, P->n_slots, implied);
+        const bool packed_v = P->jit.defer && parts.size() > 1 && pack_max >= 2 &&
+                              total / (int64_t)parts.size() <= pack_max;
+        Ji = jit_pair_kernel(Fi, c->device, packed_v ? 2 : 0, packed_v);
+        if (Ji.ok && !packed_v && Ji.rows > 2 && !parts.empty() &&
+            total / (int64_t)parts.size() < (int64_t)BLOCK * Ji.rows)
+            Ji = jit_pair_kernel(Fi, c->device, 2);
+        if (Ji.ok && (!packed_v || Ji.packed)) {
+            jp = &Ji;
+            Fp = &Fi;
+        }
+    }
+    if (jp == &P->jit && P->jit.ok && P->jit.defer && parts.size() > 1 && pack_max >= 2 &&
         total / (int64_t)parts.size() <= pack_max) {
         static std::mutex packed_mu;
         std::lock_guard<std::mutex> lock(packed_mu);
@@ -1435,7 +1473,7 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
             R.out_p = res->d_p;
             R.cap = cap;
             CK(cudaEventRecord(c->ev0, c->stream));
-            cudaError_t e = launch_jit_kernel(J, P->F, P->V, R, std::max(1, std::min(hi - lo, grid)), c->stream);
+            cudaError_t e = launch_jit_kernel(J, *Fp, P->V, R, std::max(1, std::min(hi - lo, grid)), c->stream);
             if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel launch: %s", cudaGetErrorString(e)));
             CK(cudaEventRecord(c->ev_mid, c->stream));
             CK(cudaMemcpyAsync(host_ctr, ctr, sizeof(unsigned long long) * n_counters, cudaMemcpyDeviceToHost,
@@ -1534,7 +1572,8 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
         }
         // a gate that nearly every warp iteration passes only costs its vote:
         // later runs of this program use the ungated kernel
-        if (J.gated && base[GATE + 1] > 0 && (double)base[GATE] > 0.95 * (double)base[GATE + 1]) P->gate_off = true;
+        if (Fp == &P->F && J.gated && base[GATE + 1] > 0 && (double)base[GATE] > 0.95 * (double)base[GATE + 1])
+            P->gate_off = true;
         const long long rows = (long long)base[1];
         res->count = rows;
         res->stats.comparisons = (int64_t)base[2];
@@ -1602,7 +1641,7 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
         R.scratch_stride = stride;
 
         CK(cudaEventRecord(c->ev0, c->stream));
-        e = J.ok ? launch_jit_kernel(J, P->F, P->V, R, grid, c->stream)
+        e = J.ok ? launch_jit_kernel(J, *Fp, P->V, R, grid, c->stream)
                       : launch_pair_kernel(P->F, P->V, R, std::max(1, std::min(n_items, gridg)), c->stream);
         if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel launch: %s", cudaGetErrorString(e)));
         CK(cudaEventRecord(c->ev1, c->stream));

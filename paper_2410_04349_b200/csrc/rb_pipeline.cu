@@ -38,7 +38,9 @@ struct rb_parts {
     // (no pairs), implied by the gaps -- rb_parts_copy lists them too
     std::vector<Part> parts;
     std::vector<int32_t> branch, sibling;
+    std::vector<uint8_t> first_group;  // per entry: the branch's first key group (may be the missing-value group)
     std::vector<int32_t> branch_ids;  // branch id of position range [b*n, (b+1)*n)
+    std::vector<int32_t> root_slot;   // per branch position: path slot its key implies (rb_parts_set_roots), -1 none
     int64_t n_kept = 0;               // entries of parts that are partitions
     int64_t n_partitions = 0, n_pulls = 0, n_groups = 0;
 };
@@ -218,7 +220,7 @@ struct Scratch {
 // millions of single-tuple groups, which evaluate no pairs).
 int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, int key_bits, int64_t base,
                      int32_t branch, int64_t maxp, int& sibling_counter,
-                     std::vector<std::vector<std::pair<int64_t, int64_t>>>& sib_ranges) {
+                     std::vector<std::vector<std::pair<int64_t, int64_t>>>& sib_ranges, std::vector<uint8_t>& sib_first) {
     rb_ctx* c = P->ctx;
     cudaStream_t st = c->stream;
     const int64_t n = P->n;
@@ -278,10 +280,12 @@ int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, i
     int64_t extra = 0;  // sibling sub-partitions beyond one per group: pids of the single-tuple gaps follow
     for (int64_t g = 0; g < n_multi; g++) {
         const int64_t start = h_groups[(size_t)g].y, m = h_groups[(size_t)g].z;
+        const uint8_t first = h_groups[(size_t)g].x == 0;
         if (m <= maxp) {
             P->parts.push_back(Part{base + start, m, -1, 0});
             P->branch.push_back(branch);
             P->sibling.push_back(0);
+            P->first_group.push_back(first);
         } else {
             const int64_t k = (m + maxp - 1) / maxp, q = m / k, r = m % k;
             deals.push_back(Deal{start, m, k});  // positions relative to the branch
@@ -294,10 +298,12 @@ int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, i
                 P->parts.push_back(Part{at, sz, -1, 0});
                 P->branch.push_back(branch);
                 P->sibling.push_back(sibling_counter);
+                P->first_group.push_back(first);
                 ranges.push_back({at, sz});
                 at += sz;
             }
             sib_ranges.push_back(std::move(ranges));
+            sib_first.push_back(first);
         }
     }
     P->n_groups += runs;
@@ -315,7 +321,7 @@ int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, i
 }
 
 int finish_pulls(rb_parts* P, bool pulls, const std::vector<std::vector<std::pair<int64_t, int64_t>>>& sib_ranges,
-                 const std::vector<int32_t>& sib_branch) {
+                 const std::vector<int32_t>& sib_branch, const std::vector<uint8_t>& sib_first) {
     P->n_kept = (int64_t)P->parts.size();
     if (!pulls) return RB_OK;
     int gid = 0;
@@ -327,6 +333,7 @@ int finish_pulls(rb_parts* P, bool pulls, const std::vector<std::vector<std::pai
                 P->parts.push_back(Part{rg[i].first, rg[i].second + rg[j].second, rg[i].second, rg[j].first});
                 P->branch.push_back(sib_branch[g]);
                 P->sibling.push_back(gid);
+                P->first_group.push_back(sib_first[g]);
                 P->n_pulls++;
             }
     }
@@ -363,6 +370,7 @@ int partition_impl(rb_ctx* c, rb_rel* rel, const int32_t* cols, const int64_t* k
     int sibling_counter = 0;
     std::vector<std::vector<std::pair<int64_t, int64_t>>> sib_ranges;
     std::vector<int32_t> sib_branch;
+    std::vector<uint8_t> sib_first;
     {
         Scratch S(st);
         uint64_t* key;
@@ -400,12 +408,13 @@ int partition_impl(rb_ctx* c, rb_rel* rel, const int32_t* cols, const int64_t* k
             }
             if (cudaError_t e = cudaGetLastError()) return bail(fail(RB_ERR_CUDA, "partition keys: %s", cudaGetErrorString(e)));
             const size_t before = sib_ranges.size();
-            if (int rc = partition_branch(P, key, tid, key_bits, (int64_t)b * n, bid, maxp, sibling_counter, sib_ranges))
+            if (int rc = partition_branch(P, key, tid, key_bits, (int64_t)b * n, bid, maxp, sibling_counter, sib_ranges,
+                                          sib_first))
                 return bail(rc);
             for (size_t g = before; g < sib_ranges.size(); g++) sib_branch.push_back(bid);
         }
     }
-    finish_pulls(P, (flags & RB_PART_PULLS) != 0, sib_ranges, sib_branch);
+    finish_pulls(P, (flags & RB_PART_PULLS) != 0, sib_ranges, sib_branch, sib_first);
     *out = P;
     return RB_OK;
 }
@@ -550,6 +559,16 @@ int rb_parts_copy(const rb_parts* p, int32_t* refs, int64_t* base, int64_t* size
     return RB_OK;
 }
 
+int rb_parts_set_roots(rb_parts* p, const int32_t* root_slot, int32_t n_branches) {
+    if (!p || (n_branches && !root_slot)) return fail(RB_ERR_INVALID, "rb_parts_set_roots: null argument");
+    if (n_branches != (int32_t)p->branch_ids.size() && !(p->n == 0 && p->branch_ids.empty()))
+        return fail(RB_ERR_INVALID, "rb_parts_set_roots: %d slots for %zu branches", n_branches, p->branch_ids.size());
+    p->root_slot.assign(root_slot, root_slot + p->branch_ids.size());
+    for (int32_t s : p->root_slot)
+        if (s >= RB_MAX_SLOTS) return fail(RB_ERR_INVALID, "rb_parts_set_roots: slot %d", s);
+    return RB_OK;
+}
+
 int rb_parts_destroy(rb_parts* p) {
     if (!p) return RB_OK;
     cudaSetDevice(p->ctx->device);
@@ -574,9 +593,13 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
     for (size_t k = 0; k < parts->parts.size(); k++)
         if (pair_count(parts->parts[k], sym) > 0) units.push_back((int64_t)k);
     std::vector<Part> mine;
+    std::vector<int64_t> sel;  // entry index of every unit of `mine`
     if (world == 1) {
         mine.reserve(units.size());
-        for (int64_t k : units) mine.push_back(parts->parts[(size_t)k]);
+        for (int64_t k : units) {
+            mine.push_back(parts->parts[(size_t)k]);
+            sel.push_back(k);
+        }
     } else {
         // static longest-processing-time placement on pair counts (the same on
         // every rank): units in descending cost to the least-loaded rank
@@ -596,9 +619,63 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
             heap.push(top);
         }
         for (int64_t k : units)
-            if (take[(size_t)k]) mine.push_back(parts->parts[(size_t)k]);
+            if (take[(size_t)k]) {
+                mine.push_back(parts->parts[(size_t)k]);
+                sel.push_back(k);
+            }
     }
-    return run_mixed(c, rel, P, parts->d_refs, (int64_t)parts->n_branches * parts->n, mine, flags, false, out, true);
+    std::vector<int> sel_bpos(sel.size(), -1);  // branch position of every unit
+    for (size_t q = 0; q < sel.size(); q++)
+        for (size_t b = 0; b < parts->branch_ids.size(); b++)
+            if (parts->branch_ids[b] == parts->branch[(size_t)sel[q]]) {
+                sel_bpos[q] = (int)b;
+                break;
+            }
+    const int64_t total = (int64_t)parts->n_branches * parts->n;
+    // Units of a branch keyed on an equality root hold that slot for all their
+    // pairs (except the first key group, which may be the missing-value
+    // group): the branch holding most of this rank's pairs runs with the slot
+    // implied (rb::choose_gate), the other units as usual, one merged result.
+    int64_t best = 0;
+    int32_t best_b = -1;
+    if (!parts->root_slot.empty() && !std::getenv("RB_IMPLIED_OFF")) {
+        std::vector<int64_t> by_b(parts->branch_ids.size(), 0);
+        int64_t all = 0;
+        for (size_t q = 0; q < sel.size(); q++) {
+            const int64_t pc = pair_count(mine[q], sym);
+            all += pc;
+            const int bpos = sel_bpos[q];
+            if (bpos >= 0 && parts->root_slot[(size_t)bpos] >= 0 && !parts->first_group[(size_t)sel[q]]) by_b[(size_t)bpos] += pc;
+        }
+        for (size_t b = 0; b < by_b.size(); b++)
+            if (by_b[b] > best) {
+                best = by_b[b];
+                best_b = (int32_t)b;
+            }
+        if (best * 2 < all) best_b = -1;  // not worth a second run
+    }
+    if (best_b < 0) return run_mixed(c, rel, P, parts->d_refs, total, mine, flags, false, out, true);
+    std::vector<Part> pi, po;
+    std::vector<int32_t> ii, io;
+    for (size_t q = 0; q < sel.size(); q++) {
+        const bool imp = sel_bpos[q] == best_b && !parts->first_group[(size_t)sel[q]];
+        (imp ? pi : po).push_back(mine[q]);
+        (imp ? ii : io).push_back((int32_t)q);
+    }
+    const uint64_t implied = 1ull << parts->root_slot[(size_t)best_b];
+    rb_result* ri = nullptr;
+    int rc = run(c, rel, P, parts->d_refs, total, pi, 0, INT64_MAX, flags, false, &ri, true, implied);
+    if (rc != RB_OK || po.empty()) {
+        *out = ri;
+        return rc;
+    }
+    rb_result* ro = nullptr;
+    rc = run(c, rel, P, parts->d_refs, total, po, 0, INT64_MAX, flags, false, &ro, true);
+    if (rc != RB_OK) {
+        rb_result_destroy(ri);
+        return rc;
+    }
+    return merge_results(c, ro, ri, false, io, ii, out);
 }
 
 int rb_result_collect(rb_result* res, int64_t n_tuples, int32_t n_rules) {

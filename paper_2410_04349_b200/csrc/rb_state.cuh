@@ -184,6 +184,10 @@ struct rb_prog {
     std::map<int, std::vector<std::pair<int, int>>> range_plans;
     std::mutex ranges_mu;  // guards range_plans (a program may be run from several threads)
     uint64_t shape_key = 0;  // hash of the program arrays + relation shape (rb_ctx::learned)
+    // the stage-1 gate's inputs (rb::choose_gate), kept for the runs that know
+    // a slot holds for all their pairs (rb_run_parts: a branch's equality root)
+    std::vector<uint64_t> gate_need;
+    std::vector<int> gate_first_pos;
 };
 
 
@@ -214,7 +218,15 @@ struct Part {
 // when refs_on_device; parts index positions of refs
 int run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
         int64_t row_lo, int64_t row_hi, uint32_t flags, bool want_parts, rb_result** out,
-        bool refs_on_device = false);
+        bool refs_on_device = false, uint64_t implied = 0);
+// one result from two (rows of `a`, then of `b`); part indices remapped
+// through ia / ib when `want_parts`; consumes a and b
+int merge_results(rb_ctx* c, rb_result* a, rb_result* b, bool want_parts, const std::vector<int32_t>& ia,
+                  const std::vector<int32_t>& ib, rb_result** out);
+// the stage-1 gate of a filter plan (rb_api.cu); `implied`: slots true for every pair of the run
+void choose_gate(FilterPlan& F, const std::vector<uint64_t>& need, const std::vector<int>& first_pos, int n_slots,
+                 uint64_t implied);
+
 // with RB_MIXED=1, a batch mixing large and small units runs as two runs --
 // the units with a full item of rows on both sides on the large-partition
 // kernel, the rest on the small / packed variant -- and one merged result

@@ -299,6 +299,19 @@ class DeviceParts:
                 for k in range(self.n_partitions, self.n_partitions + self.n_pulls)]
 
 
+def implied_root_slots(path, branch_ids) -> list:
+    """Per branch: the path slot its partition key implies for every pair of
+    a group -- the root slot of a same-attribute equality edge (equal
+    canonical keys <=> equal codes <=> the slot holds, outside the missing
+    group) -- or -1 (minhash bands, cross-attribute keys)."""
+    out = []
+    for b in branch_ids:
+        s = path.root_slots[b]
+        p = path.predicate_table[s]
+        out.append(int(s) if p.comparator == "eq" and not p.is_cross_attr and p.rhs_attr is not None else -1)
+    return out
+
+
 def partition_on_device(prog, *, keys=None, code_cols=None, branch_ids, max_partition_size: int, pulls: bool,
                         key_groups=None) -> DeviceParts:
     """rb_partition / rb_partition_codes over the program's relation.
@@ -320,7 +333,10 @@ def partition_on_device(prog, *, keys=None, code_cols=None, branch_ids, max_part
         cols = np.ascontiguousarray(code_cols, dtype=np.int32)
         _lib.check(L.rb_partition_codes(prog.ctx.handle, prog.drel.handle, _lib.ptr(cols), _lib.ptr(bids), len(bids),
                                         int(max_partition_size), flags, _lib.ctypes.byref(h)))
-    return DeviceParts(h, prog.ctx, key_groups)
+    parts = DeviceParts(h, prog.ctx, key_groups)
+    roots = np.ascontiguousarray(implied_root_slots(prog.path, list(bids)), dtype=np.int32)
+    _lib.check(L.rb_parts_set_roots(h, _lib.ptr(roots), len(roots)))
+    return parts
 
 
 @dataclass

@@ -134,3 +134,34 @@ def test_device_collect_equals_lexsort(n_tuples, n_rules, k):
     assert cnt.value == len(want[0])
     for a, b in zip(got, want):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [30_000, 200_000])
+def test_implied_root_regating_keeps_the_candidate_set(n, monkeypatch):
+    """rb_run_parts evaluates the branch holding most pairs with its
+    equality root implied (rb::choose_gate): the same collected rows and
+    comparison counts as the plain filter plan (RB_IMPLIED_OFF)."""
+    from paper_2410_04349_b200 import synth
+    from paper_2410_04349_b200.pipeline import PipelineConfig, run_pipeline_encoded, root_predicates
+
+    w = synth.person5(n, seed=4)
+    roots = root_predicates(w.path)
+    bids = branch_order(w.path)
+    cols = [w.enc.get(("codes", roots[b].lhs_attr)) for b in bids]
+    cfg = PipelineConfig(max_partition_size=4096 if n > 50_000 else 512, enable_pulls=True,
+                         single_partition_threshold=0)
+    out = []
+    for off in ("1", None):
+        if off:
+            monkeypatch.setenv("RB_IMPLIED_OFF", off)
+        else:
+            monkeypatch.delenv("RB_IMPLIED_OFF", raising=False)
+        res = run_pipeline_encoded(w.enc, w.path, cfg, EngineConfig(), code_cols=cols, branch_ids=bids)
+        out.append((res.candidates.arrays, res.candidates.stats.total_comparisons()))
+        res.parts.close()
+    (a, ca), (b, cb) = out
+    assert ca == cb
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    assert len(a[0]) > 0
