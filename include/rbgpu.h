@@ -203,10 +203,11 @@ int rb_parts_copy(const rb_parts* parts, int32_t* refs, int64_t* base, int64_t* 
 /* The path slot each branch's key implies (root_slot[b], branch positions as
  * given to rb_partition; -1 for none): a branch keyed on the canonical value
  * of a same-attribute equality root holds that slot for every pair of its
- * groups, except possibly the first (the missing-value group).  rb_run_parts
- * then evaluates the branch holding most of the pairs with a filter plan
- * regated without that slot (the slot's test can never fail there). */
-int rb_parts_set_roots(rb_parts* parts, const int32_t* root_slot, int32_t n_branches);
+ * groups except the missing-value group (rb_partition_codes: key 0;
+ * rb_partition: the first group, unless first_missing[b] == 0 -- may be
+ * NULL).  rb_run_parts then evaluates the branch holding most of the pairs
+ * with a filter plan regated without that slot (its test cannot fail there). */
+int rb_parts_set_roots(rb_parts* parts, const int32_t* root_slot, const uint8_t* first_missing, int32_t n_branches);
 int rb_parts_destroy(rb_parts* parts);
 /* One batched run over every partition with pairs and every pull of
  * `parts` that rank `rank` of `world` owns: static longest-processing-time

@@ -89,7 +89,7 @@ _SIGNATURES = {
     "rb_parts_info": (ctypes.c_int, [c_vp, c_i64p, c_i64p, c_i64p, c_i64p]),
     "rb_parts_copy": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "rb_parts_destroy": (ctypes.c_int, [c_vp]),
-    "rb_parts_set_roots": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int32]),
+    "rb_parts_set_roots": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int32]),
     "rb_run_parts": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, c_vpp]),
     "rb_result_collect": (ctypes.c_int, [c_vp, ctypes.c_int64, ctypes.c_int32]),
     "rb_collect_device": (

@@ -41,6 +41,8 @@ struct rb_parts {
     std::vector<uint8_t> first_group;  // per entry: the branch's first key group (may be the missing-value group)
     std::vector<int32_t> branch_ids;  // branch id of position range [b*n, (b+1)*n)
     std::vector<int32_t> root_slot;   // per branch position: path slot its key implies (rb_parts_set_roots), -1 none
+    std::vector<uint8_t> first_missing;  // per branch position: its first key group may be the missing-value group
+    bool keyed_on_codes = false;
     int64_t n_kept = 0;               // entries of parts that are partitions
     int64_t n_partitions = 0, n_pulls = 0, n_groups = 0;
 };
@@ -264,6 +266,8 @@ int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, i
     tb = tbm;
     CKS(cub::DeviceSelect::Flagged(temp, tb, thrust::counting_iterator<int32_t>(0), flag, sel, d_sel, runs, st));
     int64_t n_multi = 0;
+    uint64_t first_key = 1;
+    if (runs) CKS(cudaMemcpyAsync(&first_key, uniq, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     CKS(cudaMemcpyAsync(&n_multi, d_sel, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CKS(cudaStreamSynchronize(st));
     CKS(S.get(&groups, n_multi));
@@ -308,6 +312,9 @@ int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, i
     }
     P->n_groups += runs;
     P->n_partitions += runs + extra;
+    // codes keys: missing values (code < 0) carry key 0, present ones code + 1;
+    // int64 keys: the first group is the smallest key, which may be the missing key
+    P->first_missing.push_back(P->keyed_on_codes ? (runs && first_key == 0) : 1);
     if (!deals.empty()) {
         // the deal reads the sorted ids (tid_out) and rewrites the oversize groups of dst
         Deal* d_deals;
@@ -359,6 +366,7 @@ int partition_impl(rb_ctx* c, rb_rel* rel, const int32_t* cols, const int64_t* k
     P->ctx = c;
     P->n = n;
     P->n_branches = nb;
+    P->keyed_on_codes = cols != nullptr;
     cudaStream_t st = c->stream;
     auto bail = [&](int rc) {
         dev_free(P->d_refs, st);
@@ -559,11 +567,14 @@ int rb_parts_copy(const rb_parts* p, int32_t* refs, int64_t* base, int64_t* size
     return RB_OK;
 }
 
-int rb_parts_set_roots(rb_parts* p, const int32_t* root_slot, int32_t n_branches) {
+int rb_parts_set_roots(rb_parts* p, const int32_t* root_slot, const uint8_t* first_missing, int32_t n_branches) {
     if (!p || (n_branches && !root_slot)) return fail(RB_ERR_INVALID, "rb_parts_set_roots: null argument");
     if (n_branches != (int32_t)p->branch_ids.size() && !(p->n == 0 && p->branch_ids.empty()))
         return fail(RB_ERR_INVALID, "rb_parts_set_roots: %d slots for %zu branches", n_branches, p->branch_ids.size());
     p->root_slot.assign(root_slot, root_slot + p->branch_ids.size());
+    if (first_missing && !p->keyed_on_codes)  // int64 keys: the caller knows whether key 0 is the missing key
+        for (size_t b = 0; b < p->branch_ids.size() && b < p->first_missing.size(); b++)
+            p->first_missing[b] = first_missing[b] ? 1 : 0;
     for (int32_t s : p->root_slot)
         if (s >= RB_MAX_SLOTS) return fail(RB_ERR_INVALID, "rb_parts_set_roots: slot %d", s);
     return RB_OK;
@@ -645,7 +656,9 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
             const int64_t pc = pair_count(mine[q], sym);
             all += pc;
             const int bpos = sel_bpos[q];
-            if (bpos >= 0 && parts->root_slot[(size_t)bpos] >= 0 && !parts->first_group[(size_t)sel[q]]) by_b[(size_t)bpos] += pc;
+            if (bpos >= 0 && parts->root_slot[(size_t)bpos] >= 0 &&
+                !(parts->first_group[(size_t)sel[q]] && parts->first_missing[(size_t)bpos]))
+                by_b[(size_t)bpos] += pc;
         }
         for (size_t b = 0; b < by_b.size(); b++)
             if (by_b[b] > best) {
@@ -658,7 +671,8 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
     std::vector<Part> pi, po;
     std::vector<int32_t> ii, io;
     for (size_t q = 0; q < sel.size(); q++) {
-        const bool imp = sel_bpos[q] == best_b && !parts->first_group[(size_t)sel[q]];
+        const bool imp = sel_bpos[q] == best_b &&
+                         !(parts->first_group[(size_t)sel[q]] && parts->first_missing[(size_t)best_b]);
         (imp ? pi : po).push_back(mine[q]);
         (imp ? ii : io).push_back((int32_t)q);
     }

@@ -335,7 +335,11 @@ def partition_on_device(prog, *, keys=None, code_cols=None, branch_ids, max_part
                                         int(max_partition_size), flags, _lib.ctypes.byref(h)))
     parts = DeviceParts(h, prog.ctx, key_groups)
     roots = np.ascontiguousarray(implied_root_slots(prog.path, list(bids)), dtype=np.int32)
-    _lib.check(L.rb_parts_set_roots(h, _lib.ptr(roots), len(roots)))
+    first_missing = None
+    if keys is not None:  # ranked key strings: the missing key sorts first when a branch has one
+        first_missing = np.array([1 if key_groups is None or not key_groups.get(int(b)) else
+                                  int(key_groups[int(b)][0] == MISSING_KEY) for b in bids], dtype=np.uint8)
+    _lib.check(L.rb_parts_set_roots(h, _lib.ptr(roots), _lib.ptr(first_missing), len(roots)))
     return parts
 
 
@@ -766,7 +770,7 @@ def _streamed_pipeline(relation, enc, path, pipe_cfg, engine_cfg, devices, reg) 
                 t0 = time.perf_counter()
                 parts = partition_on_device(prog, keys=keys_b[None, :], branch_ids=[b],
                                             max_partition_size=pipe_cfg.max_partition_size,
-                                            pulls=pipe_cfg.enable_pulls, key_groups={b: groups_b} if k == 0 else None)
+                                            pulls=pipe_cfg.enable_pulls, key_groups={b: groups_b})
                 t1 = time.perf_counter()
                 res = prog.run_parts(parts, flags, k, len(devs))
                 d["stats"].append(res.stats())
