@@ -56,10 +56,35 @@ using rb::g_err;
 // partition).  Exactness is unaffected: the filter only prunes, the
 // interpreter re-decides every survivor.
 void rb::choose_gate(FilterPlan& F, const std::vector<uint64_t>& need, const std::vector<int>& first_pos, int n_slots,
-                     uint64_t implied) {
-    if (implied)
+                     uint64_t implied, const std::vector<int>* cls) {
+    if (implied) {
         for (int f = 0; f < F.n_eq; f++)
             if (F.eq_slots[f] && (F.eq_slots[f] & ~implied) == 0) F.eq_kill[f] = 0;
+        // a token / string feature is "always" needed when some rule using it
+        // has no slot filtered before it; an implied slot filters nothing
+        if (cls && (int)cls->size() >= n_slots) {
+            for (int f = 0; f < F.n_tok; f++)
+                for (size_t r = 0; r < need.size() && !F.tok_always[f]; r++) {
+                    bool uses = false, earlier = false;
+                    for (int s = 0; s < n_slots; s++) {
+                        if (!(need[r] & (1ull << s))) continue;
+                        if ((*cls)[s] == 1 + f) uses = true;
+                        if ((*cls)[s] >= 0 && (*cls)[s] < 1 + f && !((implied >> s) & 1)) earlier = true;
+                    }
+                    if (uses && !earlier) F.tok_always[f] = 1;
+                }
+            for (int f = 0; f < F.n_str; f++)
+                for (size_t r = 0; r < need.size() && !F.str_always[f]; r++) {
+                    bool uses = false, earlier = false;
+                    for (int s = 0; s < n_slots; s++) {
+                        if (!(need[r] & (1ull << s))) continue;
+                        if ((*cls)[s] == 1 + MAX_TOK + f) uses = true;
+                        if ((*cls)[s] >= 0 && (*cls)[s] < 1 + MAX_TOK + f && !((implied >> s) & 1)) earlier = true;
+                    }
+                    if (uses && !earlier) F.str_always[f] = 1;
+                }
+        }
+    }
     const char* env_gate = std::getenv("RB_GATE");
     bool covered_all = !(env_gate && env_gate[0] == '0');
     uint64_t covered = 0;
@@ -699,6 +724,7 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             if (op[k] == 0 && first_pos[slot[k]] == INT32_MAX) first_pos[slot[k]] = k;
         P->gate_need = need;
         P->gate_first_pos = first_pos;
+        P->gate_cls.assign(cls.begin(), cls.end());
         choose_gate(F, need, first_pos, n_slots, 0);
     }
     std::vector<int32_t> stab(TAB_BASE, 0);  // guard entries: lookups of missing (-1) lengths land here
@@ -1223,7 +1249,7 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
     const FilterPlan* Fp = &P->F;
     if (implied && P->jit.ok && !P->gate_need.empty()) {
         Fi = P->F;
-        choose_gate(Fi, P->gate_need, P->gate_first_pos, P->n_slots, implied);
+        choose_gate(Fi, P->gate_need, P->gate_first_pos, P->n_slots, implied, &P->gate_cls);
         const bool packed_v = P->jit.defer && parts.size() > 1 && pack_max >= 2 &&
                               total / (int64_t)parts.size() <= pack_max;
         Ji = jit_pair_kernel(Fi, c->device, packed_v ? 2 : 0, packed_v);

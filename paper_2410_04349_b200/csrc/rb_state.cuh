@@ -188,6 +188,7 @@ struct rb_prog {
     // a slot holds for all their pairs (rb_run_parts: a branch's equality root)
     std::vector<uint64_t> gate_need;
     std::vector<int> gate_first_pos;
+    std::vector<int> gate_cls;  // feature class of every slot (0 eq / const, 1 + f token, 1 + MAX_TOK + f string)
 };
 
 
@@ -225,7 +226,7 @@ int merge_results(rb_ctx* c, rb_result* a, rb_result* b, bool want_parts, const 
                   const std::vector<int32_t>& ib, rb_result** out);
 // the stage-1 gate of a filter plan (rb_api.cu); `implied`: slots true for every pair of the run
 void choose_gate(FilterPlan& F, const std::vector<uint64_t>& need, const std::vector<int>& first_pos, int n_slots,
-                 uint64_t implied);
+                 uint64_t implied, const std::vector<int>* cls = nullptr);
 
 // with RB_MIXED=1, a batch mixing large and small units runs as two runs --
 // the units with a full item of rows on both sides on the large-partition
