@@ -496,10 +496,35 @@ def unit_sample(units, budget, seed=0):
     return chosen
 
 
+def oracle_units(enc, program, units, cores):
+    """The oracle over whole units [(refs, split)]: units of under 1e6 pairs
+    spread over a pool of `cores` host threads, one OpenMP thread each (the
+    C oracle releases the GIL; an OpenMP team per tiny unit would cost more
+    than the unit), larger ones one at a time with every thread.
+    Returns [(rows, pairs, evals)] in unit order."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle
+
+    def one(u, threads):
+        refs, sp = u
+        return oracle.run(enc, program, refs, len(refs), split=sp, flags=1, nthreads=threads)
+
+    cost = [sp * (len(r) - sp) if sp >= 0 else len(r) * (len(r) - 1) // 2 for r, sp in units]
+    out = [None] * len(units)
+    small = [k for k, c in enumerate(cost) if c < 1_000_000]
+    with ThreadPoolExecutor(max_workers=max(1, cores)) as pool:
+        for k, res in zip(small, pool.map(lambda k: one(units[k], 1), small)):
+            out[k] = res
+    for k, c in enumerate(cost):
+        if c >= 1_000_000:
+            out[k] = one(units[k], cores)
+    return out
+
+
 def units_parity(job, units, budget, cores):
     """Oracle on a sample of whole units (CPU baseline), the same units as
     one GPU batch, rows compared per unit."""
-    from oracle import oracle
     from paper_2410_04349_b200._lib import RB_SYMMETRIC
 
     w, prog = job.w, job.prog
@@ -510,12 +535,12 @@ def units_parity(job, units, budget, cores):
     np.cumsum([len(r) for r, _ in sub], out=offs[1:])
     (gt, gs, gr, gp), _ = prog.run_batch(refs, offs, np.array([sp for _, sp in sub], dtype=np.int64), RB_SYMMETRIC)
     got = sorted(zip(gp.tolist(), gt.tolist(), gs.tolist(), gr.tolist()))
-    want, secs, cmp_total = [], 0.0, 0
+    want, cmp_total = [], 0
     evals = np.zeros(prog.n_slots, dtype=np.int64)
-    for bi, (r, sp) in enumerate(sub):
-        t0 = time.perf_counter()
-        rows, cmp, ev = oracle.run(w.enc, prog.program, r, len(r), split=sp, flags=1, nthreads=cores)
-        secs += time.perf_counter() - t0
+    t0 = time.perf_counter()
+    results = oracle_units(w.enc, prog.program, sub, cores)
+    secs = time.perf_counter() - t0
+    for bi, (rows, cmp, ev) in enumerate(results):
         cmp_total += cmp
         evals += ev
         want += [(bi, int(a), int(b), int(c)) for a, b, c in rows]
@@ -640,12 +665,8 @@ def run_reference(args, rank, world):
         desc = "whole units (partitions / pulls)"
 
         def one(it):
-            c_it = 0
-            for k in chosen[: (4 if it < args.warmup else None)]:
-                refs, sp = units[k]
-                _, c, _ = oracle.run(w.enc, prog, refs, len(refs), split=sp, flags=1, nthreads=cores)
-                c_it += c
-            return c_it
+            sel = chosen[: (64 if it < args.warmup else None)]
+            return sum(c for _, c, _ in oracle_units(w.enc, prog, [units[k] for k in sel], cores))
         n_sample = len(chosen)
     else:
         rows = sample_rows(w.n, args.cpu_pairs)
