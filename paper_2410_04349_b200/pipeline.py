@@ -226,14 +226,59 @@ def rank_keys(keys: list) -> tuple[np.ndarray, list]:
     return rank[inv], [distinct[k] for k in order]
 
 
-def partition_keys(relation, path, banding: Optional[BandingConfig] = None):
+def _key_of_value(v, numeric: bool) -> str:
+    """The reference's equality key string of one value (partitioning.py:48-78)."""
+    if is_missing(v):
+        return MISSING_KEY
+    return f"n:{float(v)!r}" if numeric else f"v:{str(v).strip()}"
+
+
+def eq_branch_keys(relation, enc, pred):
+    """branch_keys + rank_keys for a same-attribute equality root, from the
+    encoding's dictionary codes: the reference key string is formed once per
+    DISTINCT value (a representative tuple of each code) instead of once per
+    tuple, then ranked; equal codes <=> equal canonical values <=> equal key
+    strings (missing: code -1 <=> MISSING_KEY).  Returns (int64 rank per
+    tuple, sorted distinct key strings), as rank_keys(branch_keys(...))."""
+    enc.slot_for(pred)
+    codes = enc.columns[enc.get(("codes", pred.lhs_attr))].data
+    numeric = is_numeric_kind(relation.schema.kind_of(pred.lhs_attr))
+    present = np.flatnonzero(codes >= 0)
+    uniq, first = np.unique(codes[present], return_index=True)
+    reps = present[first]
+    if hasattr(relation, "column"):
+        col = relation.column(pred.lhs_attr)
+        vals = [col[int(t)] for t in reps]
+    else:
+        k = relation.schema.index_of(pred.lhs_attr)
+        vals = [relation.tuples[int(t)].values[k] for t in reps]
+    keys = [_key_of_value(v, numeric) for v in vals]
+    has_missing = len(present) < len(codes)
+    distinct = sorted(keys + ([MISSING_KEY] if has_missing else []))
+    pos = {key: r for r, key in enumerate(distinct)}
+    lut = np.full(int(uniq.max()) + 2 if len(uniq) else 1, -1, dtype=np.int64)
+    lut[uniq] = [pos[key] for key in keys]
+    ranks = np.where(codes >= 0, lut[np.maximum(codes, 0)], pos.get(MISSING_KEY, -1)).astype(np.int64)
+    return ranks, distinct
+
+
+def branch_ranks(relation, path, b: int, banding: BandingConfig, enc=None):
+    """(int64 key rank per tuple, sorted distinct key strings) of branch b:
+    from the encoding's codes for a same-attribute equality root (O(distinct
+    values) key strings), else from the key strings of every tuple."""
+    pred = root_predicates(path)[b]
+    if enc is not None and pred.comparator == "eq" and not pred.is_cross_attr and pred.rhs_attr is not None:
+        return eq_branch_keys(relation, enc, pred)
+    return rank_keys(branch_keys(relation, pred, banding))
+
+
+def partition_keys(relation, path, banding: Optional[BandingConfig] = None, enc=None):
     """Per branch in iteration order: (branch id, int64 key per tuple, sorted
     distinct key strings).  Equal keys <=> equal reference key strings."""
     banding = banding or BandingConfig()
-    roots = root_predicates(path)
     out = []
     for b in branch_order(path):
-        ranks, distinct = rank_keys(branch_keys(relation, roots[b], banding))
+        ranks, distinct = branch_ranks(relation, path, b, banding, enc)
         out.append((b, ranks, distinct))
     return out
 
@@ -808,7 +853,7 @@ def _streamed_pipeline(relation, enc, path, pipe_cfg, engine_cfg, devices, reg) 
     try:
         for b in branch_order(path):  # host keys of branch b overlap the devices' work on branch b - 1
             t0 = time.perf_counter()
-            ranks, distinct = rank_keys(branch_keys(relation, roots[b], pipe_cfg.banding))
+            ranks, distinct = branch_ranks(relation, path, b, pipe_cfg.banding, enc)
             keys_s += time.perf_counter() - t0
             for q in queues:
                 q.put((b, ranks, distinct))

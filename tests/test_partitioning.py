@@ -91,3 +91,31 @@ def test_plan_partitions_equal_pipeline(max_size):
     got = [(tuple(int(x) for x in r), int(sp)) for r, sp in plan_partitions(enc, path, max_size)]
     assert sorted(got) == sorted(want)
     assert any(sp >= 0 for _, sp in got) == (max_size < 40)
+
+
+def test_eq_branch_keys_from_codes_equal_key_strings():
+    """pipeline.eq_branch_keys (key strings formed once per distinct value,
+    from the encoding's codes) == rank_keys(branch_keys(...)) (the
+    reference's key string of every tuple) on every equality root of the
+    fixtures."""
+    import numpy as np
+
+    from paper_2410_04349_b200.encode import RelationEncoding
+    from paper_2410_04349_b200.pipeline import (BandingConfig, branch_keys, branch_order, eq_branch_keys, rank_keys,
+                                                root_predicates)
+
+    import goldens
+
+    checked = 0
+    for name in goldens.pipeline_names() + goldens.names():
+        rel, path, _ = goldens.load(name)
+        enc = RelationEncoding(rel)
+        for b in branch_order(path):
+            pred = root_predicates(path)[b]
+            if pred.comparator != "eq" or pred.is_cross_attr or pred.rhs_attr is None:
+                continue
+            got = eq_branch_keys(rel, enc, pred)
+            want = rank_keys(branch_keys(rel, pred, BandingConfig()))
+            assert np.array_equal(got[0], want[0]) and got[1] == want[1], (name, b)
+            checked += 1
+    assert checked > 30
