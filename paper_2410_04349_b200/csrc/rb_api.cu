@@ -973,7 +973,7 @@ __global__ void remap_parts_kernel(int32_t* __restrict__ p, int64_t k, const int
 
 int rb::run_mixed(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total,
                   const std::vector<Part>& parts, uint32_t flags, bool want_parts, rb_result** out,
-                  bool refs_on_device) {
+                  bool refs_on_device, uint64_t implied) {
     // size classes: a "large" unit fills at least one 3-row item (768 outer
     // rows) and one column chunk's worth of inner tuples
     const int64_t big = 3 * (int64_t)BLOCK;
@@ -989,14 +989,14 @@ int rb::run_mixed(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64
     const char* mixed = std::getenv("RB_MIXED");
     const bool on = mixed && std::atoi(mixed) != 0;
     if (!on || ia.empty() || ib.empty())
-        return run(c, rel, P, refs, total, parts, 0, INT64_MAX, flags, want_parts, out, refs_on_device);
+        return run(c, rel, P, refs, total, parts, 0, INT64_MAX, flags, want_parts, out, refs_on_device, implied);
     std::vector<Part> pa, pb;
     for (int32_t k : ia) pa.push_back(parts[(size_t)k]);
     for (int32_t k : ib) pb.push_back(parts[(size_t)k]);
     rb_result *ra = nullptr, *rbg = nullptr;
-    int rc = run(c, rel, P, refs, total, pb, 0, INT64_MAX, flags, want_parts, &rbg, refs_on_device);
+    int rc = run(c, rel, P, refs, total, pb, 0, INT64_MAX, flags, want_parts, &rbg, refs_on_device, implied);
     if (rc != RB_OK) return rc;
-    rc = run(c, rel, P, refs, total, pa, 0, INT64_MAX, flags, want_parts, &ra, refs_on_device);
+    rc = run(c, rel, P, refs, total, pa, 0, INT64_MAX, flags, want_parts, &ra, refs_on_device, implied);
     if (rc != RB_OK) {
         rb_result_destroy(rbg);
         return rc;

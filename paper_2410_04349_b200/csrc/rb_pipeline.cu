@@ -678,13 +678,13 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
     }
     const uint64_t implied = 1ull << parts->root_slot[(size_t)best_b];
     rb_result* ri = nullptr;
-    int rc = run(c, rel, P, parts->d_refs, total, pi, 0, INT64_MAX, flags, false, &ri, true, implied);
+    int rc = run_mixed(c, rel, P, parts->d_refs, total, pi, flags, false, &ri, true, implied);
     if (rc != RB_OK || po.empty()) {
         *out = ri;
         return rc;
     }
     rb_result* ro = nullptr;
-    rc = run(c, rel, P, parts->d_refs, total, po, 0, INT64_MAX, flags, false, &ro, true);
+    rc = run_mixed(c, rel, P, parts->d_refs, total, po, flags, false, &ro, true);
     if (rc != RB_OK) {
         rb_result_destroy(ri);
         return rc;

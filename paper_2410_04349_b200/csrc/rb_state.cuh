@@ -233,6 +233,6 @@ void choose_gate(FilterPlan& F, const std::vector<uint64_t>& need, const std::ve
 // kernel, the rest on the small / packed variant -- and one merged result
 // (part indices global); otherwise one run
 int run_mixed(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t total, const std::vector<Part>& parts,
-              uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device = false);
+              uint32_t flags, bool want_parts, rb_result** out, bool refs_on_device = false, uint64_t implied = 0);
 
 }  // namespace rb
