@@ -294,7 +294,10 @@ class Job:
 
         self.args, self.w, self.rank, self.world, self.group, self.dev = args, w, rank, world, group, dev
         self.ctx = context(dev)
-        self.stream = torch.cuda.current_stream()
+        # one created (non-default) stream for torch and the engine alike: the
+        # legacy default stream would serialise against every other stream
+        self.stream = torch.cuda.Stream(device=dev)
+        torch.cuda.set_stream(self.stream)
         self.ctx.set_stream(self.stream.cuda_stream)
         self.prog = PathProgram(w.path, w.enc, device=dev)
         self.stage_ms = {}

@@ -98,7 +98,12 @@ class Column:
         return np.diff(self.offsets)
 
     def max_row_length(self) -> int:
-        return int(self.row_lengths().max(initial=0))
+        """Longest row (computed once per column: compile_program asks per slot)."""
+        cached = self.__dict__.get("_max_len")
+        if cached is None or cached[0] is not self.offsets:
+            cached = (self.offsets, int(self.row_lengths().max(initial=0)))
+            self.__dict__["_max_len"] = cached
+        return cached[1]
 
 
 def ragged(rows: list, dtype) -> tuple[np.ndarray, np.ndarray]:
