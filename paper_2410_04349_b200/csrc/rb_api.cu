@@ -857,6 +857,7 @@ int rb_program_create(rb_ctx* c, rb_rel* rel, const int32_t* op, const int32_t* 
             const Learned& L = it->second;
             P->gate_off = L.gate_off;
             P->last_rows = L.last_rows;
+            P->rows_by_items = L.rows_by_items;
             P->last_surv = L.last_surv;
             P->surv_rate = L.surv_rate;
             P->range_plans = L.range_plans;
@@ -950,6 +951,7 @@ int rb::run(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t tot
         Learned& L = c->learned[P->shape_key];
         L.gate_off = P->gate_off;
         L.last_rows = P->last_rows;
+        L.rows_by_items = P->rows_by_items;
         L.last_surv = P->last_surv;
         L.surv_rate = P->surv_rate;
         L.range_plans = P->range_plans;
@@ -1383,8 +1385,15 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
     // output rows: the previous run's count + 25%, at least RB_OUT_MIN (1M; tests lower it
     // to drive the grow-in-place path)
     const char* env_out = std::getenv("RB_OUT_MIN");
+    const int n_items_now = (int)items.size();
+    long long prev_rows = P->last_rows;
+    {  // the previous run over the same items (a size class of a mixed batch alternates with another)
+        std::lock_guard<std::mutex> lock(P->ranges_mu);
+        auto it = P->rows_by_items.find(n_items_now);
+        if (it != P->rows_by_items.end()) prev_rows = it->second;
+    }
     long long cap = std::max<long long>(env_out ? std::max(1ll, std::atoll(env_out)) : 1 << 20,
-                                        P->last_rows + P->last_rows / 4);
+                                        prev_rows + prev_rows / 4);
     unsigned long long* ctr = (unsigned long long*)c->counters.p;
     res->ctx = c;
     unsigned long long stack_ctr[n_counters];
@@ -1609,6 +1618,12 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
         res->stats.specialized = 1;
         res->stats.jit_compile_ms = J.compile_ms;
         P->last_rows = rows;
+        {
+            std::lock_guard<std::mutex> lock(P->ranges_mu);
+            if (P->rows_by_items.size() >= 8 && !P->rows_by_items.count(n_items_now))
+                P->rows_by_items.erase(P->rows_by_items.begin());
+            P->rows_by_items[n_items_now] = rows;
+        }
         for (int s = 0; s < RB_MAX_SLOTS; s++) res->stats.slot_evals[s] = (int64_t)base[4 + s];
         mark();  // verify done
         report();

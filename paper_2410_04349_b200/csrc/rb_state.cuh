@@ -119,6 +119,7 @@ using rb::JitKernel;
 struct Learned {
     bool gate_off = false;
     long long last_rows = 0, last_surv = 0;
+    std::map<int, long long> rows_by_items;
     double surv_rate = -1.0;
     std::map<int, std::vector<std::pair<int, int>>> range_plans;
 };
@@ -175,6 +176,7 @@ struct rb_prog {
     bool jit_packed_tried = false;
     bool gate_off = false;
     long long last_rows = 0;  // output size of the previous run: sizes the next buffer
+    std::map<int, long long> rows_by_items;  // output size of the last run over that many items (guarded by ranges_mu)
     long long last_surv = 0;  // survivors of the previous run: sizes the deferred-verification buffer
     double surv_rate = -1.0;  // survivors per work item in the previous run (-1: none yet)
     // item ranges that fit the survivor buffer in earlier runs, by the run's item count: a
