@@ -204,7 +204,9 @@ int rb_ctx_destroy(rb_ctx* c) {
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->ev_mid) cudaEventDestroy(c->ev_mid);
-    for (int k = 0; k < 3; k++) dev_free(c->pool[k], c->stream);
+    for (auto& e : c->pool)
+        for (int k = 0; k < 3; k++) dev_free(e.d[k], c->stream);
+    c->pool.clear();
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->host_ctr) cudaFreeHost(c->host_ctr);
     c->host_items.release();
@@ -1025,9 +1027,12 @@ int rb::merge_results(rb_ctx* c, rb_result* ra, rb_result* rbg, bool want_parts,
     int32_t** dst[4] = {&res->d_t, &res->d_s, &res->d_r, &res->d_p};
     int32_t* srca[4] = {ra->d_t, ra->d_s, ra->d_r, ra->d_p};
     int32_t* srcb[4] = {rbg->d_t, rbg->d_s, rbg->d_r, rbg->d_p};
+    long long pcap = 0;
+    const bool pooled = c->pool_take(res->cap, &res->d_t, &res->d_s, &res->d_r, &pcap);
+    if (pooled) res->cap = pcap;
     for (int q = 0; q < 4 && !e; q++) {
         if (q == 3 && !want_parts) break;
-        e = dev_alloc((void**)dst[q], sizeof(int32_t) * (size_t)res->cap, st);
+        if (!(pooled && q < 3)) e = dev_alloc((void**)dst[q], sizeof(int32_t) * (size_t)res->cap, st);
         if (!e && ra->count) e = cudaMemcpyAsync(*dst[q], srca[q], sizeof(int32_t) * ra->count, cudaMemcpyDeviceToDevice, st);
         if (!e && rbg->count)
             e = cudaMemcpyAsync(*dst[q] + ra->count, srcb[q], sizeof(int32_t) * rbg->count, cudaMemcpyDeviceToDevice, st);
@@ -1406,13 +1411,7 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
         // larger buffer (up to SURV_LIMIT) or split in half, so any survivor
         // volume streams through a bounded buffer; the output buffer grows
         // (keeping its rows) before a verify that could overflow it.
-        if (c->pool[0] && c->pool_cap >= cap && !env_out) {
-            res->d_t = c->pool[0];
-            res->d_s = c->pool[1];
-            res->d_r = c->pool[2];
-            cap = c->pool_cap;
-            c->pool[0] = c->pool[1] = c->pool[2] = nullptr;
-            c->pool_cap = 0;
+        if (!env_out && c->pool_take(cap, &res->d_t, &res->d_s, &res->d_r, &cap)) {
         } else {
             cudaError_t e = dev_alloc((void**)&res->d_t, sizeof(int32_t) * cap, c->stream);
             if (!e) e = dev_alloc((void**)&res->d_s, sizeof(int32_t) * cap, c->stream);
@@ -1635,13 +1634,7 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
     // decided inside the pair kernel; an output overflow re-runs once with
     // the exact size
     for (int attempt = 0;; attempt++) {
-        if (c->pool[0] && c->pool_cap >= cap) {  // reuse the pooled buffers
-            res->d_t = c->pool[0];
-            res->d_s = c->pool[1];
-            res->d_r = c->pool[2];
-            cap = c->pool_cap;
-            c->pool[0] = c->pool[1] = c->pool[2] = nullptr;
-            c->pool_cap = 0;
+        if (c->pool_take(cap, &res->d_t, &res->d_s, &res->d_r, &cap)) {  // reuse cached buffers
         } else {
             res->d_t = res->d_s = res->d_r = nullptr;
             cudaError_t e = dev_alloc((void**)&res->d_t, sizeof(int32_t) * cap, c->stream);
@@ -1807,12 +1800,8 @@ int rb_result_destroy(rb_result* r) {
     rb_ctx* c = r->ctx;
     std::unique_lock<std::mutex> lock;
     if (c) lock = std::unique_lock<std::mutex>(c->mu);  // the pool is context state
-    if (c && r->d_t && r->cap > c->pool_cap) {  // keep the larger buffers for the next run
-        for (int k = 0; k < 3; k++) dev_free(c->pool[k], r->stream);
-        c->pool[0] = r->d_t;
-        c->pool[1] = r->d_s;
-        c->pool[2] = r->d_r;
-        c->pool_cap = r->cap;
+    if (c && r->d_t && r->d_s && r->d_r && r->cap > 0) {  // the rows' buffers go back to the context cache
+        c->pool_give(r->d_t, r->d_s, r->d_r, r->cap, r->stream);
         r->d_t = r->d_s = r->d_r = nullptr;
     }
     dev_free(r->d_t, r->stream);

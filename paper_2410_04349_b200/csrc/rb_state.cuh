@@ -136,9 +136,38 @@ struct rb_ctx {
     // rows -- grown once and reused, so a step allocates nothing from the pool
     DevBuf col_k0, col_k1, col_flag, col_temp, col_r1, col_r2, col_cnt, col_out[3];
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr;
-    // output buffers of the last destroyed result, reused by the next run
-    int32_t* pool[3] = {nullptr, nullptr, nullptr};
-    long long pool_cap = 0;
+    // output row buffers (t, s, rule) of destroyed results, reused best-fit by
+    // later runs, merges and collects (at most 4 triples, the largest kept):
+    // a step allocates no multi-GB buffers once the cache is warm
+    struct PoolEntry {
+        int32_t* d[3];
+        long long cap;
+    };
+    std::vector<PoolEntry> pool;
+    // the smallest cached triple holding `need` rows (removed from the cache), or false
+    bool pool_take(long long need, int32_t** t, int32_t** s, int32_t** r, long long* cap) {
+        int best = -1;
+        for (size_t k = 0; k < pool.size(); k++)
+            if (pool[k].cap >= need && (best < 0 || pool[k].cap < pool[(size_t)best].cap)) best = (int)k;
+        if (best < 0) return false;
+        *t = pool[(size_t)best].d[0];
+        *s = pool[(size_t)best].d[1];
+        *r = pool[(size_t)best].d[2];
+        *cap = pool[(size_t)best].cap;
+        pool.erase(pool.begin() + best);
+        return true;
+    }
+    // cache a triple; the smallest is freed when more than 4 are held
+    void pool_give(int32_t* t, int32_t* s, int32_t* r, long long cap, cudaStream_t st) {
+        pool.push_back(PoolEntry{{t, s, r}, cap});
+        if (pool.size() > 4) {
+            size_t small = 0;
+            for (size_t k = 1; k < pool.size(); k++)
+                if (pool[k].cap < pool[small].cap) small = k;
+            for (int q = 0; q < 3; q++) dev_free(pool[small].d[q], st);
+            pool.erase(pool.begin() + (long)small);
+        }
+    }
     unsigned long long* host_ctr = nullptr;  // pinned: counters read back after each run
     PinnedVec<Item> host_items;              // the last run's work items
     PinnedVec<int32_t> host_offs;            // the last run's part starts / ends (packed items)
