@@ -25,14 +25,39 @@ rep, wl, n, details = sys.argv[1], sys.argv[2], int(sys.argv[3]), sys.argv[4]
 pairs = int(sys.argv[5]) if len(sys.argv) > 5 else None
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-h, units, v = rows[0], rows[1], rows[2]
-m = {k: {"value": v[i], "unit": units[i]} for i, k in enumerate(h) if k.startswith(KEEP_PREFIX)}
+h, units, kernels = rows[0], rows[1], [r for r in rows[2:] if len(r) == len(rows[0])]
+
+
+def num(x):
+    try:
+        return float(str(x).replace(",", ""))
+    except ValueError:
+        return None
+
+
+# several captured launches (e.g. the two size classes / plans of one step):
+# durations and counts add up, utilisations are duration-weighted means
+it = h.index("gpu__time_duration.sum")
+dur = [num(r[it]) or 0.0 for r in kernels]
+m = {}
+for i, k in enumerate(h):
+    if not k.startswith(KEEP_PREFIX):
+        continue
+    vals = [num(r[i]) for r in kernels]
+    if len(kernels) == 1 or any(x is None for x in vals):
+        m[k] = {"value": kernels[0][i], "unit": units[i]}
+    elif k.endswith(".sum") and "pct" not in k and "per_second" not in k:
+        m[k] = {"value": repr(sum(vals)), "unit": units[i]}
+    else:
+        m[k] = {"value": repr(sum(x * d for x, d in zip(vals, dur)) / max(sum(dur), 1e-30)), "unit": units[i]}
 tb = sum(float(m[k]["value"].replace(",", "")) * SCALE[m[k]["unit"]]
          for k in ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in m)
+v = kernels[0]
 sha = hashlib.sha1(open(os.path.join(ROOT, "paper_2410_04349_b200", "csrc", "rb_device.cuh"), "rb").read()).hexdigest()[:12]
 path = os.path.join(ROOT, "profiles", "traffic.json")
 doc = json.load(open(path)) if os.path.exists(path) else {}
-doc[wl] = {"n": n, "capture": details, "kernel": v[h.index("Kernel Name")] if "Kernel Name" in h else "",
+doc[wl] = {"n": n, "capture": details, "launches": len(kernels),
+           "kernel": v[h.index("Kernel Name")] if "Kernel Name" in h else "",
            "kernel_sha": sha, "pairs": pairs, "bytes_per_launch": tb, "metrics": m}
 json.dump(doc, open(path, "w"), indent=1)
 print(wl, tb, len(m), "metrics kept")
