@@ -255,13 +255,20 @@ def roofline(w_name, n, pairs_step, kernel_ms, clocks, bytes_per_pair=None, term
     live_mhz = (clocks or {}).get("sm_mhz") or cap_mhz or 1965.0
     if cap_mhz is None:
         cap_mhz = live_mhz
+    # launches of the same step the capture timed but could not replay (a
+    # second, small launch): their share of the live pair-kernel time is
+    # taken off, so the captured launch is compared with its own live time
+    other_ns = float(entry.get("other_time") or 0.0) * {"s": 1e9, "second": 1e9, "msecond": 1e6, "ms": 1e6,
+                                                         "usecond": 1e3, "us": 1e3}.get(entry.get("time_unit", ""), 1.0)
+    live_ms = kernel_ms * (cap_ns / (cap_ns + other_ns)) if cap_ns and other_ns else kernel_ms
     # the capture's busy cycles on the pipe, replayed in this run's cycles
-    frac = have[bind] * (cap_ns * 1e-6 * cap_mhz) / (kernel_ms * live_mhz) if cap_ns else have[bind]
+    frac = have[bind] * (cap_ns * 1e-6 * cap_mhz) / (live_ms * live_mhz) if cap_ns else have[bind]
     peak = PIPE_RATE[bind] * SM_COUNT * live_mhz * 1e6
     out.update(bound=bind.lower(), frac=frac, peak=peak, achieved=frac * peak,
                traffic=entry.get("bytes_per_launch"),
                capture=entry.get("capture"), capture_frac=have[bind], capture_pipes=have,
                capture_ms=cap_ns * 1e-6 if cap_ns else None, capture_sm_mhz=cap_mhz,
+               capture_unreplayed_ms=other_ns * 1e-6, live_ms_of_captured=live_ms,
                capture_kernel_sha=entry.get("kernel_sha"), kernel_sha=kernel_source_sha(),
                capture_current=entry.get("kernel_sha") == kernel_source_sha(),
                issue_active=val.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0) / 100.0,

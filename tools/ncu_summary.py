@@ -38,6 +38,12 @@ def num(x):
 # several captured launches (e.g. the two size classes / plans of one step):
 # durations and counts add up, utilisations are duration-weighted means
 it = h.index("gpu__time_duration.sum")
+ia = h.index("smsp__inst_executed.sum")
+# a launch ncu could time but not replay reports nan metrics: only its
+# duration is kept (other_time), the metrics come from the replayed launches
+other = [r for r in kernels if num(r[ia]) is None or num(r[ia]) != num(r[ia])]
+other_time = sum(num(r[it]) or 0.0 for r in other)
+kernels = [r for r in kernels if r not in other] or kernels
 dur = [num(r[it]) or 0.0 for r in kernels]
 m = {}
 for i, k in enumerate(h):
@@ -56,7 +62,8 @@ v = kernels[0]
 sha = hashlib.sha1(open(os.path.join(ROOT, "paper_2410_04349_b200", "csrc", "rb_device.cuh"), "rb").read()).hexdigest()[:12]
 path = os.path.join(ROOT, "profiles", "traffic.json")
 doc = json.load(open(path)) if os.path.exists(path) else {}
-doc[wl] = {"n": n, "capture": details, "launches": len(kernels),
+doc[wl] = {"n": n, "capture": details, "launches": len(kernels), "other_launches": len(other),
+           "other_time": other_time, "time_unit": units[it],
            "kernel": v[h.index("Kernel Name")] if "Kernel Name" in h else "",
            "kernel_sha": sha, "pairs": pairs, "bytes_per_launch": tb, "metrics": m}
 json.dump(doc, open(path, "w"), indent=1)
