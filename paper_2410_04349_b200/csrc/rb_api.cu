@@ -127,6 +127,23 @@ void rb::choose_gate(FilterPlan& F, const std::vector<uint64_t>& need, const std
     }
     F.gate = covered_all && F.n_rules > 0 ? 1 : 0;
     for (int f = 0; f < F.n_eq; f++) F.eq_stage2[f] = F.gate && !eq_chosen[f] && F.eq_kill[f];
+    // a regated plan's remaining stage-1 keys are other attributes than the
+    // unit's own key: sparse, so OR them first (FilterPlan::eq_any)
+    F.eq_any = 0;
+    F.eq_free = F.all_rules;
+    if (implied && !std::getenv("RB_EQ_ANY_OFF")) {
+        int n1 = 0;
+        uint64_t killed = 0;
+        for (int f = 0; f < F.n_eq; f++)
+            if (!F.eq_stage2[f] && F.eq_kill[f]) {
+                n1++;
+                killed |= F.eq_kill[f];
+            }
+        if (n1 >= 2) {
+            F.eq_any = 1;
+            F.eq_free = F.all_rules & ~killed;
+        }
+    }
     for (int f = 0; f < F.n_tok; f++)
         for (int z = 0; z < F.tok_nslots[f]; z++) F.tok_slot[f][z].stage2 = F.gate && F.tok_always[f] && !tok_chosen[f][z];
     // Even with nothing deferred the gate pays when stage 1 is selective:

@@ -139,6 +139,13 @@ struct FilterPlan {
     // Stage-1 gate: a few selective tests whose (implied) kills cover every
     // rule run first; a warp with no live pair left skips all other tests.
     int32_t gate;
+    // eq_any: the stage-1 equality keys are sparse (a regated plan: the unit's
+    // own key is implied, the rest rarely match), so a pair first ORs their
+    // compares; with no key equal its rules drop to eq_free (the rules no
+    // stage-1 key kills) in one step, and the per-key kills run only behind a
+    // warp vote when some lane's row matched a key
+    int32_t eq_any;
+    uint64_t eq_free;
     const uint8_t* const_mask[MAX_CONST];
     uint64_t const_kill[MAX_CONST];
     const int64_t* tok_ooff[MAX_TOK];
@@ -703,6 +710,9 @@ struct __align__(16) Tile {
 #define RB_TOK_KILL(f, z) ((f) == 0 ? RB_PICK4(z, SPEC_TOK0_KILL_) : RB_PICK4(z, SPEC_TOK1_KILL_))
 #define RB_STR_KILL(f, z) ((f) == 0 ? RB_PICK4(z, SPEC_STR0_KILL_) : RB_PICK4(z, SPEC_STR1_KILL_))
 #define RB_GATE SPEC_GATE
+#ifndef SPEC_EQ_ANY
+#define SPEC_EQ_ANY 0
+#endif
 #define RB_EQ_STAGE2(f) RB_PICK6(f, SPEC_EQ_STAGE2_)
 #define RB_TOK_STAGE2(f, z) ((f) == 0 ? RB_PICK4(z, SPEC_TOK0_STAGE2_) : RB_PICK4(z, SPEC_TOK1_STAGE2_))
 // edit tables' shared-memory offsets as immediates: the lookup is one LEA + LDS [R + imm]
@@ -1041,10 +1051,36 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
 #else
             alive[r] = AllValid ? base : m_gate(jj >= o[r].jj_lo && jj != o[r].jj_skip, base);
 #endif
+#if defined(RB_SPEC) && SPEC_EQ_ANY
+        }
+        {
+            bool hit[ROWS];
+            bool any_hit = false;
+#pragma unroll
+            for (int r = 0; r < ROWS; r++) {
+                hit[r] = false;
+#pragma unroll
+                for (int f = 0; f < MAX_EQ; f++)
+                    if (f < RB_NEQ && !RB_EQ_STAGE2(f) && RB_EQ_KILL(f)) hit[r] |= o[r].ocode[f] == T.r[jj].head[f];
+                m_kill(alive[r], !hit[r], ~(uint64_t)SPEC_EQ_FREE);
+                any_hit |= hit[r];
+            }
+            if (__any_sync(FULL, any_hit)) {
+#pragma unroll
+                for (int r = 0; r < ROWS; r++) {
+#pragma unroll
+                    for (int f = 0; f < MAX_EQ; f++)
+                        if (f < RB_NEQ && !RB_EQ_STAGE2(f) && RB_EQ_KILL(f))
+                            m_kill(alive[r], hit[r] && o[r].ocode[f] != T.r[jj].head[f], RB_EQ_KILL(f));
+                }
+            }
+        }
+#else
 #pragma unroll
             for (int f = 0; f < MAX_EQ; f++)
                 if (f < RB_NEQ && !RB_EQ_STAGE2(f)) m_kill(alive[r], o[r].ocode[f] != T.r[jj].head[f], RB_EQ_KILL(f));
         }
+#endif
         // token tests kept for stage 2 (always-evaluated features only)
         int u_keep[ROWS][MAX_TOK];
         int need_keep[ROWS][MAX_TOK][4];
