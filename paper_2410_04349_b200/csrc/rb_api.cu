@@ -131,7 +131,8 @@ void rb::choose_gate(FilterPlan& F, const std::vector<uint64_t>& need, const std
     // unit's own key: sparse, so OR them first (FilterPlan::eq_any)
     F.eq_any = 0;
     F.eq_free = F.all_rules;
-    if (implied && !std::getenv("RB_EQ_ANY_OFF")) {
+    const char* eq_any_off = std::getenv("RB_EQ_ANY_OFF");
+    if (implied && !(eq_any_off && std::atoi(eq_any_off) != 0)) {
         int n1 = 0;
         uint64_t killed = 0;
         for (int f = 0; f < F.n_eq; f++)
