@@ -152,7 +152,8 @@ def test_implied_root_regating_keeps_the_candidate_set(n, monkeypatch):
     cfg = PipelineConfig(max_partition_size=4096 if n > 50_000 else 512, enable_pulls=True,
                          single_partition_threshold=0)
     out = []
-    for off in ("1", None):
+    for off, eq_any in (("1", "0"), (None, "0"), (None, "1")):
+        monkeypatch.setenv("RB_EQ_ANY", eq_any)  # the OR-first equality stage of the regated plan (opt-in)
         if off:
             monkeypatch.setenv("RB_IMPLIED_OFF", off)
         else:
@@ -160,8 +161,9 @@ def test_implied_root_regating_keeps_the_candidate_set(n, monkeypatch):
         res = run_pipeline_encoded(w.enc, w.path, cfg, EngineConfig(), code_cols=cols, branch_ids=bids)
         out.append((res.candidates.arrays, res.candidates.stats.total_comparisons()))
         res.parts.close()
-    (a, ca), (b, cb) = out
-    assert ca == cb
-    for x, y in zip(a, b):
-        assert np.array_equal(x, y)
+    (a, ca) = out[0]
+    for b, cb in out[1:]:
+        assert ca == cb
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
     assert len(a[0]) > 0
