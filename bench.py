@@ -425,12 +425,20 @@ class BlocksJob(Job):
         np.cumsum([len(r) for r, _ in mine], out=self.b_offs[1:])
         self.b_splits = np.array([sp for _, sp in mine], dtype=np.int64)
         self.out = None
+        # blocks keyed on an attribute's value: its equality holds for every pair
+        # (rb_run_batch_implied regates the filter plan without that slot)
+        self.implied = 0
+        if getattr(w, "block_attr", None):
+            for k, p in enumerate(w.path.predicate_table):
+                if p.comparator == "eq" and p.lhs_attr == w.block_attr and p.rhs_attr == w.block_attr:
+                    self.implied |= 1 << k
 
     def step(self):
         from paper_2410_04349_b200._lib import RB_SYMMETRIC
 
         t0 = time.perf_counter()
-        (t, s, r, p), st = self.prog.run_batch(self.b_refs, self.b_offs, self.b_splits, RB_SYMMETRIC, out=self.out)
+        (t, s, r, p), st = self.prog.run_batch(self.b_refs, self.b_offs, self.b_splits, RB_SYMMETRIC, out=self.out,
+                                               implied=self.implied)
         if self.out is None:  # later steps copy the rows into reusable pinned buffers
             import torch
 

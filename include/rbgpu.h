@@ -161,6 +161,15 @@ int rb_run_cross(rb_ctx* ctx, rb_rel* rel, rb_prog* prog, const int32_t* left, i
 int rb_run_batch(rb_ctx* ctx, rb_rel* rel, rb_prog* prog, const int32_t* refs, const int64_t* offsets,
                  const int64_t* splits, int32_t n_parts, uint32_t flags, rb_result** out);
 
+/* rb_run_batch where the caller knows path slots that hold for every pair of
+ * every part (bit s of implied_slots: e.g. the equality root every block of
+ * a blocked run shares): the batch runs a filter plan regated without them
+ * (their tests cannot fail there).  The filter only prunes, so results are
+ * exact even if an implied slot were false for some pair. */
+int rb_run_batch_implied(rb_ctx* ctx, rb_rel* rel, rb_prog* prog, const int32_t* refs, const int64_t* offsets,
+                         const int64_t* splits, int32_t n_parts, uint32_t flags, uint64_t implied_slots,
+                         rb_result** out);
+
 int rb_result_count(const rb_result* res, int64_t* rows);
 int rb_result_copy(const rb_result* res, int32_t* t, int32_t* s, int32_t* rule);
 int rb_result_copy_parts(const rb_result* res, int32_t* part);

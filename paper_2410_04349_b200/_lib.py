@@ -77,6 +77,8 @@ _SIGNATURES = {
         [c_vp, c_vp, c_vp, c_vp, ctypes.c_int64, c_vp, ctypes.c_int64, ctypes.c_uint32, c_vpp],
     ),
     "rb_run_batch": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int32, ctypes.c_uint32, c_vpp]),
+    "rb_run_batch_implied": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int32, ctypes.c_uint32,
+                                            ctypes.c_uint64, c_vpp]),
     "rb_result_count": (ctypes.c_int, [c_vp, c_i64p]),
     "rb_result_copy_parts": (ctypes.c_int, [c_vp, c_vp]),
     "rb_result_copy": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),

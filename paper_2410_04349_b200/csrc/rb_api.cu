@@ -1757,7 +1757,15 @@ int rb_run_cross(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* left, int64_
 
 int rb_run_batch(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, const int64_t* offsets,
                  const int64_t* splits, int32_t n_parts, uint32_t flags, rb_result** out) {
+    return rb_run_batch_implied(c, rel, P, refs, offsets, splits, n_parts, flags, 0, out);
+}
+
+int rb_run_batch_implied(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, const int64_t* offsets,
+                         const int64_t* splits, int32_t n_parts, uint32_t flags, uint64_t implied_slots,
+                         rb_result** out) {
     if (n_parts < 0 || (n_parts && (!offsets || !refs))) return fail(RB_ERR_INVALID, "rb_run_batch: bad arguments");
+    if (P && implied_slots >> std::min(63, P->n_slots) && P->n_slots < 64)
+        return fail(RB_ERR_INVALID, "rb_run_batch_implied: implied slots beyond the program's %d", P->n_slots);
     std::vector<Part> parts;
     parts.reserve(n_parts);
     if (n_parts && offsets[0] != 0) return fail(RB_ERR_INVALID, "rb_run_batch: offsets[0] must be 0");
@@ -1769,7 +1777,9 @@ int rb_run_batch(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, const 
         parts.push_back(Part{offsets[k], len, sp, sp >= 0 ? offsets[k] + sp : 0});
     }
     const int64_t total = n_parts ? offsets[n_parts] : 0;
-    return run_mixed(c, rel, P, refs, total, parts, flags, true, out);
+    const char* off = std::getenv("RB_IMPLIED_OFF");
+    if (off && std::atoi(off) != 0) implied_slots = 0;
+    return run_mixed(c, rel, P, refs, total, parts, flags, true, out, false, implied_slots);
 }
 
 int rb_result_copy_parts(const rb_result* r, int32_t* part) {

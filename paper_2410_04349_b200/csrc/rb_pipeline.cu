@@ -649,7 +649,8 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
     // implied (rb::choose_gate), the other units as usual, one merged result.
     int64_t best = 0;
     int32_t best_b = -1;
-    if (!parts->root_slot.empty() && !std::getenv("RB_IMPLIED_OFF")) {
+    const char* implied_off = std::getenv("RB_IMPLIED_OFF");
+    if (!parts->root_slot.empty() && !(implied_off && std::atoi(implied_off) != 0)) {
         std::vector<int64_t> by_b(parts->branch_ids.size(), 0);
         int64_t all = 0;
         for (size_t q = 0; q < sel.size(); q++) {

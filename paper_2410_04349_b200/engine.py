@@ -317,18 +317,19 @@ class PathProgram:
 
     # -- raw runs ---------------------------------------------------------
 
-    def run_batch(self, refs, offsets, splits, flags: int, out=None):
+    def run_batch(self, refs, offsets, splits, flags: int, out=None, implied: int = 0):
         """One launch over many partitions / cross blocks laid out back to
         back (rb_run_batch).  Returns ((t, s, rule, part) int32 arrays, rb_stats).
         ``out``: optional (t, s, rule, part) int32 host arrays the rows are
-        copied into when they fit (see run_raw)."""
+        copied into when they fit (see run_raw).  ``implied``: a bit mask of
+        path slots every pair of every part holds (rb_run_batch_implied)."""
         L = lib()
         res = _lib.c_vp()
         refs_a = i32(refs)
         offs = np.ascontiguousarray(offsets, dtype=np.int64)
         spl = None if splits is None else np.ascontiguousarray(splits, dtype=np.int64)
-        check(L.rb_run_batch(self.ctx.handle, self.drel.handle, self.handle, ptr(refs_a), ptr(offs), ptr(spl),
-                             len(offs) - 1, flags, _lib.ctypes.byref(res)))
+        check(L.rb_run_batch_implied(self.ctx.handle, self.drel.handle, self.handle, ptr(refs_a), ptr(offs), ptr(spl),
+                                     len(offs) - 1, flags, int(implied), _lib.ctypes.byref(res)))
         try:
             cnt = _lib.ctypes.c_int64(0)
             check(L.rb_result_count(res, _lib.ctypes.byref(cnt)))
@@ -677,7 +678,28 @@ def run_partition_rows(partition, relation, path, row_lo: int, row_hi: int, cfg=
     return _candidates(prog, rows, st, cfg, max(0, row_hi - row_lo), time.perf_counter() - started)
 
 
-def _batch(prog: PathProgram, blocks, cfg: EngineConfig):
+def implied_slots_of(path, partitions) -> int:
+    """The path slots every pair of these partitions holds: the equality root
+    of the branch they were keyed on (DataPartition.branch_id, partitioning.py:
+    93-131), when they all share it and none is the missing-value group
+    (their key_group is known and is not the missing key).  0 otherwise."""
+    bids = {getattr(p, "branch_id", None) for p in partitions}
+    if len(bids) != 1:
+        return 0
+    b = bids.pop()
+    roots = list(getattr(path, "root_slots", ()))
+    if not isinstance(b, int) or not 0 <= b < len(roots):
+        return 0
+    s = roots[b]
+    pred = path.predicate_table[s]
+    if pred.comparator != "eq" or pred.is_cross_attr or pred.rhs_attr is None:
+        return 0
+    if any(getattr(p, "key_group", None) in (None, "\x00missing") for p in partitions):
+        return 0
+    return 1 << int(s)
+
+
+def _batch(prog: PathProgram, blocks, cfg: EngineConfig, implied: int = 0):
     """blocks: list of (refs int32 array, split or -1).  One launch; returns
     one CandidateSet per block."""
     started = time.perf_counter()
@@ -686,7 +708,7 @@ def _batch(prog: PathProgram, blocks, cfg: EngineConfig):
     np.cumsum(sizes, out=offsets[1:])
     refs = np.concatenate([r for r, _ in blocks]) if blocks else np.zeros(0, np.int32)
     splits = np.array([sp for _, sp in blocks], dtype=np.int64)
-    (t, s, r, p), st = prog.run_batch(refs, offsets, splits, cfg.flags())
+    (t, s, r, p), st = prog.run_batch(refs, offsets, splits, cfg.flags(), implied=implied)
     wall = time.perf_counter() - started
     order = np.argsort(p, kind="stable")
     t, s, r, p = t[order], s[order], r[order], p[order]
@@ -719,7 +741,8 @@ def run_partitions(partitions, relation, path, cfg=None, reg=None, encoded=None,
     cfg = EngineConfig.of(cfg)
     live = [p for p in partitions if p is not None and len(p.tuple_refs)]
     prog = _program_for(path, relation, reg, encoded, program)
-    res = iter(_batch(prog, [(_refs_array(p), -1) for p in live], cfg)) if live else iter(())
+    res = iter(_batch(prog, [(_refs_array(p), -1) for p in live], cfg, implied_slots_of(path, live))) if live \
+        else iter(())
     return [next(res) if (p is not None and len(p.tuple_refs)) else CandidateSet(pairs=[]) for p in partitions]
 
 
@@ -735,7 +758,7 @@ def run_crosses(pairs, relation, path, cfg=None, reg=None, encoded=None, program
         if len(np.unique(both)) != len(both):
             raise SchemaError("partition -1 has duplicate tuple refs")
         blocks.append((both, len(lr)))
-    return _batch(prog, blocks, cfg)
+    return _batch(prog, blocks, cfg, implied_slots_of(path, [p for pair in pairs for p in pair]))
 
 
 def run_cross(left, right, relation, path, cfg=None, reg=None, encoded=None, program=None) -> CandidateSet:

@@ -54,6 +54,7 @@ class Workload:
     n: int
     blocks: object = None  # [(refs int32, split)]: cross blocks / partitions instead of one partition
     injected: object = None  # (a, b) int arrays: the generator's duplicate pairs (recall checks)
+    block_attr: object = None  # blocks keyed on this attribute's value (its equality holds inside every block)
 
     def pairs(self, symmetric: bool = True) -> int:
         if self.blocks is None:
@@ -353,7 +354,7 @@ def linkage(n: int = 1_000_000, seed: int = 5, zipf_s: float = 1.3, n_blocks: in
 
     rules = parse_ruleset(json.dumps(LINKAGE_RULES))
     path = data_aware_plan(enc, rules, sample=plan_sample, seed=seed)
-    return Workload("linkage", enc, rules, path, n, blocks=blocks, injected=(src, dup))
+    return Workload("linkage", enc, rules, path, n, blocks=blocks, injected=(src, dup), block_attr="block")
 
 
 PERSON5_RULES = [

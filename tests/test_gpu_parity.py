@@ -244,3 +244,41 @@ def test_learned_shape_replays_without_retries(monkeypatch):
     assert sorted(zip(*rows1)) == sorted(zip(*rows2))
     assert st1.survivors > 64
     assert st2.retries == 0
+
+
+def test_run_crosses_with_implied_root_equal_plain(monkeypatch):
+    """Cross blocks keyed on an equality root (config 5's shape): the batch
+    runs regated with the root implied (engine.implied_slots_of ->
+    rb_run_batch_implied); rows equal the plain plan's and the per-block runs."""
+    from paper_2410_04349_b200 import run_crosses, synth
+    from paper_2410_04349_b200.engine import PathProgram, implied_slots_of
+
+    w = synth.linkage(60_000, seed=5)
+    blk = w.enc.columns[w.enc.get(("codes", "block"))].data
+    bslot = [k for k, p in enumerate(w.path.predicate_table) if p.comparator == "eq" and p.lhs_attr == "block"]
+    assert bslot
+    prog = PathProgram(w.path, w.enc)
+    big = sorted(w.blocks, key=lambda b: -len(b[0]))[:40]
+    from paper_2410_04349_b200._lib import RB_SYMMETRIC
+    refs = np.concatenate([r for r, _ in big]).astype(np.int32)
+    offs = np.zeros(len(big) + 1, dtype=np.int64)
+    np.cumsum([len(r) for r, _ in big], out=offs[1:])
+    splits = np.array([sp for _, sp in big], dtype=np.int64)
+    plain, st0 = prog.run_batch(refs, offs, splits, RB_SYMMETRIC)
+    imp, st1 = prog.run_batch(refs, offs, splits, RB_SYMMETRIC, implied=1 << bslot[0])
+    assert st0.comparisons == st1.comparisons
+    assert sorted(zip(*plain)) == sorted(zip(*imp))
+    assert all(len(np.unique(blk[r])) == 1 for r, _ in big)  # every block shares its key
+    # the Python API derives the implied slot from DataPartition.branch_id / key_group
+    from paper_2410_04349_b200 import DataPartition
+    path = w.path
+    b = list(path.root_slots).index(bslot[0]) if bslot[0] in path.root_slots else None
+    if b is not None:
+        pairs = [(DataPartition(2 * k, tuple(r[:sp].tolist()), branch_id=b, key_group=f"v:{k}"),
+                  DataPartition(2 * k + 1, tuple(r[sp:].tolist()), branch_id=b, key_group=f"v:{k}"))
+                 for k, (r, sp) in enumerate(big)]
+        assert implied_slots_of(path, [p for pr in pairs for p in pr]) == 1 << bslot[0]
+        got = run_crosses(pairs, None, path, program=prog)
+        for (r, sp), cs in zip(big, got):
+            want = prog.run_raw(r, len(r), RB_SYMMETRIC, split=sp)[0]
+            assert sorted(cs.pairs) == sorted((int(a), int(c), path.rule_ids[int(d)]) for a, c, d in zip(*want))
