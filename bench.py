@@ -551,7 +551,9 @@ def units_parity(job, units, budget, cores):
     refs = np.concatenate([r for r, _ in sub]).astype(np.int32)
     offs = np.zeros(len(sub) + 1, dtype=np.int64)
     np.cumsum([len(r) for r, _ in sub], out=offs[1:])
-    (gt, gs, gr, gp), _ = prog.run_batch(refs, offs, np.array([sp for _, sp in sub], dtype=np.int64), RB_SYMMETRIC)
+    # the same regating as the timed run (blocks keyed on an equality root)
+    (gt, gs, gr, gp), _ = prog.run_batch(refs, offs, np.array([sp for _, sp in sub], dtype=np.int64), RB_SYMMETRIC,
+                                         implied=getattr(job, "implied", 0))
     got = sorted(zip(gp.tolist(), gt.tolist(), gs.tolist(), gr.tolist()))
     want, cmp_total = [], 0
     evals = np.zeros(prog.n_slots, dtype=np.int64)
