@@ -21,6 +21,7 @@
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
+#include <chrono>
 #include <numeric>
 #include <queue>
 
@@ -50,6 +51,10 @@ struct rb_parts {
 namespace {
 
 constexpr int PB = 256;  // threads per block of the streaming kernels
+
+double host_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 int grid_for(int64_t n, int sms) {
     const int64_t g = (n + PB - 1) / PB;
@@ -416,9 +421,13 @@ int partition_impl(rb_ctx* c, rb_rel* rel, const int32_t* cols, const int64_t* k
             }
             if (cudaError_t e = cudaGetLastError()) return bail(fail(RB_ERR_CUDA, "partition keys: %s", cudaGetErrorString(e)));
             const size_t before = sib_ranges.size();
+            static const bool timing = std::getenv("RB_HOST_TIMING") != nullptr;
+            const double t0 = timing ? host_ms() : 0.0;
             if (int rc = partition_branch(P, key, tid, key_bits, (int64_t)b * n, bid, maxp, sibling_counter, sib_ranges,
                                           sib_first))
                 return bail(rc);
+            if (timing)
+                fprintf(stderr, "rb partition: branch %d: %.3f ms, %zu entries\n", bid, host_ms() - t0, P->parts.size());
             for (size_t g = before; g < sib_ranges.size(); g++) sib_branch.push_back(bid);
         }
     }
@@ -612,27 +621,51 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
             sel.push_back(k);
         }
     } else {
-        // static longest-processing-time placement on pair counts (the same on
-        // every rank): units in descending cost to the least-loaded rank
-        std::vector<int64_t> order(units);
-        std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-            return pair_count(parts->parts[(size_t)a], sym) > pair_count(parts->parts[(size_t)b], sym);
-        });
-        using L = std::pair<int64_t, int32_t>;  // (load, rank)
-        std::priority_queue<L, std::vector<L>, std::greater<L>> heap;
-        for (int32_t w = 0; w < world; w++) heap.push({0, w});
-        std::vector<uint8_t> take(parts->parts.size(), 0);
-        for (int64_t k : order) {
-            L top = heap.top();
-            heap.pop();
-            if (top.second == rank) take[(size_t)k] = 1;
-            top.first += pair_count(parts->parts[(size_t)k], sym);
-            heap.push(top);
+        // static placement on pair counts, the same on every rank, in O(n): the
+        // largest units (at most 4096 per rank) longest-processing-time first
+        // to the least-loaded rank, then the rest -- in entry order -- dealt as
+        // contiguous runs that fill every rank up to the mean load
+        // (water-filling over a prefix sum).  A full LPT sort of 1.6M units
+        // cost ~150 ms of host time per rank at 10M tuples.
+        const size_t nu = units.size();
+        std::vector<int64_t> cost(nu);
+        int64_t all = 0;
+        for (size_t q = 0; q < nu; q++) {
+            cost[q] = pair_count(parts->parts[(size_t)units[q]], sym);
+            all += cost[q];
         }
-        for (int64_t k : units)
-            if (take[(size_t)k]) {
-                mine.push_back(parts->parts[(size_t)k]);
-                sel.push_back(k);
+        const size_t kbig = std::min(nu, (size_t)4096 * (size_t)world);
+        std::vector<size_t> idx(nu);
+        std::iota(idx.begin(), idx.end(), 0);
+        if (kbig < nu)
+            std::nth_element(idx.begin(), idx.begin() + (long)kbig, idx.end(), [&](size_t a, size_t b) {
+                return cost[a] != cost[b] ? cost[a] > cost[b] : a < b;
+            });
+        std::sort(idx.begin(), idx.begin() + (long)kbig, [&](size_t a, size_t b) {
+            return cost[a] != cost[b] ? cost[a] > cost[b] : a < b;
+        });
+        std::vector<int32_t> owner(nu, -1);
+        std::vector<int64_t> load((size_t)world, 0);
+        for (size_t q = 0; q < kbig; q++) {
+            int32_t best = 0;
+            for (int32_t w = 1; w < world; w++)
+                if (load[(size_t)w] < load[(size_t)best]) best = w;
+            owner[idx[q]] = best;
+            load[(size_t)best] += cost[idx[q]];
+        }
+        // the rest in entry order: rank w takes the next run until it reaches the mean
+        const int64_t target = (all + world - 1) / world;
+        int32_t w = 0;
+        for (size_t q = 0; q < nu; q++) {
+            if (owner[q] >= 0) continue;
+            while (w < world - 1 && load[(size_t)w] >= target) w++;
+            owner[q] = w;
+            load[(size_t)w] += cost[q];
+        }
+        for (size_t q = 0; q < nu; q++)
+            if (owner[q] == rank) {
+                mine.push_back(parts->parts[(size_t)units[q]]);
+                sel.push_back(units[q]);
             }
     }
     std::vector<int> sel_bpos(sel.size(), -1);  // branch position of every unit
