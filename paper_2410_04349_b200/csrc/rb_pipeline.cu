@@ -301,10 +301,7 @@ int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, i
     CKS(cudaStreamSynchronize(st));
     std::vector<Deal> deals;
     int64_t extra = 0;  // sibling sub-partitions beyond one per group: pids of the single-tuple gaps follow
-    P->parts.reserve(P->parts.size() + (size_t)n_multi);
-    P->branch.reserve(P->branch.size() + (size_t)n_multi);
-    P->sibling.reserve(P->sibling.size() + (size_t)n_multi);
-    P->first_group.reserve(P->first_group.size() + (size_t)n_multi);
+
     for (int64_t g = 0; g < n_multi; g++) {
         const int64_t start = h_groups[g].y, m = h_groups[g].z;
         const uint8_t first = h_groups[g].x == 0;
