@@ -301,6 +301,14 @@ int partition_branch(rb_parts* P, const uint64_t* d_key_in, int32_t* d_tid_in, i
     CKS(cudaStreamSynchronize(st));
     std::vector<Deal> deals;
     int64_t extra = 0;  // sibling sub-partitions beyond one per group: pids of the single-tuple gaps follow
+    auto room = [&](auto& v) {  // geometric growth ahead of this branch's groups
+        const size_t need = v.size() + (size_t)n_multi;
+        if (v.capacity() < need) v.reserve(std::max(need, 2 * v.capacity()));
+    };
+    room(P->parts);
+    room(P->branch);
+    room(P->sibling);
+    room(P->first_group);
 
     for (int64_t g = 0; g < n_multi; g++) {
         const int64_t start = h_groups[g].y, m = h_groups[g].z;
