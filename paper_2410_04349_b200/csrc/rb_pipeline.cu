@@ -22,6 +22,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <chrono>
+#include <map>
 #include <numeric>
 #include <queue>
 
@@ -692,12 +693,21 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
             }
     }
     std::vector<int> sel_bpos(sel.size(), -1);  // branch position of every unit
-    for (size_t q = 0; q < sel.size(); q++)
-        for (size_t b = 0; b < parts->branch_ids.size(); b++)
-            if (parts->branch_ids[b] == parts->branch[(size_t)sel[q]]) {
-                sel_bpos[q] = (int)b;
-                break;
+    {
+        std::map<int32_t, int> pos_of;
+        for (size_t b = 0; b < parts->branch_ids.size(); b++) pos_of.emplace(parts->branch_ids[b], (int)b);
+        int32_t last_id = INT32_MIN;
+        int last_pos = -1;
+        for (size_t q = 0; q < sel.size(); q++) {
+            const int32_t id = parts->branch[(size_t)sel[q]];
+            if (id != last_id) {  // units come branch by branch
+                auto it = pos_of.find(id);
+                last_pos = it == pos_of.end() ? -1 : it->second;
+                last_id = id;
             }
+            sel_bpos[q] = last_pos;
+        }
+    }
     const int64_t total = (int64_t)parts->n_branches * parts->n;
     // Units of a branch keyed on an equality root hold that slot for all their
     // pairs (except the first key group, which may be the missing-value
