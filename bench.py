@@ -428,32 +428,48 @@ class BlocksJob(Job):
                 j = int(np.argmin(load))
                 owner[k] = j
                 load[j] += cost[k]
-        mine = [w.blocks[k] for k in np.flatnonzero(owner == self.rank)]
-        self.b_refs = pin_array(np.concatenate([r for r, _ in mine]).astype(np.int32)) if mine else np.zeros(0, np.int32)
-        self.b_offs = np.zeros(len(mine) + 1, dtype=np.int64)
-        np.cumsum([len(r) for r, _ in mine], out=self.b_offs[1:])
-        self.b_splits = np.array([sp for _, sp in mine], dtype=np.int64)
-        self.out = None
+        sel = np.flatnonzero(owner == self.rank)
         # blocks keyed on an attribute's value: its equality holds for every pair
-        # (rb_run_batch_implied regates the filter plan without that slot)
-        self.implied = 0
+        # (rb_run_batch_implied regates the filter plan without that slot); blocks
+        # from several branches (w.block_implied) run one batch per branch
+        implied_all = 0
         if getattr(w, "block_attr", None):
             for k, p in enumerate(w.path.predicate_table):
                 if p.comparator == "eq" and p.lhs_attr == w.block_attr and p.rhs_attr == w.block_attr:
-                    self.implied |= 1 << k
+                    implied_all |= 1 << k
+        per_block = getattr(w, "block_implied", None)
+        masks = np.array([per_block[k] if per_block is not None else implied_all for k in sel], dtype=np.int64)
+        self.batches = []
+        for m in sorted(set(masks.tolist())):
+            mine = [w.blocks[k] for k in sel[masks == m]]
+            refs = pin_array(np.concatenate([r for r, _ in mine]).astype(np.int32)) if mine else np.zeros(0, np.int32)
+            offs = np.zeros(len(mine) + 1, dtype=np.int64)
+            np.cumsum([len(r) for r, _ in mine], out=offs[1:])
+            self.batches.append([refs, offs, np.array([sp for _, sp in mine], dtype=np.int64), int(m), None])
+        self.implied = implied_all
 
     def step(self):
+        from types import SimpleNamespace
+
         from paper_2410_04349_b200._lib import RB_SYMMETRIC
 
         t0 = time.perf_counter()
-        (t, s, r, p), st = self.prog.run_batch(self.b_refs, self.b_offs, self.b_splits, RB_SYMMETRIC, out=self.out,
-                                               implied=self.implied)
-        if self.out is None:  # later steps copy the rows into reusable pinned buffers
-            import torch
+        rows, stats = [], []
+        for b in self.batches:
+            (t, s, r, p), st = self.prog.run_batch(b[0], b[1], b[2], RB_SYMMETRIC, out=b[4], implied=b[3])
+            if b[4] is None:  # later steps copy the rows into reusable pinned buffers
+                import torch
 
-            self.out = tuple(torch.empty(max(1, len(t)), dtype=torch.int32, pin_memory=True).numpy() for _ in range(4))
+                b[4] = tuple(torch.empty(max(1, len(t)), dtype=torch.int32, pin_memory=True).numpy() for _ in range(4))
+            rows.append((t, s, r))
+            stats.append(st)
         self.stage_ms = {"execute": 1e3 * (time.perf_counter() - t0)}
-        return (t, s, r), st
+        if len(rows) == 1:
+            return rows[0], stats[0]
+        st = SimpleNamespace(**{f: sum(getattr(x, f) for x in stats) for f in (
+            "comparisons", "survivors", "emitted", "kernel_ms", "pair_ms", "launches", "retries")})
+        st.specialized = min(x.specialized for x in stats)
+        return tuple(np.concatenate([r[c] for r in rows]) for c in range(3)), st
 
     def e2e_step(self, host_enc):
         from paper_2410_04349_b200.engine import DeviceRelation, PathProgram

@@ -734,14 +734,38 @@ def _batch(prog: PathProgram, blocks, cfg: EngineConfig, implied: int = 0):
     return out
 
 
+SPLIT_PAIRS = 50_000_000  # batches with at least this many pairs run one launch per implied root
+
+
+def _batched(prog, path, units, blocks, cfg, symmetric_units: bool) -> list:
+    """_batch over `blocks` (one per unit); a large batch mixing branches runs
+    one launch per branch so each gets its equality root implied
+    (implied_slots_of), small ones one launch with the roots common to all."""
+    def pairs_of(b):
+        r, sp = b
+        return sp * (len(r) - sp) if sp >= 0 else len(r) * (len(r) - 1) // 2
+    masks = [implied_slots_of(path, u) for u in units]
+    if len(set(masks)) <= 1 or sum(pairs_of(b) for b in blocks) < SPLIT_PAIRS:
+        common = masks[0] if masks and len(set(masks)) == 1 else 0
+        return _batch(prog, blocks, cfg, common)
+    out = [None] * len(blocks)
+    for m in sorted(set(masks)):
+        idx = [k for k, x in enumerate(masks) if x == m]
+        for k, cs in zip(idx, _batch(prog, [blocks[k] for k in idx], cfg, m)):
+            out[k] = cs
+    return out
+
+
 def run_partitions(partitions, relation, path, cfg=None, reg=None, encoded=None, program=None) -> list:
     """run_partition over many partitions in ONE device launch (the
-    pipeline's per-task loop, pipeline.py:177-209, batched).  Returns one
-    CandidateSet per partition, each identical to run_partition's."""
+    pipeline's per-task loop, pipeline.py:177-209, batched) -- or one per
+    branch when a large batch mixes equality-rooted branches (each runs with
+    its root implied).  Returns one CandidateSet per partition, each
+    identical to run_partition's."""
     cfg = EngineConfig.of(cfg)
     live = [p for p in partitions if p is not None and len(p.tuple_refs)]
     prog = _program_for(path, relation, reg, encoded, program)
-    res = iter(_batch(prog, [(_refs_array(p), -1) for p in live], cfg, implied_slots_of(path, live))) if live \
+    res = iter(_batched(prog, path, [[p] for p in live], [(_refs_array(p), -1) for p in live], cfg, True)) if live \
         else iter(())
     return [next(res) if (p is not None and len(p.tuple_refs)) else CandidateSet(pairs=[]) for p in partitions]
 
@@ -758,7 +782,7 @@ def run_crosses(pairs, relation, path, cfg=None, reg=None, encoded=None, program
         if len(np.unique(both)) != len(both):
             raise SchemaError("partition -1 has duplicate tuple refs")
         blocks.append((both, len(lr)))
-    return _batch(prog, blocks, cfg, implied_slots_of(path, [p for pair in pairs for p in pair]))
+    return _batched(prog, path, [list(pr) for pr in pairs], blocks, cfg, False)
 
 
 def run_cross(left, right, relation, path, cfg=None, reg=None, encoded=None, program=None) -> CandidateSet:

@@ -470,7 +470,7 @@ def citation3_parts(n: int = 1_000_000, seed: int = 2024, part: int = 512) -> Wo
     return w
 
 
-def plan_partitions(enc: Encoded, path, max_partition_size: int = 65536) -> list:
+def plan_partitions(enc: Encoded, path, max_partition_size: int = 65536, slots: list = None) -> list:
     """The reference pipeline's partitions and sibling pulls for a plan whose
     root edges are all same-attribute equalities (iter_partitions,
     partitioning.py:93-131; sibling_pull_pairs, 144-157), from the encoded
@@ -480,11 +480,13 @@ def plan_partitions(enc: Encoded, path, max_partition_size: int = 65536) -> list
     round-robin into ceil(|g| / max) siblings, and every sibling pair pulled
     as a cross block.  Returns [(refs int32, split)] with split = -1 for a
     partition and |left| for a pull; single-tuple partitions (no pairs) are
-    dropped as pipeline_run drops them in symmetric mode."""
+    dropped as pipeline_run drops them in symmetric mode.  ``slots``: when
+    given a list, receives each block's root slot (the equality its key
+    implies for all its pairs; -1 for the missing-value group)."""
     from .pipeline import root_predicates
 
     blocks = []
-    for pred in root_predicates(path):
+    for b, pred in enumerate(root_predicates(path)):
         if pred.comparator != "eq" or pred.is_cross_attr:
             raise ValueError(f"plan_partitions handles equality roots only, not {pred.describe()}")
         codes = enc.columns[enc.get(("codes", pred.lhs_attr))].data
@@ -494,14 +496,17 @@ def plan_partitions(enc: Encoded, path, max_partition_size: int = 65536) -> list
         sizes = np.diff(np.r_[starts, len(sc)])
         for a, m in zip(starts[sizes > 1].tolist(), sizes[sizes > 1].tolist()):  # single tuples: no pairs
             g = order[a:a + m]
+            n_before = len(blocks)
             if len(g) <= max_partition_size:
-                if len(g) > 1:
-                    blocks.append((g, -1))
-                continue
-            k = -(-len(g) // max_partition_size)
-            subs = [g[i::k] for i in range(k)]
-            blocks += [(x, -1) for x in subs if len(x) > 1]
-            blocks += [(np.concatenate([subs[i], subs[j]]), len(subs[i])) for i in range(k) for j in range(i + 1, k)]
+                blocks.append((g, -1))
+            else:
+                k = -(-len(g) // max_partition_size)
+                subs = [g[i::k] for i in range(k)]
+                blocks += [(x, -1) for x in subs if len(x) > 1]
+                blocks += [(np.concatenate([subs[i], subs[j]]), len(subs[i])) for i in range(k) for j in range(i + 1, k)]
+            if slots is not None:
+                slot = -1 if sc[a] < 0 else int(path.root_slots[b])
+                slots += [slot] * (len(blocks) - n_before)
     return blocks
 
 
@@ -511,7 +516,9 @@ def person5_parts(n: int = 1_000_000, seed: int = 4, max_partition_size: int = 6
     equality root, max_partition_size = 65536) plus sibling pulls, in one
     batched launch."""
     w = person5(n, seed)
-    w.blocks = plan_partitions(w.enc, w.path, max_partition_size)
+    slots: list = []
+    w.blocks = plan_partitions(w.enc, w.path, max_partition_size, slots)
+    w.block_implied = [0 if s < 0 else 1 << s for s in slots]  # each block's branch root holds for its pairs
     w.name = "person5_parts"
     return w
 

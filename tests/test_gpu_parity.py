@@ -282,3 +282,21 @@ def test_run_crosses_with_implied_root_equal_plain(monkeypatch):
         for (r, sp), cs in zip(big, got):
             want = prog.run_raw(r, len(r), RB_SYMMETRIC, split=sp)[0]
             assert sorted(cs.pairs) == sorted((int(a), int(c), path.rule_ids[int(d)]) for a, c, d in zip(*want))
+
+
+@pytest.mark.parametrize("name", goldens.pipeline_names())
+def test_run_partitions_split_by_branch_root(name, monkeypatch):
+    """run_partitions over the partitions of several equality-rooted
+    branches: forced to split (engine.SPLIT_PAIRS = 0), every branch's
+    batch runs with its root implied; each partition's rows equal its own
+    run_partition."""
+    import paper_2410_04349_b200.engine as eng
+    from paper_2410_04349_b200 import run_partitions
+    from paper_2410_04349_b200.pipeline import BandingConfig, iter_partitions
+
+    rel, path, _ = goldens.load(name)
+    parts = [p for p in iter_partitions(rel, path, 16, BandingConfig()) if len(p.tuple_refs) > 1]
+    monkeypatch.setattr(eng, "SPLIT_PAIRS", 0)
+    got = run_partitions(parts, rel, path)
+    for p, cs in zip(parts, got):
+        assert sorted(cs.pairs) == sorted(run_partition(p, rel, path).pairs)
