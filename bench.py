@@ -437,11 +437,13 @@ class BlocksJob(Job):
             for k, p in enumerate(w.path.predicate_table):
                 if p.comparator == "eq" and p.lhs_attr == w.block_attr and p.rhs_attr == w.block_attr:
                     implied_all |= 1 << k
+        from paper_2410_04349_b200.engine import split_by_root
+
         per_block = getattr(w, "block_implied", None)
-        masks = np.array([per_block[k] if per_block is not None else implied_all for k in sel], dtype=np.int64)
+        masks = [per_block[k] if per_block is not None else implied_all for k in sel]
         self.batches = []
-        for m in sorted(set(masks.tolist())):
-            mine = [w.blocks[k] for k in sel[masks == m]]
+        for idx, m in split_by_root(masks, [int(cost[k]) for k in sel]):
+            mine = [w.blocks[sel[q]] for q in idx]
             refs = pin_array(np.concatenate([r for r, _ in mine]).astype(np.int32)) if mine else np.zeros(0, np.int32)
             offs = np.zeros(len(mine) + 1, dtype=np.int64)
             np.cumsum([len(r) for r, _ in mine], out=offs[1:])

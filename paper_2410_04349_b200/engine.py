@@ -734,23 +734,41 @@ def _batch(prog: PathProgram, blocks, cfg: EngineConfig, implied: int = 0):
     return out
 
 
-SPLIT_PAIRS = 50_000_000  # batches with at least this many pairs run one launch per implied root
+SPLIT_PAIRS = 10_000_000_000  # a mixed-branch batch this large splits off its dominant branch (one extra launch)
+
+
+def split_by_root(masks, pairs):
+    """Batches of unit indices for a batch mixing branches: the dominant
+    implied root (at least half the pairs, when the batch has SPLIT_PAIRS
+    pairs or more) in a batch of its own, regated; the rest in one batch with
+    the roots common to all of it.  Returns [(indices, implied mask)]."""
+    total = sum(pairs)
+    kinds = set(masks)
+    if len(kinds) == 1:
+        return [(list(range(len(masks))), masks[0] if masks else 0)]
+    by = {}
+    for m, c in zip(masks, pairs):
+        by[m] = by.get(m, 0) + c
+    dom = max(by, key=by.get)
+    if total < SPLIT_PAIRS or dom == 0 or 2 * by[dom] < total:
+        return [(list(range(len(masks))), 0)]
+    rest = [k for k, m in enumerate(masks) if m != dom]
+    rest_masks = {masks[k] for k in rest}
+    return [([k for k, m in enumerate(masks) if m == dom], dom),
+            (rest, rest_masks.pop() if len(rest_masks) == 1 else 0)]
 
 
 def _batched(prog, path, units, blocks, cfg, symmetric_units: bool) -> list:
-    """_batch over `blocks` (one per unit); a large batch mixing branches runs
-    one launch per branch so each gets its equality root implied
-    (implied_slots_of), small ones one launch with the roots common to all."""
+    """_batch over `blocks` (one per unit), split by split_by_root."""
     def pairs_of(b):
         r, sp = b
         return sp * (len(r) - sp) if sp >= 0 else len(r) * (len(r) - 1) // 2
     masks = [implied_slots_of(path, u) for u in units]
-    if len(set(masks)) <= 1 or sum(pairs_of(b) for b in blocks) < SPLIT_PAIRS:
-        common = masks[0] if masks and len(set(masks)) == 1 else 0
-        return _batch(prog, blocks, cfg, common)
+    groups = split_by_root(masks, [pairs_of(b) for b in blocks])
+    if len(groups) == 1:
+        return _batch(prog, blocks, cfg, groups[0][1])
     out = [None] * len(blocks)
-    for m in sorted(set(masks)):
-        idx = [k for k, x in enumerate(masks) if x == m]
+    for idx, m in groups:
         for k, cs in zip(idx, _batch(prog, [blocks[k] for k in idx], cfg, m)):
             out[k] = cs
     return out
