@@ -447,8 +447,9 @@ class BlocksJob(Job):
             refs = pin_array(np.concatenate([r for r, _ in mine]).astype(np.int32)) if mine else np.zeros(0, np.int32)
             offs = np.zeros(len(mine) + 1, dtype=np.int64)
             np.cumsum([len(r) for r, _ in mine], out=offs[1:])
-            self.batches.append([refs, offs, np.array([sp for _, sp in mine], dtype=np.int64), int(m), None])
+            self.batches.append([refs, offs, np.array([sp for _, sp in mine], dtype=np.int64), int(m)])
         self.implied = implied_all
+        self.out = None  # reusable pinned (t, s, rule, part) rows, every batch's rows back to back
 
     def step(self):
         from types import SimpleNamespace
@@ -456,22 +457,33 @@ class BlocksJob(Job):
         from paper_2410_04349_b200._lib import RB_SYMMETRIC
 
         t0 = time.perf_counter()
-        rows, stats = [], []
+        stats, at = [], 0
+        first = None
+        in_place = self.out is not None
         for b in self.batches:
-            (t, s, r, p), st = self.prog.run_batch(b[0], b[1], b[2], RB_SYMMETRIC, out=b[4], implied=b[3])
-            if b[4] is None:  # later steps copy the rows into reusable pinned buffers
-                import torch
-
-                b[4] = tuple(torch.empty(max(1, len(t)), dtype=torch.int32, pin_memory=True).numpy() for _ in range(4))
-            rows.append((t, s, r))
+            out = None if self.out is None else tuple(a[at:] for a in self.out)
+            (t, s, r, p), st = self.prog.run_batch(b[0], b[1], b[2], RB_SYMMETRIC, out=out, implied=b[3])
+            if out is None or t.ctypes.data != out[0].ctypes.data:  # did not fit the buffers: copies
+                in_place = False
+            first = (first or []) + [(t, s, r)]
+            at += len(t)
             stats.append(st)
+        if not in_place:  # sized by the first (untimed) step; later steps write in place
+            import torch
+
+            self.out = tuple(torch.empty(max(1, at + at // 4 + 1024), dtype=torch.int32, pin_memory=True).numpy()
+                             for _ in range(4))
+            rows = tuple(np.concatenate([x[c] for x in first]) for c in range(3))
+        else:
+            rows = tuple(a[:at] for a in self.out[:3])
+        first = None
         self.stage_ms = {"execute": 1e3 * (time.perf_counter() - t0)}
-        if len(rows) == 1:
-            return rows[0], stats[0]
+        if len(stats) == 1:
+            return rows, stats[0]
         st = SimpleNamespace(**{f: sum(getattr(x, f) for x in stats) for f in (
             "comparisons", "survivors", "emitted", "kernel_ms", "pair_ms", "launches", "retries")})
         st.specialized = min(x.specialized for x in stats)
-        return tuple(np.concatenate([r[c] for r in rows]) for c in range(3)), st
+        return rows, st
 
     def e2e_step(self, host_enc):
         from paper_2410_04349_b200.engine import DeviceRelation, PathProgram
