@@ -1289,6 +1289,22 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
             Fp = &Fi;
         }
     }
+    // Batches of small symmetric partitions (every part a partition of at most
+    // TJS tuples, on average above the packing size): the SMEM-resident
+    // variant stages each whole partition once and lets every warp run its
+    // own balanced pair of row blocks (no per-tile barrier); RB_SMALLRES=0 off
+    JitKernel Jsr;
+    {
+        const char* env_sr = std::getenv("RB_SMALLRES");
+        bool fits = P->jit.ok && P->jit.defer && (flags & RB_SYMMETRIC) && !parts.empty() &&
+                    !(env_sr && std::atoi(env_sr) == 0) && total / (int64_t)parts.size() > std::max<int64_t>(pack_max, 1);
+        for (size_t k = 0; k < parts.size() && fits; k++)
+            fits = parts[k].split < 0 && parts[k].n <= TJS;
+        if (fits) {
+            Jsr = jit_pair_kernel(*Fp, c->device, 2, false, true);
+            if (Jsr.ok && Jsr.smallres) jp = &Jsr;
+        }
+    }
     if (jp == &P->jit && P->jit.ok && P->jit.defer && parts.size() > 1 && pack_max >= 2 &&
         total / (int64_t)parts.size() <= pack_max) {
         static std::mutex packed_mu;
