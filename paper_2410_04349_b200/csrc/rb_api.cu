@@ -1292,12 +1292,15 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
     // Batches of small symmetric partitions (every part a partition of at most
     // TJS tuples, on average above the packing size): the SMEM-resident
     // variant stages each whole partition once and lets every warp run its
-    // own balanced pair of row blocks (no per-tile barrier); RB_SMALLRES=0 off
+    // own balanced pair of row blocks (no per-tile barrier).  Opt-in (RB_SMALLRES=1):
+    // measured slower than the tiled 2-row kernel on 512-tuple partitions (3.03e11
+    // vs 3.82e11 pairs/s, gpurun_out r2ab): one row per lane doubles the
+    // per-inner-tuple work per pair, which costs more than the barrier waits
     JitKernel Jsr;
     {
         const char* env_sr = std::getenv("RB_SMALLRES");
         bool fits = P->jit.ok && P->jit.defer && (flags & RB_SYMMETRIC) && !parts.empty() &&
-                    !(env_sr && std::atoi(env_sr) == 0) && total / (int64_t)parts.size() > std::max<int64_t>(pack_max, 1);
+                    env_sr && std::atoi(env_sr) != 0 && total / (int64_t)parts.size() > std::max<int64_t>(pack_max, 1);
         for (size_t k = 0; k < parts.size() && fits; k++)
             fits = parts[k].split < 0 && parts[k].n <= TJS;
         if (fits) {
@@ -1491,17 +1494,45 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
         std::vector<std::pair<int, int>> ranges, done_ranges, plan;
         std::vector<long long> done_counts;  // survivors of each completed range
         size_t replay = 0;
+        // the plan's key: the item count, tuple count, flags and a sample of the work
+        // items (the ends and ~1k evenly spaced; hashing them all would cost ~1 ns per
+        // byte of a multi-MB item list on every run).  Not the kernel variant: the
+        // gated and ungated kernels of one layout leave the same survivors
+        uint64_t plan_key = 1469598103934665603ull;
+        {
+            auto mixw = [&](uint64_t w) {
+                plan_key ^= w + 0x9e3779b97f4a7c15ull + (plan_key << 6) + (plan_key >> 2);
+                plan_key *= 0xff51afd7ed558ccdull;
+            };
+            mixw((uint64_t)total);
+            mixw((uint64_t)flags);
+            mixw((uint64_t)items.size());
+            auto mix_item = [&](size_t k) {
+                const uint64_t* w = reinterpret_cast<const uint64_t*>(items.p + k);
+                for (size_t q = 0; q < sizeof(Item) / sizeof(uint64_t); q++) mixw(w[q]);
+            };
+            const size_t ni = items.size(), ends = std::min<size_t>(ni, 256);
+            for (size_t k = 0; k < ends; k++) mix_item(k);
+            for (size_t k = ni - ends; k < ni; k++) mix_item(k);
+            const size_t step = std::max<size_t>(1, ni / 1024);
+            for (size_t k = 0; k < ni; k += step) mix_item(k);
+        }
+        long long plan_widest = 0;
         {
             std::lock_guard<std::mutex> lock(P->ranges_mu);
-            auto it = P->range_plans.find(n_items);
-            if (it != P->range_plans.end()) plan = it->second;
+            auto it = P->range_plans.find(plan_key);
+            if (it != P->range_plans.end()) {
+                plan = it->second.ranges;
+                plan_widest = it->second.widest;
+            }
         }
-        if (!plan.empty() && P->last_surv > scap) {  // replayed ranges: the buffer the last run ended with
-            scap = P->last_surv;
+        if (!plan.empty() && plan_widest > scap) {  // replayed ranges: the buffer that plan's widest range needs
+            scap = std::min(SURV_LIMIT, plan_widest);
             if (cudaError_t e = c->surv.grow(sizeof(int4) * (size_t)scap, c->stream))
                 return cleanup(fail(RB_ERR_OOM, "survivor buffer of %lld entries: %s", scap, cudaGetErrorString(e)));
         }
         int retries = 0, next = 0;
+        bool sync_next = false;  // the next range runs checked (an optimistic attempt of it did not fit)
         long long done_items = 0, done_surv = 0;
         for (;;) {
             if (ranges.empty()) {
@@ -1532,6 +1563,20 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
             }
             const int lo = ranges.back().first, hi = ranges.back().second;
             ranges.pop_back();
+            // Optimistic range: when the survivors seen so far say this range fits the
+            // survivor buffer and the output, the verify kernel is queued right behind
+            // the pair kernel and the host waits once.  Both kernels bound their writes
+            // by the capacities and count past them, so a range that did not fit is
+            // rolled back (counters restored) and re-run through the checked path.
+            bool opt = false;
+            {
+                const double rate_now = done_items ? (double)done_surv / (double)done_items : P->surv_rate;
+                if (!sync_next && rate_now >= 0) {
+                    const long long expect = (long long)(rate_now * (double)(hi - lo) * 1.25) + 4096;
+                    opt = expect <= scap && (long long)base[1] + expect * per_row <= cap;
+                }
+                sync_next = false;
+            }
             CK(cudaMemsetAsync(&ctr[0], 0, sizeof(unsigned long long), c->stream));
             CK(cudaMemsetAsync(&ctr[SURV], 0, sizeof(unsigned long long), c->stream));
             R.items = (const Item*)c->items.p + lo;
@@ -1547,6 +1592,39 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
             cudaError_t e = launch_jit_kernel(J, *Fp, P->V, R, std::max(1, std::min(hi - lo, grid)), c->stream);
             if (e) return cleanup(fail(RB_ERR_CUDA, "pair kernel launch: %s", cudaGetErrorString(e)));
             CK(cudaEventRecord(c->ev_mid, c->stream));
+            if (opt) {
+                if ((e = launch_jit_verify(J, P->V, R, grid_v, c->stream)))
+                    return cleanup(fail(RB_ERR_CUDA, "verify kernel launch: %s", cudaGetErrorString(e)));
+                CK(cudaEventRecord(c->ev1, c->stream));
+                CK(cudaMemcpyAsync(host_ctr, ctr, sizeof(unsigned long long) * n_counters, cudaMemcpyDeviceToHost,
+                                   c->stream));
+                if ((e = cudaStreamSynchronize(c->stream)))
+                    return cleanup(fail(RB_ERR_CUDA, "pair + verify kernels: %s", cudaGetErrorString(e)));
+                if (host_ctr[BAD]) return cleanup(bad_refs());
+                const long long surv = (long long)host_ctr[SURV];
+                if (surv > scap || (long long)host_ctr[1] > cap) {  // did not fit: roll back, re-run checked
+                    retries++;
+                    CK(cudaMemcpyAsync(ctr, base.data(), sizeof(unsigned long long) * n_counters,
+                                       cudaMemcpyHostToDevice, c->stream));
+                    ranges.push_back({lo, hi});
+                    sync_next = true;
+                    continue;
+                }
+                float pms = 0, vms = 0;
+                cudaEventElapsedTime(&pms, c->ev0, c->ev_mid);
+                cudaEventElapsedTime(&vms, c->ev_mid, c->ev1);
+                res->stats.pair_ms += pms;
+                res->stats.kernel_ms += pms + vms;
+                res->stats.launches += 2;
+                mark();  // [3] (first range) pair + verify done
+                std::copy(host_ctr, host_ctr + n_counters, base.begin());
+                P->last_surv = std::max(P->last_surv, surv);
+                done_ranges.push_back({lo, hi});
+                done_counts.push_back(surv);
+                done_items += hi - lo;
+                done_surv += surv;
+                continue;
+            }
             CK(cudaMemcpyAsync(host_ctr, ctr, sizeof(unsigned long long) * n_counters, cudaMemcpyDeviceToHost,
                                c->stream));
             if ((e = cudaStreamSynchronize(c->stream))) return cleanup(fail(RB_ERR_CUDA, "pair kernel: %s", cudaGetErrorString(e)));
@@ -1634,12 +1712,14 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
             }
             widest = std::max(widest, acc);  // survivors of the largest merged range: the buffer a replay needs
         }
-        P->last_surv = std::max(P->last_surv, widest);
+        P->last_surv = widest;  // this run's own figure: a later run over other data re-adapts
         {
             std::lock_guard<std::mutex> lock(P->ranges_mu);
-            if (P->range_plans.size() >= 8 && !P->range_plans.count(n_items))
+            if (P->range_plans.size() >= 8 && !P->range_plans.count(plan_key))
                 P->range_plans.erase(P->range_plans.begin());
-            P->range_plans[n_items].swap(merged);
+            RangePlan& rp = P->range_plans[plan_key];
+            rp.ranges.swap(merged);
+            rp.widest = widest;
         }
         // a gate that nearly every warp iteration passes only costs its vote:
         // later runs of this program use the ungated kernel

@@ -116,12 +116,19 @@ using rb::JitKernel;
 // program over a relation of the same shape (the public API building its
 // objects afresh on every call) starts from it instead of probing again.
 // Only sizing hints: overflow handling keeps every run exact.
+// item ranges that fit the survivor buffer in an earlier run over the same work
+// items, and the survivors of the largest of them (the buffer a replay needs)
+struct RangePlan {
+    std::vector<std::pair<int, int>> ranges;
+    long long widest = 0;
+};
+
 struct Learned {
     bool gate_off = false;
     long long last_rows = 0, last_surv = 0;
     std::map<int, long long> rows_by_items;
     double surv_rate = -1.0;
-    std::map<int, std::vector<std::pair<int, int>>> range_plans;
+    std::map<uint64_t, RangePlan> range_plans;
 };
 
 struct rb_ctx {
@@ -206,13 +213,14 @@ struct rb_prog {
     bool gate_off = false;
     long long last_rows = 0;  // output size of the previous run: sizes the next buffer
     std::map<int, long long> rows_by_items;  // output size of the last run over that many items (guarded by ranges_mu)
-    long long last_surv = 0;  // survivors of the previous run: sizes the deferred-verification buffer
+    long long last_surv = 0;  // survivors of the previous run's largest range: sizes the deferred-verification buffer
     double surv_rate = -1.0;  // survivors per work item in the previous run (-1: none yet)
-    // item ranges that fit the survivor buffer in earlier runs, by the run's item count: a
-    // run over the same items (a repeated batch, or one of the size classes of a mixed
-    // batch) replays them instead of re-learning where the survivors concentrate (each
-    // range that overflows is re-run).  At most 8 item counts are kept.
-    std::map<int, std::vector<std::pair<int, int>>> range_plans;
+    // item ranges that fit the survivor buffer in earlier runs, keyed on a hash of the
+    // run's work items, its tuple count and kernel variant: a run over the same items
+    // (a repeated batch, or one of the size classes of a mixed batch) replays them
+    // instead of re-learning where the survivors concentrate (each range that
+    // overflows is re-run).  At most 8 plans are kept.
+    std::map<uint64_t, RangePlan> range_plans;
     std::mutex ranges_mu;  // guards range_plans (a program may be run from several threads)
     uint64_t shape_key = 0;  // hash of the program arrays + relation shape (rb_ctx::learned)
     // the stage-1 gate's inputs (rb::choose_gate), kept for the runs that know
