@@ -298,11 +298,35 @@ int rb_relation_add_mask(rb_rel* r, const uint8_t* mask, int32_t* col) {
 
 static int check_offsets(const int64_t* offsets, int64_t n, int64_t* max_len) {
     if (offsets[0] != 0) return fail(RB_ERR_INVALID, "offsets[0] must be 0");
+    // longest row and first non-monotone row; large columns are scanned by
+    // several host threads (a 10M-row column is 80 MB of offsets, ~10 ms on one
+    // core, ahead of its upload)
+    auto scan = [offsets](int64_t lo, int64_t hi, int64_t* m_out, int64_t* bad_out) {
+        int64_t m = 0, bad = -1;
+        for (int64_t i = lo; i < hi; i++) {
+            const int64_t l = offsets[i + 1] - offsets[i];
+            if (l < 0) {
+                bad = i;
+                break;
+            }
+            m = l > m ? l : m;
+        }
+        *m_out = m;
+        *bad_out = bad;
+    };
+    const int nt = n >= (1 << 20) ? (int)std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency())) : 1;
+    std::vector<int64_t> ms((size_t)nt, 0), bads((size_t)nt, -1);
+    {
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; t++)
+            th.emplace_back(scan, n * t / nt, n * (t + 1) / nt, &ms[(size_t)t], &bads[(size_t)t]);
+        scan(0, n / nt, &ms[0], &bads[0]);
+        for (auto& x : th) x.join();
+    }
     int64_t m = 0;
-    for (int64_t i = 0; i < n; i++) {
-        int64_t l = offsets[i + 1] - offsets[i];
-        if (l < 0) return fail(RB_ERR_INVALID, "offsets not monotone at row %lld", (long long)i);
-        m = std::max(m, l);
+    for (int t = 0; t < nt; t++) {
+        if (bads[(size_t)t] >= 0) return fail(RB_ERR_INVALID, "offsets not monotone at row %lld", (long long)bads[(size_t)t]);
+        m = std::max(m, ms[(size_t)t]);
     }
     if (m > INT32_MAX / 2) return fail(RB_ERR_LIMIT, "row of %lld elements is too long", (long long)m);
     *max_len = m;
@@ -1289,25 +1313,6 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
             Fp = &Fi;
         }
     }
-    // Batches of small symmetric partitions (every part a partition of at most
-    // TJS tuples, on average above the packing size): the SMEM-resident
-    // variant stages each whole partition once and lets every warp run its
-    // own balanced pair of row blocks (no per-tile barrier).  Opt-in (RB_SMALLRES=1):
-    // measured slower than the tiled 2-row kernel on 512-tuple partitions (3.03e11
-    // vs 3.82e11 pairs/s, gpurun_out r2ab): one row per lane doubles the
-    // per-inner-tuple work per pair, which costs more than the barrier waits
-    JitKernel Jsr;
-    {
-        const char* env_sr = std::getenv("RB_SMALLRES");
-        bool fits = P->jit.ok && P->jit.defer && (flags & RB_SYMMETRIC) && !parts.empty() &&
-                    env_sr && std::atoi(env_sr) != 0 && total / (int64_t)parts.size() > std::max<int64_t>(pack_max, 1);
-        for (size_t k = 0; k < parts.size() && fits; k++)
-            fits = parts[k].split < 0 && parts[k].n <= TJS;
-        if (fits) {
-            Jsr = jit_pair_kernel(*Fp, c->device, 2, false, true);
-            if (Jsr.ok && Jsr.smallres) jp = &Jsr;
-        }
-    }
     if (jp == &P->jit && P->jit.ok && P->jit.defer && parts.size() > 1 && pack_max >= 2 &&
         total / (int64_t)parts.size() <= pack_max) {
         static std::mutex packed_mu;
@@ -1494,28 +1499,12 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
         std::vector<std::pair<int, int>> ranges, done_ranges, plan;
         std::vector<long long> done_counts;  // survivors of each completed range
         size_t replay = 0;
-        // the plan's key: the item count, tuple count, flags and a sample of the work
-        // items (the ends and ~1k evenly spaced; hashing them all would cost ~1 ns per
-        // byte of a multi-MB item list on every run).  Not the kernel variant: the
-        // gated and ungated kernels of one layout leave the same survivors
+        // the plan's key: the item count, the run's tuple count and flags (not the
+        // kernel variant: the gated and ungated kernels leave the same survivors)
         uint64_t plan_key = 1469598103934665603ull;
-        {
-            auto mixw = [&](uint64_t w) {
-                plan_key ^= w + 0x9e3779b97f4a7c15ull + (plan_key << 6) + (plan_key >> 2);
-                plan_key *= 0xff51afd7ed558ccdull;
-            };
-            mixw((uint64_t)total);
-            mixw((uint64_t)flags);
-            mixw((uint64_t)items.size());
-            auto mix_item = [&](size_t k) {
-                const uint64_t* w = reinterpret_cast<const uint64_t*>(items.p + k);
-                for (size_t q = 0; q < sizeof(Item) / sizeof(uint64_t); q++) mixw(w[q]);
-            };
-            const size_t ni = items.size(), ends = std::min<size_t>(ni, 256);
-            for (size_t k = 0; k < ends; k++) mix_item(k);
-            for (size_t k = ni - ends; k < ni; k++) mix_item(k);
-            const size_t step = std::max<size_t>(1, ni / 1024);
-            for (size_t k = 0; k < ni; k += step) mix_item(k);
+        for (uint64_t w : {(uint64_t)items.size(), (uint64_t)total, (uint64_t)flags}) {
+            plan_key ^= w + 0x9e3779b97f4a7c15ull + (plan_key << 6) + (plan_key >> 2);
+            plan_key *= 0xff51afd7ed558ccdull;
         }
         long long plan_widest = 0;
         {
@@ -1527,7 +1516,7 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
             }
         }
         if (!plan.empty() && plan_widest > scap) {  // replayed ranges: the buffer that plan's widest range needs
-            scap = std::min(SURV_LIMIT, plan_widest);
+            scap = plan_widest;  // may exceed SURV_LIMIT: a single item with more survivors
             if (cudaError_t e = c->surv.grow(sizeof(int4) * (size_t)scap, c->stream))
                 return cleanup(fail(RB_ERR_OOM, "survivor buffer of %lld entries: %s", scap, cudaGetErrorString(e)));
         }

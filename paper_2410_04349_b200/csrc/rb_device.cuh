@@ -58,9 +58,6 @@ typedef unsigned long long uintptr_t;
 namespace rb {
 
 constexpr int MAX_COLS = 64;
-#ifndef SPEC_SMALLRES
-#define SPEC_SMALLRES 0  // 1: items of at most TJS rows x TJS columns, staged whole (dynamic shared memory)
-#endif
 #ifndef SPEC_PACKED
 #define SPEC_PACKED 0  // 1: the kernel also takes MODE_PACKED items (batches of tiny partitions)
 #endif
@@ -680,14 +677,6 @@ struct __align__(16) Tile {
     Rec r[TJ];
 };
 
-// The SMEM-resident small-partition variant (SPEC_SMALLRES): a whole
-// symmetric partition of at most TJS tuples staged once (dynamic shared
-// memory), so the CTA's warps never meet at a per-tile barrier.
-constexpr int TJS = 512;
-struct __align__(16) TileS {
-    Rec r[TJS];
-};
-
 // Shape of the filter program: compile-time constants in a specialised
 // (NVRTC) build, kernel-parameter reads in the generic build.
 #ifdef RB_SPEC
@@ -997,7 +986,7 @@ struct Outer {
     }
 
     // valid(jj) <=> jj >= jj_lo && jj != jj_skip, for the tile starting at jt
-    __device__ __forceinline__ bool tile(int mode, int64_t jt, int tj = TJ) {
+    __device__ __forceinline__ bool tile(int mode, int64_t jt) {
         jj_lo = 0;
         jj_skip = -1;
 #if SPEC_PACKED
@@ -1012,52 +1001,22 @@ struct Outer {
         }
 #endif
         if (!ok) {
-            jj_lo = tj + 1;
+            jj_lo = TJ + 1;
         } else if (mode == MODE_SYM) {
             const int64_t d = i - jt + 1;
-            jj_lo = d < 0 ? 0 : (d > tj + 1 ? tj + 1 : (int)d);
+            jj_lo = d < 0 ? 0 : (d > TJ + 1 ? TJ + 1 : (int)d);
         } else if (mode == MODE_ASYM) {
             const int64_t d = i - jt;
-            jj_skip = (d >= 0 && d < tj) ? (int)d : -1;
+            jj_skip = (d >= 0 && d < TJ) ? (int)d : -1;
         }
         return jj_lo == 0 && jj_skip < 0;
     }
 };
 
-// One inner tuple's record (position j of the run's refs) into shared memory.
-__device__ __forceinline__ void stage_rec(const FilterPlan& F, const RunParams& R, const int32_t* tab, Rec& rec,
-                                          int64_t j) {
-    const int32_t sj = R.refs ? __ldg(R.refs + j) : (int32_t)j;
-    rec.tid = sj;
-#pragma unroll
-    for (int f = 0; f < MAX_EQ; f++)
-        if (f < RB_NEQ) rec.head[f] = __ldg(F.eq_inner[f] + sj);
-#pragma unroll
-    for (int f = 0; f < MAX_TOK; f++)
-        if (f < RB_NTOK) {
-            rec.head[RB_NEQ + f] = __ldg(F.tok_ilen[f] + sj);
-            uint4 sg = __ldg(F.tok_isig[f] + sj);
-            if (RB_TOK_SIG64(f)) sg = make_uint4(sg.x | sg.z, sg.y | sg.w, 0u, 0u);
-            rec.toksig[f] = sg;
-            rec.tokhash[f] = __ldg(F.tok_ihash[f] + sj);
-        }
-#pragma unroll
-    for (int f = 0; f < MAX_STR; f++)
-        if (f < RB_NSTR) {
-            const int lb = __ldg(F.str_ilen[f] + sj);
-            rec.strlen_[f] = lb;
-            const uint4 bg = __ldg(F.str_ibag[f] + sj);
-            rec.strbag[f] = RB_STR_FOLD(f) ? fold_bag(bg) : bg;
-#pragma unroll
-            for (int z = 0; z < MAX_FSLOTS; z++)
-                if (z < RB_STR_NS(f)) rec.strm2[f][z] = str_m2(tab, F.str_slot[f][z], RB_STR_OFF(f, z), lb);
-        }
-}
-
 // The per-pair filter over one shared tile for ROWS outer tuples per thread.
 // AllValid: every (outer, jj) pair of the warp is inside the pair space.
-template <typename Mask, int ROWS, bool AllValid, bool DEFER, typename TileT>
-__device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg& V, const RunParams& R, const TileT& T,
+template <typename Mask, int ROWS, bool AllValid, bool DEFER>
+__device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg& V, const RunParams& R, const Tile& T,
                                           const int32_t* tab, Outer<Mask> (&o)[ROWS], int jj0, int tn, int2* q, int& qn,
                                           int part, int part_hi, const int* cp_rule, int32_t* scratch,
                                           unsigned long long& my_surv, unsigned& gate_hits, unsigned& gate_iters) {
@@ -1291,12 +1250,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
 // ROWS outer tuples per thread: a work item covers BLOCK * ROWS outer rows.
 template <typename Mask, int ROWS, bool DEFER = false>
 __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg& V, const RunParams& R) {
-#if SPEC_SMALLRES
-    extern __shared__ __align__(16) unsigned char rb_dyn_smem[];
-    TileS& TS = *reinterpret_cast<TileS*>(rb_dyn_smem);
-#else
     __shared__ Tile T;
-#endif
     __shared__ int2 queue[NWARPS][QCAP];
     __shared__ __align__(16) int32_t tab[SMEM_TAB];
     __shared__ int cp_rule[MAX_RULES];
@@ -1315,50 +1269,6 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
     for (int k = threadIdx.x; k < MAX_RULES; k += BLOCK) cp_rule[k] = V.cp_rule[k];
     for (int k = threadIdx.x; k < F.n_tab; k += BLOCK) tab[k] = F.tab_src[k];
 
-#if SPEC_SMALLRES
-    // Small symmetric partitions: an item is at most TJS outer rows x TJS inner
-    // columns, staged ONCE, then every warp runs its own two row blocks -- block
-    // w and block 15 - w of 16, so each warp has about the same pairs of the
-    // triangle -- against the whole staged range with no CTA barrier in between
-    // (the per-tile barriers of the tiled loop idle the warps whose rows end
-    // early: 5.9 barrier stalls per issue on 512-tuple partitions).
-    for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_item = (int)atomicAdd(R.item_counter, 1u);
-        __syncthreads();
-        const int it = s_item;
-        if (it >= R.n_items) break;
-        const Item item = R.items[it];
-        const int64_t col0 = item.col0, col1 = item.col1, row0 = item.row0, row_hi = item.row_hi;
-        const int part = item.part;
-        const int ncol = (int)(col1 - col0), nrow = (int)(row_hi - row0);
-        for (int k = threadIdx.x; k < ncol; k += BLOCK) stage_rec(F, R, tab, TS.r[k], col0 + k);
-        __syncthreads();
-        const int bs = (nrow + 2 * NWARPS - 1) / (2 * NWARPS);  // rows per block (<= 32)
-#pragma unroll 1
-        for (int half = 0; half < 2; half++) {
-            const int blk = half ? 2 * NWARPS - 1 - warp : warp;
-            const int rr = blk * bs + lane;
-            Outer<Mask> o1[1];
-            o1[0].load(F, R, tab, item.mode, (lane < bs && rr < nrow) ? row0 + rr : row_hi, row_hi, col0, col1, my_pairs,
-                       part, -1);
-            o1[0].tile(item.mode, col0, TJS);
-            const int jj0 = __reduce_min_sync(FULL, o1[0].jj_lo);
-            if (jj0 < ncol)
-                tile_loop<Mask, 1, false, DEFER>(F, V, R, TS, tab, o1, jj0, ncol, q, qn, part, -1, cp_rule, scratch,
-                                                 my_surv, gate_hits, gate_iters);
-        }
-        if (qn) {
-            __syncwarp();
-            if (DEFER)
-                flush_survivors(R, q, qn, part, -1);
-            else
-                drain_queue(V, R, q, qn, part, cp_rule, scratch);
-            __syncwarp();
-            qn = 0;
-        }
-    }
-#else
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) s_item = (int)atomicAdd(R.item_counter, 1u);
@@ -1382,7 +1292,34 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
         for (int64_t jt = col0; jt < col1; jt += TJ) {
             const int tn = (int)(col1 - jt < TJ ? col1 - jt : TJ);
             __syncthreads();
-            for (int k = threadIdx.x; k < tn; k += BLOCK) stage_rec(F, R, tab, T.r[k], jt + k);
+            for (int k = threadIdx.x; k < tn; k += BLOCK) {
+                const int64_t j = jt + k;
+                const int32_t sj = R.refs ? __ldg(R.refs + j) : (int32_t)j;
+                T.r[k].tid = sj;
+#pragma unroll
+                for (int f = 0; f < MAX_EQ; f++)
+                    if (f < RB_NEQ) T.r[k].head[f] = __ldg(F.eq_inner[f] + sj);
+#pragma unroll
+                for (int f = 0; f < MAX_TOK; f++)
+                    if (f < RB_NTOK) {
+                        T.r[k].head[RB_NEQ + f] = __ldg(F.tok_ilen[f] + sj);
+                        uint4 sg = __ldg(F.tok_isig[f] + sj);
+                        if (RB_TOK_SIG64(f)) sg = make_uint4(sg.x | sg.z, sg.y | sg.w, 0u, 0u);
+                        T.r[k].toksig[f] = sg;
+                        T.r[k].tokhash[f] = __ldg(F.tok_ihash[f] + sj);
+                    }
+#pragma unroll
+                for (int f = 0; f < MAX_STR; f++)
+                    if (f < RB_NSTR) {
+                        const int lb = __ldg(F.str_ilen[f] + sj);
+                        T.r[k].strlen_[f] = lb;
+                        const uint4 bg = __ldg(F.str_ibag[f] + sj);
+                        T.r[k].strbag[f] = RB_STR_FOLD(f) ? fold_bag(bg) : bg;
+#pragma unroll
+                        for (int z = 0; z < MAX_FSLOTS; z++)
+                            if (z < RB_STR_NS(f)) T.r[k].strm2[f][z] = str_m2(tab, F.str_slot[f][z], RB_STR_OFF(f, z), lb);
+                    }
+            }
             __syncthreads();
 
             bool all_valid = true;
@@ -1421,8 +1358,6 @@ __device__ __forceinline__ void pair_body(const FilterPlan& F, const VerifyProg&
             qn = 0;
         }
     }
-
-#endif  // SPEC_SMALLRES
 
     // ---- statistics
 #pragma unroll

@@ -49,8 +49,6 @@ struct JitKernel {
     bool defer = false;  // survivors go to a buffer decided by `verify` (see RunParams::surv)
     bool gated = false;  // compiled with the stage-1 gate (counts gate passes in RunParams::stat_gate)
     bool packed = false;  // takes MODE_PACKED items (several tiny partitions per item)
-    bool smallres = false;  // items of at most TJS x TJS staged whole (SPEC_SMALLRES)
-    int dyn_smem = 0;       // dynamic shared memory bytes per CTA (smallres: the staged partition)
     cudaKernel_t verify = nullptr;
     int verify_blocks_per_sm = 1;
     double compile_ms = 0;
@@ -59,8 +57,7 @@ struct JitKernel {
 };
 // force_rows > 0 compiles that many outer rows per thread (the small-partition variant);
 // packed: the variant also takes MODE_PACKED items (deferred kernels only)
-JitKernel jit_pair_kernel(const FilterPlan& F, int device, int force_rows = 0, bool packed = false,
-                          bool smallres = false);
+JitKernel jit_pair_kernel(const FilterPlan& F, int device, int force_rows = 0, bool packed = false);
 cudaError_t launch_jit_kernel(const JitKernel& k, const FilterPlan& F, const VerifyProg& V, const RunParams& R,
                               int grid, cudaStream_t st);
 cudaError_t launch_jit_verify(const JitKernel& k, const VerifyProg& V, const RunParams& R, int grid, cudaStream_t st);

@@ -25,6 +25,7 @@
 #include <map>
 #include <numeric>
 #include <queue>
+#include <thread>
 
 #include "rb_state.cuh"
 
@@ -52,6 +53,35 @@ struct rb_parts {
 namespace {
 
 constexpr int PB = 256;  // threads per block of the streaming kernels
+
+// The host lists of the last destroyed partition set, handed to the next one:
+// a 10M-tuple step builds ~1.6M entries (60+ MB) and fresh vectors cost their
+// first-touch page faults every step; recycled ones keep their capacity.
+std::mutex g_spare_mu;
+std::vector<Part> g_spare_parts;
+std::vector<int32_t> g_spare_branch, g_spare_sibling;
+std::vector<uint8_t> g_spare_first;
+
+void spare_lists_take(rb_parts* P) {
+    std::lock_guard<std::mutex> lock(g_spare_mu);
+    P->parts.swap(g_spare_parts);
+    P->branch.swap(g_spare_branch);
+    P->sibling.swap(g_spare_sibling);
+    P->first_group.swap(g_spare_first);
+    P->parts.clear();
+    P->branch.clear();
+    P->sibling.clear();
+    P->first_group.clear();
+}
+
+void spare_lists_put(rb_parts* P) {
+    std::lock_guard<std::mutex> lock(g_spare_mu);
+    if (P->parts.capacity() <= g_spare_parts.capacity()) return;  // keep the larger set
+    P->parts.swap(g_spare_parts);
+    P->branch.swap(g_spare_branch);
+    P->sibling.swap(g_spare_sibling);
+    P->first_group.swap(g_spare_first);
+}
 
 double host_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -392,6 +422,7 @@ int partition_impl(rb_ctx* c, rb_rel* rel, const int32_t* cols, const int64_t* k
     std::lock_guard<std::mutex> lock(c->mu);
     rb_parts* P = new (std::nothrow) rb_parts();
     if (!P) return fail(RB_ERR_OOM, "host allocation failed");
+    spare_lists_take(P);
     P->ctx = c;
     P->n = n;
     P->n_branches = nb;
@@ -621,6 +652,7 @@ int rb_parts_destroy(rb_parts* p) {
         dev_free(p->d_refs, p->ctx->stream);
         cudaStreamSynchronize(p->ctx->stream);
     }
+    spare_lists_put(p);
     delete p;
     return RB_OK;
 }
@@ -631,15 +663,51 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
     if (parts->ctx != c) return fail(RB_ERR_INVALID, "rb_run_parts: parts belong to another context");
     if (world < 1 || rank < 0 || rank >= world) return fail(RB_ERR_INVALID, "rb_run_parts: rank %d of %d", rank, world);
     const bool sym = (flags & RB_SYMMETRIC) != 0;
+    static const bool timing = std::getenv("RB_HOST_TIMING") != nullptr;
+    double tm[8] = {timing ? host_ms() : 0.0};
+    int ntm = 1;
+    auto mark = [&]() {
+        if (timing && ntm < 8) tm[ntm++] = host_ms();
+    };
+    auto report = [&](const char* what) {
+        if (!timing) return;
+        fprintf(stderr, "rb run_parts (%s):", what);
+        for (int k = 1; k < ntm; k++) fprintf(stderr, " %.3f", tm[k] - tm[k - 1]);
+        fprintf(stderr, " ms\n");
+    };
+    // Host lists of the run, kept per thread between calls: fresh multi-MB
+    // vectors cost ~80 ms of first-touch page faults per 10M-tuple step while
+    // the GPU waits for the first launch (clear() keeps the capacity)
+    struct Lists {
+        std::vector<int64_t> units, sel;
+        std::vector<Part> mine, pi, po;
+        std::vector<int32_t> ii, io;
+        std::vector<int> sel_bpos;
+        std::vector<int64_t> cost;
+        std::vector<size_t> idx;
+        std::vector<int32_t> owner;
+    };
+    static thread_local Lists LS;
     // the evaluated units: partitions with pairs, and the pulls
-    std::vector<int64_t> units;
-    units.reserve(parts->parts.size());
-    for (size_t k = 0; k < parts->parts.size(); k++)
-        if (pair_count(parts->parts[k], sym) > 0) units.push_back((int64_t)k);
-    std::vector<Part> mine;
-    std::vector<int64_t> sel;  // entry index of every unit of `mine`
-    if (world == 1) {
+    std::vector<int64_t>& units = LS.units;
+    units.clear();
+    std::vector<Part>& mine = LS.mine;
+    std::vector<int64_t>& sel = LS.sel;  // entry index of every unit of `mine`
+    mine.clear();
+    sel.clear();
+    // one rank whose every entry has pairs (the usual case: partitions of one
+    // tuple are not entries): the entries themselves are the units, no copies
+    bool alias = world == 1;
+    for (size_t k = 0; k < parts->parts.size() && alias; k++) alias = pair_count(parts->parts[k], sym) > 0;
+    if (!alias) {
+        units.reserve(parts->parts.size());
+        for (size_t k = 0; k < parts->parts.size(); k++)
+            if (pair_count(parts->parts[k], sym) > 0) units.push_back((int64_t)k);
+    }
+    if (alias) {
+    } else if (world == 1) {
         mine.reserve(units.size());
+        sel.reserve(units.size());
         for (int64_t k : units) {
             mine.push_back(parts->parts[(size_t)k]);
             sel.push_back(k);
@@ -652,14 +720,16 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
         // (water-filling over a prefix sum).  A full LPT sort of 1.6M units
         // cost ~150 ms of host time per rank at 10M tuples.
         const size_t nu = units.size();
-        std::vector<int64_t> cost(nu);
+        std::vector<int64_t>& cost = LS.cost;
+        cost.resize(nu);
         int64_t all = 0;
         for (size_t q = 0; q < nu; q++) {
             cost[q] = pair_count(parts->parts[(size_t)units[q]], sym);
             all += cost[q];
         }
         const size_t kbig = std::min(nu, (size_t)4096 * (size_t)world);
-        std::vector<size_t> idx(nu);
+        std::vector<size_t>& idx = LS.idx;
+        idx.resize(nu);
         std::iota(idx.begin(), idx.end(), 0);
         if (kbig < nu)
             std::nth_element(idx.begin(), idx.begin() + (long)kbig, idx.end(), [&](size_t a, size_t b) {
@@ -668,7 +738,8 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
         std::sort(idx.begin(), idx.begin() + (long)kbig, [&](size_t a, size_t b) {
             return cost[a] != cost[b] ? cost[a] > cost[b] : a < b;
         });
-        std::vector<int32_t> owner(nu, -1);
+        std::vector<int32_t>& owner = LS.owner;
+        owner.assign(nu, -1);
         std::vector<int64_t> load((size_t)world, 0);
         for (size_t q = 0; q < kbig; q++) {
             int32_t best = 0;
@@ -692,14 +763,19 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
                 sel.push_back(units[q]);
             }
     }
-    std::vector<int> sel_bpos(sel.size(), -1);  // branch position of every unit
+    mark();  // [1] units selected and placed
+    const std::vector<Part>& M = alias ? parts->parts : mine;  // the units
+    const size_t nsel = M.size();
+    auto S = [&](size_t q) -> size_t { return alias ? q : (size_t)sel[q]; };  // entry index of unit q
+    std::vector<int>& sel_bpos = LS.sel_bpos;  // branch position of every unit
+    sel_bpos.assign(nsel, -1);
     {
         std::map<int32_t, int> pos_of;
         for (size_t b = 0; b < parts->branch_ids.size(); b++) pos_of.emplace(parts->branch_ids[b], (int)b);
         int32_t last_id = INT32_MIN;
         int last_pos = -1;
-        for (size_t q = 0; q < sel.size(); q++) {
-            const int32_t id = parts->branch[(size_t)sel[q]];
+        for (size_t q = 0; q < nsel; q++) {
+            const int32_t id = parts->branch[S(q)];
             if (id != last_id) {  // units come branch by branch
                 auto it = pos_of.find(id);
                 last_pos = it == pos_of.end() ? -1 : it->second;
@@ -719,12 +795,12 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
     if (!parts->root_slot.empty() && !(implied_off && std::atoi(implied_off) != 0)) {
         std::vector<int64_t> by_b(parts->branch_ids.size(), 0);
         int64_t all = 0;
-        for (size_t q = 0; q < sel.size(); q++) {
-            const int64_t pc = pair_count(mine[q], sym);
+        for (size_t q = 0; q < nsel; q++) {
+            const int64_t pc = pair_count(M[q], sym);
             all += pc;
             const int bpos = sel_bpos[q];
             if (bpos >= 0 && parts->root_slot[(size_t)bpos] >= 0 &&
-                !(parts->first_group[(size_t)sel[q]] && parts->first_missing[(size_t)bpos]))
+                !(parts->first_group[S(q)] && parts->first_missing[(size_t)bpos]))
                 by_b[(size_t)bpos] += pc;
         }
         for (size_t b = 0; b < by_b.size(); b++)
@@ -734,29 +810,59 @@ int rb_run_parts(rb_ctx* c, rb_rel* rel, rb_prog* P, const rb_parts* parts, int3
             }
         if (best * 2 < all) best_b = -1;  // not worth a second run
     }
-    if (best_b < 0) return run_mixed(c, rel, P, parts->d_refs, total, mine, flags, false, out, true);
-    std::vector<Part> pi, po;
-    std::vector<int32_t> ii, io;
-    for (size_t q = 0; q < sel.size(); q++) {
-        const bool imp = sel_bpos[q] == best_b &&
-                         !(parts->first_group[(size_t)sel[q]] && parts->first_missing[(size_t)best_b]);
-        (imp ? pi : po).push_back(mine[q]);
-        (imp ? ii : io).push_back((int32_t)q);
+    mark();  // [2] branch totals
+    if (best_b < 0) {
+        const int rc0 = run_mixed(c, rel, P, parts->d_refs, total, M, flags, false, out, true);
+        mark();
+        report("one run: select, branches, run");
+        return rc0;
     }
+    std::vector<Part>&pi = LS.pi, &po = LS.po;
+    std::vector<int32_t>&ii = LS.ii, &io = LS.io;
+    pi.clear();
+    po.clear();
+    ii.clear();
+    io.clear();
+    auto implied_unit = [&](size_t q) {
+        return sel_bpos[q] == best_b && !(parts->first_group[S(q)] && parts->first_missing[(size_t)best_b]);
+    };
+    // the implied units now; the others (most of the list) by a host thread
+    // while the implied run is on the GPU
+    for (size_t q = 0; q < nsel; q++)
+        if (implied_unit(q)) {
+            pi.push_back(M[q]);
+            ii.push_back((int32_t)q);
+        }
+    std::thread plain_lists([&]() {
+        po.reserve(nsel - pi.size());
+        io.reserve(nsel - pi.size());
+        for (size_t q = 0; q < nsel; q++)
+            if (!implied_unit(q)) {
+                po.push_back(M[q]);
+                io.push_back((int32_t)q);
+            }
+    });
     const uint64_t implied = 1ull << parts->root_slot[(size_t)best_b];
     rb_result* ri = nullptr;
+    mark();  // [3] implied / plain split
     int rc = run_mixed(c, rel, P, parts->d_refs, total, pi, flags, false, &ri, true, implied);
+    plain_lists.join();
+    mark();  // [4] implied run
     if (rc != RB_OK || po.empty()) {
         *out = ri;
         return rc;
     }
     rb_result* ro = nullptr;
     rc = run_mixed(c, rel, P, parts->d_refs, total, po, flags, false, &ro, true);
+    mark();  // [5] plain run
     if (rc != RB_OK) {
         rb_result_destroy(ri);
         return rc;
     }
-    return merge_results(c, ro, ri, false, io, ii, out);
+    rc = merge_results(c, ro, ri, false, io, ii, out);
+    mark();  // [6] merged
+    report("select, branches, split, implied run, plain run, merge");
+    return rc;
 }
 
 int rb_result_collect(rb_result* res, int64_t n_tuples, int32_t n_rules) {

@@ -300,36 +300,3 @@ def test_run_partitions_split_by_branch_root(name, monkeypatch):
     got = run_partitions(parts, rel, path)
     for p, cs in zip(parts, got):
         assert sorted(cs.pairs) == sorted(run_partition(p, rel, path).pairs)
-
-
-@pytest.mark.parametrize("name", ["citation", "grouped", "random_052", "random_071", "edge_unicode"])
-@pytest.mark.parametrize("smallres", ["1", "0"])
-def test_small_partition_batches_resident_variant(name, smallres, monkeypatch):
-    """Batches of symmetric partitions of 65..512 tuples run the
-    SMEM-resident variant (whole partition staged once, balanced row blocks
-    per warp): every partition's rows and comparison count equal the oracle's
-    (RB_SMALLRES=0: the tiled kernel)."""
-    from oracle import oracle
-    from paper_2410_04349_b200 import run_partitions
-    from paper_2410_04349_b200.encode import RelationEncoding, compile_program
-
-    monkeypatch.setenv("RB_SMALLRES", smallres)
-    rel, path, _ = goldens.load(name)
-    n = len(rel)
-    rng = np.random.default_rng(9)
-    perm = rng.permutation(n)
-    parts, at = [], 0
-    while at < n:
-        size = int(rng.integers(65, 513))
-        refs = tuple(int(x) for x in perm[at:at + size])
-        if len(refs) > 1:
-            parts.append(DataPartition(len(parts), refs))
-        at += size
-    got = run_partitions(parts, rel, path, EngineConfig())
-    enc = RelationEncoding(rel).prepare(path.predicate_table)
-    prog = compile_program(path, enc)
-    for p, cs in zip(parts, got):
-        refs = np.array(p.tuple_refs, dtype=np.int32)
-        want, cmp, _ = oracle.run(enc, prog, refs, len(refs), flags=1)
-        assert sorted(cs.pairs) == sorted((int(a), int(b), path.rule_ids[int(c)]) for a, b, c in want.tolist())
-        assert cs.stats.total_comparisons() == cmp

@@ -26,12 +26,12 @@ def _compile(defs):
     return rc == nvrtc.nvrtcResult.NVRTC_SUCCESS, log.decode(errors="replace")
 
 
-def _spec_defs(rows=3, packed=0, mask="uint32_t", eq_any=0, smallres=0):
+def _spec_defs(rows=3, packed=0, mask="uint32_t", eq_any=0):
     names = sorted(set(re.findall(r"\bSPEC_[A-Z0-9_]+", open(SRC).read())))
     vals = {"SPEC_MASK": mask, "SPEC_NEQ": "2", "SPEC_NTOK": "1", "SPEC_NSTR": "1", "SPEC_TOK0_NS": "2",
             "SPEC_TOK0_NJ": "2", "SPEC_STR0_NS": "1", "SPEC_ROWS": str(rows), "SPEC_MINBLOCKS": "3",
             "SPEC_UNROLL": "2", "SPEC_DEFER": "1", "SPEC_PACKED": str(packed), "SPEC_ALL_RULES": "0x7",
-            "SPEC_TOK2D": "1", "SPEC_GATE": "1", "SPEC_TOK0_SIG64": "1", "SPEC_EQ_ANY": str(eq_any), "SPEC_SMALLRES": str(smallres),
+            "SPEC_TOK2D": "1", "SPEC_GATE": "1", "SPEC_TOK0_SIG64": "1", "SPEC_EQ_ANY": str(eq_any),
             "SPEC_EQ_FREE": "0x1", "SPEC_EQ_KILL_0": "0x2", "SPEC_EQ_KILL_1": "0x4"}
     full = set()
     for n in names:  # token-pasted families (RB_PICK*(f, SPEC_EQ_KILL_) -> SPEC_EQ_KILL_0..7)
@@ -52,10 +52,4 @@ def test_generic_shape_compiles():
                                                      (2, 0, "uint32_t", 1), (3, 1, "rb::RuleBits<3>", 1)])
 def test_specialised_shape_compiles(rows, packed, mask, eq_any):
     ok, log = _compile(_spec_defs(rows, packed, mask, eq_any))
-    assert ok, log
-
-
-@pytest.mark.parametrize("mask", ["uint32_t", "rb::RuleBits<3>"])
-def test_smallres_shape_compiles(mask):
-    ok, log = _compile(_spec_defs(2, 0, mask, 0, smallres=1))
     assert ok, log
