@@ -58,6 +58,9 @@ typedef unsigned long long uintptr_t;
 namespace rb {
 
 constexpr int MAX_COLS = 64;
+#ifndef SPEC_PREANY
+#define SPEC_PREANY 1  // gated kernels: the stage-1 pre-vote in tile_loop (RB_PREANY=0 at run time: off)
+#endif
 #ifndef SPEC_PACKED
 #define SPEC_PACKED 0  // 1: the kernel also takes MODE_PACKED items (batches of tiny partitions)
 #endif
@@ -1038,6 +1041,71 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
 #pragma unroll SPEC_UNROLL
 #endif
     for (int jj = jj0; jj < tn; jj++) {
+#if defined(RB_SPEC) && RB_GATE && !SPEC_EQ_ANY && SPEC_PREANY
+        {
+            // Stage-1 pre-vote: whether any rule of any row survives the stage-1
+            // tests, as one sum of products of the test outcomes (rule k lives
+            // iff every stage-1 test whose kill set holds k passes).  The same
+            // condition as the gate below, without building the rule masks:
+            // most warp iterations stop here after the compares, popcounts and
+            // a few predicate ops; the rest re-run the tests and build the masks.
+            bool anyw = false;
+#pragma unroll
+            for (int r = 0; r < ROWS; r++) {
+#if SPEC_PACKED
+                const bool valid = AllValid || (jj >= o[r].jj_lo && jj != o[r].jj_skip && jj < o[r].jj_hi);
+#else
+                const bool valid = AllValid || (jj >= o[r].jj_lo && jj != o[r].jj_skip);
+#endif
+                bool peq[MAX_EQ];
+#pragma unroll
+                for (int f = 0; f < MAX_EQ; f++) {
+                    peq[f] = true;
+                    if (f < RB_NEQ && !RB_EQ_STAGE2(f) && RB_EQ_KILL(f)) peq[f] = o[r].ocode[f] == T.r[jj].head[f];
+                }
+                bool ptk[MAX_TOK][MAX_FSLOTS];
+#pragma unroll
+                for (int f = 0; f < MAX_TOK; f++) {
+                    int u = 0;
+                    uint32_t a = 0;
+                    if (f < RB_NTOK && RB_TOK_NJ(f) > 0) {
+                        const uint4 is = T.r[jj].toksig[f];
+                        u = RB_TOK_SIG64(f) ? __popc(o[r].lev[f][0] & is.x) + __popc(o[r].lev[f][1] & is.y) + o[r].orem[f]
+                                            : __popc(o[r].lev[f][0] & is.x) + __popc(o[r].lev[f][1] & is.y) +
+                                                  __popc(o[r].lev[f][2] & is.z) + __popc(o[r].lev[f][3] & is.w) +
+                                                  o[r].orem[f];
+                        a = o[r].orow[f] + ((uint32_t)(T.r[jj].head[RB_NEQ + f] * RB_TOK_NJP(f)) << 2);
+                    }
+#pragma unroll
+                    for (int z = 0; z < MAX_FSLOTS; z++) {
+                        ptk[f][z] = true;
+                        if (f < RB_NTOK && z < RB_TOK_NS(f) && !RB_TOK_STAGE2(f, z) && RB_TOK_KILL(f, z))
+                            ptk[f][z] = z < RB_TOK_NJ(f) ? u >= lds_s32(a + 4u * z)
+                                                         : T.r[jj].tokhash[f].x == o[r].ohash[f].x;
+                    }
+                }
+                bool any_r = false;
+#pragma unroll
+                for (int k = 0; k < 64; k++) {
+                    if (!(((uint64_t)RB_ALL_RULES >> k) & 1)) continue;
+                    bool ok = RB_NCONST == 0 || m_hits(o[r].alive_c, 1ull << k);
+#pragma unroll
+                    for (int f = 0; f < MAX_EQ; f++)
+                        if (f < RB_NEQ && !RB_EQ_STAGE2(f) && (((uint64_t)RB_EQ_KILL(f) >> k) & 1)) ok = ok && peq[f];
+#pragma unroll
+                    for (int f = 0; f < MAX_TOK; f++)
+#pragma unroll
+                        for (int z = 0; z < MAX_FSLOTS; z++)
+                            if (f < RB_NTOK && z < RB_TOK_NS(f) && !RB_TOK_STAGE2(f, z) &&
+                                (((uint64_t)RB_TOK_KILL(f, z) >> k) & 1))
+                                ok = ok && ptk[f][z];
+                    any_r = any_r || ok;
+                }
+                anyw = anyw || (valid && any_r);
+            }
+            if (!__any_sync(FULL, anyw)) continue;
+        }
+#endif
         Mask alive[ROWS];
 #pragma unroll
         for (int r = 0; r < ROWS; r++) {
