@@ -676,6 +676,9 @@ struct __align__(16) Rec {
     int32_t strm2[MAX_STR][MAX_FSLOTS];  // 2*maxd[|s|] per edit slot (see the string filter)
 };
 
+// byte offset of a Rec field (the pre-vote's explicit shared-memory loads)
+#define RB_REC_OFF(field) ((uint32_t)(uintptr_t)(&((const Rec*)nullptr)->field))
+
 struct __align__(16) Tile {
     Rec r[TJ];
 };
@@ -764,6 +767,23 @@ static __device__ __forceinline__ int lds_s32(uint32_t addr) {
 static __device__ __forceinline__ int4 lds_s32x4(uint32_t addr) {
     int4 v;
     asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+// non-volatile forms for the read-only tile inside the pair loop: the
+// compiler may schedule and combine them freely
+static __device__ __forceinline__ int lds_ro(uint32_t addr) {
+    int v;
+    asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+static __device__ __forceinline__ uint2 lds_ro2(uint32_t addr) {
+    uint2 v;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+static __device__ __forceinline__ uint4 lds_ro4(uint32_t addr) {
+    uint4 v;
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
     return v;
 }
 static __device__ __forceinline__ int2 lds_s32x2(uint32_t addr) {
@@ -1026,6 +1046,11 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << (threadIdx.x & 31)) - 1u;
     const uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(tab);
+    // the tile's shared-memory address, made opaque to the compiler so the
+    // pre-vote's record address is one add per inner tuple (not the shared
+    // window base re-derived in uniform registers every iteration)
+    uint32_t rec_s;
+    asm volatile("mov.u32 %0, %1;" : "=r"(rec_s) : "r"((uint32_t)__cvta_generic_to_shared(&T.r[0])));
 #ifdef RB_SPEC
     // The specialised loop starts every pair from the constant rule set (or
     // the row's constant-test survivors): a row whose t side is missing or
@@ -1050,6 +1075,7 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
             // most warp iterations stop here after the compares, popcounts and
             // a few predicate ops; the rest re-run the tests and build the masks.
             bool anyw = false;
+            const uint32_t ra = rec_s + (uint32_t)jj * (uint32_t)sizeof(Rec);  // this inner tuple's record
 #pragma unroll
             for (int r = 0; r < ROWS; r++) {
 #if SPEC_PACKED
@@ -1061,7 +1087,8 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
 #pragma unroll
                 for (int f = 0; f < MAX_EQ; f++) {
                     peq[f] = true;
-                    if (f < RB_NEQ && !RB_EQ_STAGE2(f) && RB_EQ_KILL(f)) peq[f] = o[r].ocode[f] == T.r[jj].head[f];
+                    if (f < RB_NEQ && !RB_EQ_STAGE2(f) && RB_EQ_KILL(f))
+                        peq[f] = o[r].ocode[f] == lds_ro(ra + RB_REC_OFF(head) + 4u * f);
                 }
                 bool ptk[MAX_TOK][MAX_FSLOTS];
 #pragma unroll
@@ -1069,19 +1096,27 @@ __device__ __forceinline__ void tile_loop(const FilterPlan& F, const VerifyProg&
                     int u = 0;
                     uint32_t a = 0;
                     if (f < RB_NTOK && RB_TOK_NJ(f) > 0) {
-                        const uint4 is = T.r[jj].toksig[f];
+                        const uint32_t sa = ra + RB_REC_OFF(toksig) + 16u * f;
+                        uint4 is;
+                        if (RB_TOK_SIG64(f)) {
+                            const uint2 h2 = lds_ro2(sa);
+                            is = make_uint4(h2.x, h2.y, 0u, 0u);
+                        } else {
+                            is = lds_ro4(sa);
+                        }
                         u = RB_TOK_SIG64(f) ? __popc(o[r].lev[f][0] & is.x) + __popc(o[r].lev[f][1] & is.y) + o[r].orem[f]
                                             : __popc(o[r].lev[f][0] & is.x) + __popc(o[r].lev[f][1] & is.y) +
                                                   __popc(o[r].lev[f][2] & is.z) + __popc(o[r].lev[f][3] & is.w) +
                                                   o[r].orem[f];
-                        a = o[r].orow[f] + ((uint32_t)(T.r[jj].head[RB_NEQ + f] * RB_TOK_NJP(f)) << 2);
+                        a = o[r].orow[f] + ((uint32_t)(lds_ro(ra + RB_REC_OFF(head) + 4u * (RB_NEQ + f)) * RB_TOK_NJP(f)) << 2);
                     }
 #pragma unroll
                     for (int z = 0; z < MAX_FSLOTS; z++) {
                         ptk[f][z] = true;
                         if (f < RB_NTOK && z < RB_TOK_NS(f) && !RB_TOK_STAGE2(f, z) && RB_TOK_KILL(f, z))
                             ptk[f][z] = z < RB_TOK_NJ(f) ? u >= lds_s32(a + 4u * z)
-                                                         : T.r[jj].tokhash[f].x == o[r].ohash[f].x;
+                                                         : (uint32_t)lds_ro(ra + RB_REC_OFF(tokhash) + 8u * f) ==
+                                                               o[r].ohash[f].x;
                     }
                 }
                 bool any_r = false;
