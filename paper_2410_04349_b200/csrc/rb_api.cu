@@ -1561,7 +1561,9 @@ int run_impl(rb_ctx* c, rb_rel* rel, rb_prog* P, const int32_t* refs, int64_t to
             {
                 const double rate_now = done_items ? (double)done_surv / (double)done_items : P->surv_rate;
                 if (!sync_next && rate_now >= 0) {
-                    const long long expect = (long long)(rate_now * (double)(hi - lo) * 1.25) + 4096;
+                    const char* env_margin = std::getenv("RB_OPT_MARGIN");  // tests: 0 forces roll-backs
+                    const long long margin = env_margin ? std::max(0ll, std::atoll(env_margin)) : 4096;
+                    const long long expect = (long long)(rate_now * (double)(hi - lo) * 1.25) + margin;
                     opt = expect <= scap && (long long)base[1] + expect * per_row <= cap;
                 }
                 sync_next = false;

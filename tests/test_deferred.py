@@ -209,3 +209,39 @@ def test_repeated_run_replays_the_ranges_that_fit(monkeypatch):
     assert rows1 == sorted(zip(t2.tolist(), s2.tolist(), r2.tolist())) and len(rows1) > 100
     assert st1.retries > 0 and st2.retries == 0 and st2.launches < st1.launches
     assert st1.comparisons == st2.comparisons == len(rel) * (len(rel) - 1) // 2
+
+
+@pytest.mark.gpu
+def test_optimistic_range_overflow_rolls_back(monkeypatch):
+    """A range queued optimistically (pair + verify with one host wait, on the
+    survivor rate of the program's previous run) that overflows the survivor
+    buffer is rolled back and re-run through the checked path: same rows as a
+    fresh program, at least one retry."""
+    import numpy as np
+
+    from paper_2410_04349_b200._lib import RB_SYMMETRIC
+    from paper_2410_04349_b200.encode import RelationEncoding
+    from paper_2410_04349_b200.engine import PathProgram
+
+    monkeypatch.delenv("RB_JIT", raising=False)
+    rel, path, _ = goldens.load("citation")
+    enc = RelationEncoding(rel).prepare(path.predicate_table)
+    fresh = PathProgram(path, enc, device=0)
+    (t0, s0, r0), st0 = fresh.run_raw(None, len(rel), RB_SYMMETRIC)
+    want = sorted(zip(t0.tolist(), s0.tolist(), r0.tolist()))
+    assert st0.survivors > 8 and len(want) > 100
+
+    monkeypatch.setenv("RB_SURV_MIN", "8")
+    monkeypatch.setenv("RB_SURV_LIMIT", "8")  # the range sizing cannot grow the buffer ahead
+    monkeypatch.setenv("RB_OPT_MARGIN", "0")
+    prog = PathProgram(path, enc, device=0)
+    # a run without survivors teaches the program a zero survivor rate ...
+    for k in range(1, len(rel)):
+        _, st1 = prog.run_raw(np.array([0, k], dtype=np.int32), 2, RB_SYMMETRIC)
+        if st1.survivors == 0:
+            break
+    assert st1.survivors == 0
+    # ... so the whole relation's first range is queued optimistically and overflows
+    (t2, s2, r2), st2 = prog.run_raw(None, len(rel), RB_SYMMETRIC)
+    assert sorted(zip(t2.tolist(), s2.tolist(), r2.tolist())) == want
+    assert st2.retries >= 1 and st2.comparisons == st0.comparisons
